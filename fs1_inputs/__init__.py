@@ -1,0 +1,195 @@
+"""Seeded synthetic inputs for the five BASELINE.json configurations.
+
+This module is shared by the oracle side (tests, golden scripts) and the CUDA
+side (tests, bench).  It holds NO arithmetic of the method (no kernel, no
+Sinkhorn step, no cost): it only draws histograms, following the recipe of
+SURVEY.md §8(d) "Synthetic inputs" (recorded again in DESIGN.md §3).
+
+Every pair p of config c draws from its own stream
+``Generator(PCG64(SeedSequence(seed_c, spawn_key=(p,))))`` with
+``seed_c = 22021004200 + c``; a is drawn before b.  Per-pair streams make the
+inputs independent of batch slicing and of the number of ranks.
+
+Grid: every axis is [0, 1] with spacing h = 1/n and cell centres
+x_i = (i + 1/2) h (reading R12).
+"""
+from __future__ import annotations
+
+import dataclasses
+import math
+
+import numpy as np
+
+SEED_BASE = 22021004200
+
+
+@dataclasses.dataclass(frozen=True)
+class Config:
+    name: str
+    ndim: int
+    n: int            # points along axis 1
+    m: int            # points along axis 2 (1 in 1D)
+    batch: int
+    dtype: str        # "f64" | "f32"
+    domain: str       # "scaling" | "log"
+    eps: float
+    itr_max: int
+    tol: float
+    input_is_log: bool
+    description: str
+
+    @property
+    def size(self) -> int:
+        return self.n * self.m
+
+    @property
+    def h1(self) -> float:
+        return 1.0 / self.n
+
+    @property
+    def h2(self) -> float:
+        return 1.0 / self.m if self.ndim == 2 else 0.0
+
+    @property
+    def np_dtype(self):
+        return np.float64 if self.dtype == "f64" else np.float32
+
+
+CONFIGS = {
+    "c1": Config("c1", 1, 1000, 1, 1, "f64", "scaling", 1e-2, 2000, 1e-9, False,
+                 "1D N=1000 on [0,1], h=1/N, one pair fp64, 2-component Gaussian mixtures "
+                 "+1e-6 floor, eps=1e-2, 2000 iters or marginal L1 err <= 1e-9"),
+    "c2": Config("c2", 1, 1024, 1, 4096, "f32", "scaling", 5e-3, 500, 0.0, False,
+                 "batch 4096 pairs, 1D N=1024 fp32, Dirichlet(1) smoothed by width-5 box, "
+                 "eps=5e-3, 500 iters"),
+    "c3": Config("c3", 1, 1 << 24, 1, 1, "f64", "log", 1e-4, 1000, 0.0, True,
+                 "one pair 1D N=2^24 fp64 log domain, mixtures of 8 Gaussians (std 1e-3..1e-2), "
+                 "eps=1e-4, 1000 iters"),
+    "c4": Config("c4", 2, 2048, 2048, 1, "f32", "log", 1e-3, 300, 0.0, True,
+                 "2D 2048x2048 l1 cost, fp32 log domain, sums of 16 anisotropic Gaussians, "
+                 "eps=1e-3, 300 iters"),
+    "c5": Config("c5", 1, 4096, 1, 65536, "f32", "log", 1e-3, 1000, 0.0, False,
+                 "batch 65536 pairs (8192 per GPU at 8 GPUs), 1D N=4096 fp32 log domain, "
+                 "lognormal(0,1) bin weights, eps=1e-3, 1000 iters"),
+}
+
+
+def pair_rng(cfg_index: int, pair: int) -> np.random.Generator:
+    return np.random.Generator(np.random.PCG64(np.random.SeedSequence(SEED_BASE + cfg_index,
+                                                                       spawn_key=(pair,))))
+
+
+def centres(n: int) -> np.ndarray:
+    return (np.arange(n, dtype=np.float64) + 0.5) / n
+
+
+def _logsumexp(x: np.ndarray, axis=None) -> np.ndarray:
+    mx = np.max(x, axis=axis, keepdims=True)
+    out = mx + np.log(np.sum(np.exp(x - mx), axis=axis, keepdims=True))
+    return np.squeeze(out, axis=axis) if axis is not None else out.reshape(())
+
+
+# ---------------------------------------------------------------- per-config draws
+def _c1_hist(rng, n):
+    x = centres(n)
+    mu = rng.uniform(0.2, 0.8, size=2)
+    sd = rng.uniform(0.05, 0.1, size=2)
+    p = np.zeros(n)
+    for k in range(2):
+        p += np.exp(-0.5 * ((x - mu[k]) / sd[k]) ** 2) / (sd[k] * math.sqrt(2 * math.pi))
+    p /= p.sum()
+    p += 1e-6
+    return p / p.sum()
+
+
+def _c2_hist(rng, n):
+    w = rng.exponential(1.0, size=n)          # Dirichlet(1) = iid Exp(1), normalised
+    w /= w.sum()
+    # width-5 box filter as a truncated-window mean (edges average the in-range cells)
+    c = np.concatenate([[0.0], np.cumsum(w)])
+    lo = np.clip(np.arange(n) - 2, 0, n)
+    hi = np.clip(np.arange(n) + 3, 0, n)
+    s = (c[hi] - c[lo]) / (hi - lo)
+    return s / s.sum()
+
+
+def _c3_loghist(rng, n):
+    x = centres(n)
+    mu = rng.uniform(0.0, 1.0, size=8)
+    sd = rng.uniform(1e-3, 1e-2, size=8)
+    comps = np.empty((8, n))
+    for k in range(8):
+        comps[k] = -0.5 * ((x - mu[k]) / sd[k]) ** 2 - math.log(sd[k])
+    la = _logsumexp(comps, axis=0)
+    return la - _logsumexp(la)
+
+
+def _c4_loghist(rng, n, m):
+    # column-major flattening: flat index j*n + i, i along axis 1 (h1), j along axis 2 (h2)
+    xi = centres(n)[:, None]
+    yj = centres(m)[None, :]
+    cx = rng.uniform(0.1, 0.9, size=16)
+    cy = rng.uniform(0.1, 0.9, size=16)
+    s1 = rng.uniform(0.01, 0.1, size=16)
+    s2 = rng.uniform(0.01, 0.1, size=16)
+    th = rng.uniform(0.0, math.pi, size=16)
+    acc = np.full((n, m), -np.inf)
+    for k in range(16):
+        dx, dy = xi - cx[k], yj - cy[k]
+        u = math.cos(th[k]) * dx + math.sin(th[k]) * dy
+        v = -math.sin(th[k]) * dx + math.cos(th[k]) * dy
+        comp = -0.5 * ((u / s1[k]) ** 2 + (v / s2[k]) ** 2) - math.log(s1[k] * s2[k])
+        acc = np.logaddexp(acc, comp)
+    la = acc - _logsumexp(acc.ravel())
+    return la.ravel(order="F")
+
+
+def _c5_hist(rng, n):
+    w = rng.lognormal(0.0, 1.0, size=n)
+    return w / w.sum()
+
+
+_DRAW = {
+    "c1": lambda rng, cfg: _c1_hist(rng, cfg.n),
+    "c2": lambda rng, cfg: _c2_hist(rng, cfg.n),
+    "c3": lambda rng, cfg: _c3_loghist(rng, cfg.n),
+    "c4": lambda rng, cfg: _c4_loghist(rng, cfg.n, cfg.m),
+    "c5": lambda rng, cfg: _c5_hist(rng, cfg.n),
+}
+
+
+def pair(cfg: Config | str, p: int, n: int | None = None):
+    """(a, b) for pair p in fp64 before any cast.  Log-weights when cfg.input_is_log.
+
+    ``n`` overrides the grid size (smaller parity cases with the same recipe)."""
+    if isinstance(cfg, str):
+        cfg = CONFIGS[cfg]
+    if n is not None and n != cfg.n:
+        cfg = dataclasses.replace(cfg, n=n, m=(n if cfg.ndim == 2 else 1))
+    idx = int(cfg.name[1:])
+    rng = pair_rng(idx, p)
+    a = _DRAW[cfg.name](rng, cfg)
+    b = _DRAW[cfg.name](rng, cfg)
+    return a, b
+
+
+def batch(cfg: Config | str, pairs, n: int | None = None):
+    """Arrays [len(pairs)][size] in the config dtype (the values both sides consume)."""
+    if isinstance(cfg, str):
+        cfg = CONFIGS[cfg]
+    A, B = [], []
+    for p in pairs:
+        a, b = pair(cfg, p, n)
+        A.append(a)
+        B.append(b)
+    A = np.stack(A).astype(cfg.np_dtype)
+    B = np.stack(B).astype(cfg.np_dtype)
+    return A, B
+
+
+def random_positive(rng: np.random.Generator, shape, lo=0.05, hi=1.0, normalise=True):
+    """Generic strictly positive histograms for small edge-case tests."""
+    x = rng.uniform(lo, hi, size=shape)
+    if normalise:
+        x = x / x.sum(axis=-1, keepdims=True)
+    return x

@@ -1,0 +1,118 @@
+/* FS-1 ORACLE — TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
+ *
+ * The paper's O(N) kernel apply written out literally, in plain sequential C,
+ * fp64.  Used by the oracle where the dense O(N^2) apply is infeasible
+ * (N = 2^24, 2048 x 2048).  Validated against the dense apply in
+ * tests/test_oracle_apply.py wherever both run.
+ *
+ *  fs1o_sweep_scaling : Eq. (recursion), i.e. Algorithm 1
+ *                       lines 3-6:
+ *                         r_1 = x_1, r_{i+1} = lam r_i + x_{i+1}
+ *                         s_N = 0,   s_{N-i} = lam (s_{N-i+1} + x_{N-i+1})
+ *                         y = r + s
+ *  fs1o_sweep_log     : the same two sweeps in log-sum-exp form
+ *                       (BASELINE.json north_star), c = h/eps:
+ *                         R_1 = X_1, R_{i+1} = logaddexp(R_i - c, X_{i+1})
+ *                         S_N = -inf, S_{N-i} = -c + logaddexp(S_{N-i+1}, X_{N-i+1})
+ *                         Y = logaddexp(R, S)
+ *  fs1o_wsweep_log    : log of the distance-weighted apply whose bilinear form
+ *                       is Algorithm 1's return line:
+ *                       (W x)_k = sum_j |k-j| h lam^{|k-j|} x_j, from
+ *                         P'_1 = 0, P'_{k+1} = lam (P'_k + p_k)   (p = inclusive forward sum)
+ *                         Q'_N = 0, Q'_k = lam (Q'_{k+1} + t_{k+1}) (t = inclusive backward sum)
+ *                       (W x)_k = h (P'_k + Q'_k).  SURVEY.md §8(c) Q7 / DESIGN.md R7.
+ *
+ * Every routine works on `lines` independent lines of `n` points with element
+ * stride `stride` and line stride `lstride` (2D: axis 1 = columns, contiguous;
+ * axis 2 = rows, stride N; PAPER.md:244-255 column-major flattening).
+ * Lines are independent (PAPER.md:282-312 applies K0 column by column), so the
+ * loop over lines may run in parallel; arithmetic within a line is sequential.
+ */
+#include <math.h>
+#include <stdlib.h>
+
+static double lae(double a, double b) {           /* log(e^a + e^b) */
+  if (a == -INFINITY) return b;
+  if (b == -INFINITY) return a;
+  double m = a > b ? a : b;
+  return m + log1p(exp(-fabs(a - b)));
+}
+
+void fs1o_sweep_scaling(const double* x, long n, long stride, long lines, long lstride,
+                        double lam, double* y) {
+#pragma omp parallel for schedule(static)
+  for (long l = 0; l < lines; ++l) {
+    const double* xl = x + l * lstride;
+    double* yl = y + l * lstride;
+    double* r = (double*)malloc(sizeof(double) * n);
+    double* s = (double*)malloc(sizeof(double) * n);
+    r[0] = xl[0];
+    s[n - 1] = 0.0;
+    for (long i = 1; i <= n - 1; ++i) {              /* for i = 1 : N-1 (1-based) */
+      r[i] = lam * r[i - 1] + xl[i * stride];        /* r_{i+1} = lam r_i + x_{i+1} */
+      long k = n - 1 - i;                            /* 0-based index of s_{N-i}    */
+      s[k] = lam * (s[k + 1] + xl[(k + 1) * stride]);/* s_{N-i} = lam(s_{N-i+1}+x_{N-i+1}) */
+    }
+    for (long i = 0; i < n; ++i) yl[i * stride] = r[i] + s[i];
+    free(r);
+    free(s);
+  }
+}
+
+void fs1o_sweep_log(const double* X, long n, long stride, long lines, long lstride,
+                    double c, double* Y) {
+#pragma omp parallel for schedule(static)
+  for (long l = 0; l < lines; ++l) {
+    const double* xl = X + l * lstride;
+    double* yl = Y + l * lstride;
+    double* r = (double*)malloc(sizeof(double) * n);
+    double* s = (double*)malloc(sizeof(double) * n);
+    r[0] = xl[0];
+    s[n - 1] = -INFINITY;
+    for (long i = 1; i <= n - 1; ++i) {
+      r[i] = lae(r[i - 1] - c, xl[i * stride]);
+      long k = n - 1 - i;
+      s[k] = -c + lae(s[k + 1], xl[(k + 1) * stride]);
+    }
+    for (long i = 0; i < n; ++i) yl[i * stride] = lae(r[i], s[i]);
+    free(r);
+    free(s);
+  }
+}
+
+void fs1o_wsweep_log(const double* X, long n, long stride, long lines, long lstride,
+                     double c, double h, double* Y) {
+#pragma omp parallel for schedule(static)
+  for (long l = 0; l < lines; ++l) {
+    const double* xl = X + l * lstride;
+    double* yl = Y + l * lstride;
+    double* p = (double*)malloc(sizeof(double) * n);   /* log inclusive forward sums  */
+    double* t = (double*)malloc(sizeof(double) * n);   /* log inclusive backward sums */
+    double* P = (double*)malloc(sizeof(double) * n);   /* log P'                       */
+    double* Q = (double*)malloc(sizeof(double) * n);   /* log Q'                       */
+    p[0] = xl[0];
+    for (long i = 1; i < n; ++i) p[i] = lae(p[i - 1] - c, xl[i * stride]);
+    t[n - 1] = xl[(n - 1) * stride];
+    for (long i = n - 2; i >= 0; --i) t[i] = lae(t[i + 1] - c, xl[i * stride]);
+    P[0] = -INFINITY;
+    for (long i = 1; i < n; ++i) P[i] = -c + lae(P[i - 1], p[i - 1]);
+    Q[n - 1] = -INFINITY;
+    for (long i = n - 2; i >= 0; --i) Q[i] = -c + lae(Q[i + 1], t[i + 1]);
+    double lh = log(h);
+    for (long i = 0; i < n; ++i) yl[i * stride] = lh + lae(P[i], Q[i]);
+    free(p);
+    free(t);
+    free(P);
+    free(Q);
+  }
+}
+
+/* sum_k exp(A_k + B_k) over n entries, in fp64 (cost and error reductions). */
+double fs1o_sum_exp2(const double* A, const double* B, long n) {
+  double s = 0.0;
+  for (long i = 0; i < n; ++i) {
+    double v = A[i] + B[i];
+    if (v != -INFINITY) s += exp(v);
+  }
+  return s;
+}
