@@ -1,0 +1,160 @@
+/* fs1.h — C ABI of the B200-native FS-1 hot path (libfs1.so).
+ *
+ * FS-1 (Liao, Chen, Wang, Bai, Jin, Wu; arXiv 2202.10042) solves the
+ * entropy-regularised Wasserstein-1 problem on a uniform grid,
+ *
+ *   min_gamma  sum_ij gamma_ij |i-j| h + eps gamma_ij ln gamma_ij       PAPER.md:69-75, Eq. (2.3)
+ *   s.t. sum_j gamma_ij = a_i, sum_i gamma_ij = b_j,
+ *
+ * by Sinkhorn's iteration gamma = diag(phi) K diag(psi), K_ij = lambda^{|i-j|},
+ * lambda = e^{-h/eps}
+ *
+ *   psi <- b ./ (K^T phi),   phi <- a ./ (K psi)          (psi first)
+ *
+ * where every K x is evaluated in O(N) by a forward and a backward
+ * first-order recursion (Eq. "recursion"; Algorithm 1,
+ * PAPER.md:141-165).  In 2D (Algorithm 2) the kernel is the
+ * block-Toeplitz K = T_M(lambda2) (x) T_N(lambda1) and the cost is
+ * |i1-i2| h1 + |j1-j2| h2.
+ *
+ * Notation map: the paper's histograms u, v are this ABI's
+ * a, b; the paper's scalings phi, psi are this ABI's u, v.
+ *
+ * Conventions common to every entry point
+ *  - Every data pointer is a DEVICE pointer owned by the caller; the library
+ *    never allocates, frees or synchronises inside fs1_solve / fs1_cost /
+ *    fs1_apply; every call is asynchronous on `stream` (a cudaStream_t,
+ *    passed as void*, NULL = legacy default stream).
+ *  - Batched layout: `batch` independent problems, each `n*m` contiguous
+ *    values of the plan's dtype, problem-major: x[p*(n*m) + k].
+ *    2D arrays are flattened column-major, k = j*n + i, i along axis 1 (h1),
+ *    j along axis 2 (h2)
+ *  - Call-level errors are returned synchronously before any launch (only
+ *    argument, shape and support problems are detected; data is not
+ *    validated).  Per-problem outcomes go to device arrays.
+ *  - The library holds no global mutable state; a plan is immutable after
+ *    fs1_plan and may be shared by threads and streams; concurrent calls
+ *    need distinct workspaces.
+ */
+#ifndef FS1_H
+#define FS1_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FS1_ABI_VERSION 1
+
+typedef enum {
+  FS1_OK = 0,
+  FS1_ERR_ARG = 1,          /* NULL pointer, batch < 1, n < 1, m < 1, itr_max < 0, tol < 0, ... */
+  FS1_ERR_EPS = 2,          /* eps <= 0 or h <= 0 or non-finite (SPEC's NonPositiveEpsilon)     */
+  FS1_ERR_UNSUPPORTED = 3,  /* dtype / domain / size combination with no kernel                 */
+  FS1_ERR_CUDA = 4,         /* a CUDA runtime error (launch failure, no device, ...)           */
+  FS1_ERR_WORKSPACE = 5     /* workspace NULL or misaligned while the plan needs one           */
+} fs1_status;
+
+typedef enum { FS1_F32 = 0, FS1_F64 = 1 } fs1_dtype;
+
+/* FS1_SCALING: u, v hold phi, psi; the plain (unstabilised) iteration of
+ *              Algorithm 1; overflow terminates the problem (NONFINITE),
+ *              as the paper's unstabilised runs do.
+ * FS1_LOG:     u, v hold F = log phi, G = log psi.  Internally the kernels
+ *              keep phi, psi as mantissas with one binary exponent per chunk
+ *              of consecutive grid points, i.e. the absorption of Remark 2.1
+ *              / Remark 3.2 carried out every
+ *              half-step in exact powers of two.  It never
+ *              overflows and matches the log-sum-exp iteration of the
+ *              north star to rounding.                                         */
+typedef enum { FS1_SCALING = 0, FS1_LOG = 1 } fs1_domain;
+
+/* per-problem flags (bit set) */
+#define FS1_FLAG_CONVERGED 1  /* stopped because err <= tol (tol > 0)               */
+#define FS1_FLAG_NONFINITE 2  /* phi or psi became non-finite ("terminates abnormally") */
+#define FS1_FLAG_ITR_MAX 4    /* stopped at itr_max                                  */
+
+typedef struct {
+  int32_t ndim;          /* 1 or 2                                                            */
+  int64_t n;             /* points along axis 1 (>= 1)                                         */
+  int64_t m;             /* points along axis 2 (1 for ndim == 1)                             */
+  double h1, h2;         /* grid spacings (> 0); h2 ignored when ndim == 1                   */
+  double eps;            /* regularisation epsilon (> 0)                                      */
+  int64_t batch;         /* number of independent problems (>= 1)                             */
+  fs1_dtype dtype;       /* element type of a, b, u, v                                        */
+  fs1_domain domain;     /* see above                                                         */
+  int32_t input_is_log;  /* FS1_LOG only: a, b hold log-weights (may be -inf)                */
+  int32_t itr_max;       /* iteration cap (>= 0)                                              */
+  double tol;            /* >= 0; stop when the marginal error <= tol;
+                            0 = fixed iterations (the paper's §5 protocol)     */
+  int32_t check_interval;/* >= 1: the error is evaluated when l % check_interval == 0       */
+  int32_t warm_start;    /* 1: u, v hold the initial phi, psi (LOG: F, G); 0: 1/(n m)        */
+} fs1_desc;
+
+typedef struct fs1_plan_s fs1_plan_t;
+
+typedef struct {
+  char kernel[48];       /* name of the kernel family chosen                                  */
+  int32_t chunk;         /* grid points per thread (E)                                        */
+  int32_t threads;       /* threads per CTA                                                   */
+  int32_t ctas_per_problem;
+  int64_t grid;          /* CTAs launched by fs1_solve                                        */
+  size_t smem_bytes;     /* dynamic shared memory per CTA                                     */
+  size_t workspace_bytes;
+} fs1_plan_info_t;
+
+/* fs1_plan — validate `desc`, choose a kernel, size the workspace.
+ *   desc      : problem description (copied).
+ *   device    : CUDA device ordinal the plan will run on.
+ *   out       : receives the plan (free with fs1_plan_destroy).
+ *   workspace_bytes : receives the device workspace fs1_solve / fs1_cost need
+ *               (may be 0; pass a buffer of at least this size, 256-byte aligned).
+ * Kernel choice: n*m up to FS1_MAX_PERSIST points per problem ->
+ * the persistent one-CTA-per-problem kernel; larger 1D problems -> the
+ * multi-CTA HBM-streaming scan kernel; 2D -> the separable kernel.
+ * Returns FS1_ERR_ARG / FS1_ERR_EPS / FS1_ERR_UNSUPPORTED / FS1_ERR_CUDA.    */
+fs1_status fs1_plan(const fs1_desc* desc, int device, fs1_plan_t** out, size_t* workspace_bytes);
+
+/* fs1_solve — run Algorithm 1 (ndim 1) or Algorithm 2 (ndim 2) on every problem.
+ *   a, b   : [batch][n*m] source / target histograms (paper's u, v), dtype of the plan;
+ *            linear weights (> 0 in the scaling domain), or log-weights when
+ *            desc.input_is_log (LOG domain).  Read only.
+ *   u, v   : [batch][n*m] out (in, if warm_start): SCALING -> phi, psi;
+ *            LOG -> F = log phi, G = log psi.  On return they hold the state
+ *            (phi^(l), psi^(l)) at which the loop stopped.
+ *   iters  : [batch] int32, l at exit (number of completed iterations).
+ *   err    : [batch] fp64, sum_i |psi_i (K^T phi)_i - b_i| evaluated on the exit
+ *            state (PAPER.md:148 and §5's termination rule).
+ *   flags  : [batch] int32, FS1_FLAG_* bits.
+ *   cost   : [batch] fp64 or NULL; the return line
+ *            sum_ij phi_i psi_j lambda^{|i-j|} |i-j| h (2D :339),
+ *            evaluated in O(N) on the exit state.
+ *   workspace : device buffer of fs1_plan's size (may be NULL if that size is 0).
+ *   stream : cudaStream_t.
+ * Problems are independent; a NONFINITE problem stops alone.                    */
+fs1_status fs1_solve(const fs1_plan_t* plan, const void* a, const void* b, void* u, void* v,
+                     int32_t* iters, double* err, int32_t* flags, double* cost,
+                     void* workspace, void* stream);
+
+/* fs1_cost — the return line alone, on caller-given u, v (same layout and
+ * domain as fs1_solve's outputs).  cost: [batch] fp64.                          */
+fs1_status fs1_cost(const fs1_plan_t* plan, const void* u, const void* v, double* cost,
+                    void* workspace, void* stream);
+
+/* fs1_apply — y = K x for each of the batch vectors (Eq. 3.1 / Eq. 4.x evaluated by
+ * the recursion of PAPER.md:129-137 / 2D :300-309).  SCALING: x, y linear;
+ * LOG: x, y are logs (y = log K e^x).  The kernel-level entry point used by the
+ * parity tests.  x, y: [batch][n*m], must not alias.                             */
+fs1_status fs1_apply(const fs1_plan_t* plan, const void* x, void* y, void* workspace, void* stream);
+
+fs1_status fs1_plan_info(const fs1_plan_t* plan, fs1_plan_info_t* info);
+void fs1_plan_destroy(fs1_plan_t* plan);
+const char* fs1_status_string(fs1_status s);
+int fs1_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FS1_H */

@@ -1,0 +1,232 @@
+// fs1_api.cu — the C ABI of include/fs1.h: plan validation, kernel choice,
+// scan-multiplier tables and launches.  No device allocation, no synchronisation.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <mutex>
+#include <new>
+
+#include "../../include/fs1.h"
+#include "fs1_dispatch.h"
+#include "fs1_params.h"
+
+using namespace fs1;
+
+struct fs1_plan_s {
+  fs1_desc d;
+  int device;
+  int kind;  // 0 persistent
+  const PersistEntry* pe;
+  PersistParams base;  // multipliers + scalars; pointers filled per call
+  size_t ws;
+  fs1_plan_info_t info;
+};
+
+namespace {
+
+constexpr int KIND_PERSIST = 0;
+
+// lambda^L as (mantissa in [1,2), exponent), from log2(lambda^L) = -L c / ln 2 in long double.
+void er_pow(long double c, long double L, double* m, int* e) {
+  if (L == 0) {
+    *m = 1.0;
+    *e = 0;
+    return;
+  }
+  long double x = -L * c / logl(2.0L);
+  long double f = floorl(x);
+  *m = (double)exp2l(x - f);
+  *e = (int)f;
+  if (*m >= 2.0) { *m *= 0.5; *e += 1; }
+}
+
+double powl_d(long double c, long double L) { return (double)expl(-c * L); }
+
+void fill_persist_tables(PersistParams& P, double c, int E) {
+  const long double C = (long double)c;
+  for (int k = 0; k < 5; ++k) {
+    const long double L = (long double)E * (1 << k);
+    P.lvA[k] = powl_d(C, ceill(L / 2));
+    P.lvB[k] = powl_d(C, floorl(L / 2));
+    P.lvd[k] = powl_d(C, L);
+    er_pow(C, L, &P.lvm[k], &P.lve[k]);
+  }
+  er_pow(C, 32.0L * E, &P.lvm[5], &P.lve[5]);
+  P.wA = powl_d(C, 16.0L * E);
+  P.wB = powl_d(C, 16.0L * E);
+  for (int l = 0; l < 32; ++l) {
+    const long double L = (long double)E * l;
+    P.laneA[l] = powl_d(C, ceill(L / 2));
+    P.laneB[l] = powl_d(C, floorl(L / 2));
+    er_pow(C, L, &P.lanem[l], &P.lanee[l]);
+  }
+}
+
+std::mutex g_attr_mu;
+
+}  // namespace
+
+extern "C" {
+
+int fs1_abi_version(void) { return FS1_ABI_VERSION; }
+
+const char* fs1_status_string(fs1_status s) {
+  switch (s) {
+    case FS1_OK: return "FS1_OK";
+    case FS1_ERR_ARG: return "FS1_ERR_ARG: invalid argument";
+    case FS1_ERR_EPS: return "FS1_ERR_EPS: eps and h must be finite and > 0";
+    case FS1_ERR_UNSUPPORTED: return "FS1_ERR_UNSUPPORTED: no kernel for this dtype/domain/size";
+    case FS1_ERR_CUDA: return "FS1_ERR_CUDA: CUDA runtime error";
+    case FS1_ERR_WORKSPACE: return "FS1_ERR_WORKSPACE: workspace missing or misaligned";
+  }
+  return "FS1_?: unknown status";
+}
+
+fs1_status fs1_plan(const fs1_desc* desc, int device, fs1_plan_t** out, size_t* workspace_bytes) {
+  if (!desc || !out) return FS1_ERR_ARG;
+  *out = nullptr;
+  const fs1_desc& d = *desc;
+  if (d.ndim != 1 && d.ndim != 2) return FS1_ERR_ARG;
+  if (d.n < 1 || d.m < 1 || d.batch < 1 || d.itr_max < 0 || d.check_interval < 1) return FS1_ERR_ARG;
+  if (!(d.tol >= 0.0) || !isfinite(d.tol)) return FS1_ERR_ARG;
+  if (d.ndim == 1 && d.m != 1) return FS1_ERR_ARG;
+  if (d.dtype != FS1_F32 && d.dtype != FS1_F64) return FS1_ERR_ARG;
+  if (d.domain != FS1_SCALING && d.domain != FS1_LOG) return FS1_ERR_ARG;
+  if (!(d.eps > 0.0) || !isfinite(d.eps) || !(d.h1 > 0.0) || !isfinite(d.h1)) return FS1_ERR_EPS;
+  if (d.ndim == 2 && (!(d.h2 > 0.0) || !isfinite(d.h2))) return FS1_ERR_EPS;
+  if (d.batch > 0x7fffffffLL) return FS1_ERR_UNSUPPORTED;
+
+  fs1_plan_s* p = new (std::nothrow) fs1_plan_s();
+  if (!p) return FS1_ERR_ARG;
+  p->d = d;
+  p->device = device;
+  const bool logd = d.domain == FS1_LOG;
+  const double c = d.h1 / d.eps;
+
+  if (d.ndim == 1) {
+    // persistent kernel: the smallest (E, W) instantiation whose 32 W E covers n
+    int cnt = 0;
+    const PersistEntry* tab = d.dtype == FS1_F32 ? persist_table_f32(&cnt) : persist_table_f64(&cnt);
+    const PersistEntry* best = nullptr;
+    for (int i = 0; i < cnt; ++i) {
+      const PersistEntry& e = tab[i];
+      if (e.logd != logd) continue;
+      const long long cap = 32LL * e.W * e.E;
+      if (cap < d.n) continue;
+      if (logd) {
+        // mantissa range per chunk and exactness of the fp64 warp scan
+        const double lim_chunk = d.dtype == FS1_F32 ? 40.0 : 300.0;
+        if (c * e.E > lim_chunk || c * e.E * 32.0 > 650.0) continue;
+      }
+      if (!best || cap < 32LL * best->W * best->E ||
+          (cap == 32LL * best->W * best->E && e.W < best->W))
+        best = &e;
+    }
+    if (!best) {
+      delete p;
+      return FS1_ERR_UNSUPPORTED;
+    }
+    p->kind = KIND_PERSIST;
+    p->pe = best;
+    memset(&p->base, 0, sizeof(p->base));
+    p->base.n = d.n;
+    p->base.batch = d.batch;
+    p->base.lam = exp(-c);
+    p->base.h = d.h1;
+    p->base.tol = d.tol;
+    p->base.itr_max = d.itr_max;
+    p->base.check_interval = d.check_interval;
+    p->base.warm = d.warm_start;
+    p->base.input_is_log = logd ? d.input_is_log : 0;
+    p->base.write_uv = 1;
+    fill_persist_tables(p->base, c, best->E);
+    {
+      std::lock_guard<std::mutex> lk(g_attr_mu);
+      int cur = 0;
+      if (cudaGetDevice(&cur) != cudaSuccess) { delete p; return FS1_ERR_CUDA; }
+      if (cur != device && cudaSetDevice(device) != cudaSuccess) { delete p; return FS1_ERR_CUDA; }
+      cudaError_t e1 = cudaFuncSetAttribute(best->solve_fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)best->smem);
+      cudaError_t e2 = cudaFuncSetAttribute(best->apply_fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)best->smem);
+      if (cur != device) cudaSetDevice(cur);
+      if (e1 != cudaSuccess || e2 != cudaSuccess) {
+        delete p;
+        return FS1_ERR_CUDA;
+      }
+    }
+    p->ws = 0;
+    snprintf(p->info.kernel, sizeof(p->info.kernel), "persist_%s_%s_E%d_W%d",
+             d.dtype == FS1_F32 ? "f32" : "f64", logd ? "log" : "scaling", best->E, best->W);
+    p->info.chunk = best->E;
+    p->info.threads = 32 * best->W;
+    p->info.ctas_per_problem = 1;
+    p->info.grid = d.batch;
+    p->info.smem_bytes = best->smem;
+    p->info.workspace_bytes = 0;
+  } else {
+    delete p;
+    return FS1_ERR_UNSUPPORTED;
+  }
+  if (workspace_bytes) *workspace_bytes = p->ws;
+  *out = p;
+  return FS1_OK;
+}
+
+fs1_status fs1_plan_info(const fs1_plan_t* plan, fs1_plan_info_t* info) {
+  if (!plan || !info) return FS1_ERR_ARG;
+  *info = plan->info;
+  return FS1_OK;
+}
+
+void fs1_plan_destroy(fs1_plan_t* plan) { delete plan; }
+
+fs1_status fs1_solve(const fs1_plan_t* plan, const void* a, const void* b, void* u, void* v,
+                     int32_t* iters, double* err, int32_t* flags, double* cost, void* workspace,
+                     void* stream) {
+  if (!plan || !a || !b || !u || !v) return FS1_ERR_ARG;
+  if (plan->ws && (!workspace || ((uintptr_t)workspace & 255))) return FS1_ERR_WORKSPACE;
+  if (plan->kind == KIND_PERSIST) {
+    PersistParams P = plan->base;
+    P.a = a; P.b = b; P.u = u; P.v = v;
+    P.iters = iters; P.err = err; P.flags = flags; P.cost = cost;
+    cudaError_t e = plan->pe->launch_solve(P, plan->d.batch, (cudaStream_t)stream);
+    return e == cudaSuccess ? FS1_OK : FS1_ERR_CUDA;
+  }
+  return FS1_ERR_UNSUPPORTED;
+}
+
+fs1_status fs1_cost(const fs1_plan_t* plan, const void* u, const void* v, double* cost,
+                    void* workspace, void* stream) {
+  if (!plan || !u || !v || !cost) return FS1_ERR_ARG;
+  if (plan->ws && (!workspace || ((uintptr_t)workspace & 255))) return FS1_ERR_WORKSPACE;
+  if (plan->kind == KIND_PERSIST) {
+    // The loop top with l = itr_max = 0 on the given state: evaluates err and the
+    // return line, leaves u, v untouched.  a = b = u (never read for the cost).
+    PersistParams P = plan->base;
+    P.itr_max = 0;
+    P.tol = 0.0;
+    P.warm = 1;
+    P.write_uv = 0;
+    P.input_is_log = plan->d.domain == FS1_LOG;
+    P.a = u; P.b = v; P.u = const_cast<void*>(u); P.v = const_cast<void*>(v);
+    P.iters = nullptr; P.err = nullptr; P.flags = nullptr; P.cost = cost;
+    cudaError_t e = plan->pe->launch_solve(P, plan->d.batch, (cudaStream_t)stream);
+    return e == cudaSuccess ? FS1_OK : FS1_ERR_CUDA;
+  }
+  return FS1_ERR_UNSUPPORTED;
+}
+
+fs1_status fs1_apply(const fs1_plan_t* plan, const void* x, void* y, void* workspace, void* stream) {
+  if (!plan || !x || !y || x == y) return FS1_ERR_ARG;
+  if (plan->ws && (!workspace || ((uintptr_t)workspace & 255))) return FS1_ERR_WORKSPACE;
+  if (plan->kind == KIND_PERSIST) {
+    cudaError_t e = plan->pe->launch_apply(plan->base, x, y, plan->d.batch, (cudaStream_t)stream);
+    return e == cudaSuccess ? FS1_OK : FS1_ERR_CUDA;
+  }
+  return FS1_ERR_UNSUPPORTED;
+}
+
+}  // extern "C"

@@ -1,0 +1,133 @@
+// fs1_common.cuh — device helpers shared by the FS-1 kernels (sm_100a).
+//
+// * Tr<T>      : per-dtype bit tricks (exact powers of two, exponent extraction,
+//                reciprocal) used by the chunk-exponent ("extended range")
+//                representation of the log domain.
+// * ER<T>      : extended-range number m * 2^e, m in [1,2) or 0.  It carries the
+//                scan carries between chunks of the log-domain kernels so that a
+//                carry lambda^L * x never underflows in isolation (Remark 3.3,
+//                "stepwise multiplication of lambda").
+// * warp/block reductions (deterministic trees, no float atomics).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace fs1 {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int ZE = -(1 << 28);  // exponent of an ER zero
+
+template <class T> struct Tr;
+
+template <> struct Tr<float> {
+  using V = float4;
+  static constexpr int VEC = 4;
+  static constexpr int LIM = 60;  // carries up to 2^LIM above a chunk stay in the fast path
+  __device__ __forceinline__ static float pow2(int d) {  // exact 2^d, 0 below 2^-126
+    d = min(d, 127);
+    return d >= -126 ? __uint_as_float((unsigned)(d + 127) << 23) : 0.f;
+  }
+  __device__ __forceinline__ static int expo(float m) {  // unbiased exponent of a normal m
+    return (int)((__float_as_uint(m) >> 23) & 0xffu) - 127;
+  }
+  __device__ __forceinline__ static float mant(float m) {  // m with exponent 0 -> [1,2)
+    return __uint_as_float((__float_as_uint(m) & 0x807fffffu) | 0x3f800000u);
+  }
+  __device__ __forceinline__ static float rcp(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+  }
+  __device__ __forceinline__ static void unpack(const V& v, float* o) {
+    o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+  }
+  __device__ __forceinline__ static V pack(const float* o) { return make_float4(o[0], o[1], o[2], o[3]); }
+};
+
+template <> struct Tr<double> {
+  using V = double2;
+  static constexpr int VEC = 2;
+  static constexpr int LIM = 600;
+  __device__ __forceinline__ static double pow2(int d) {
+    d = min(d, 1023);
+    return d >= -1022 ? __longlong_as_double((long long)(d + 1023) << 52) : 0.0;
+  }
+  __device__ __forceinline__ static int expo(double m) {
+    return (int)((__double_as_longlong(m) >> 52) & 0x7ff) - 1023;
+  }
+  __device__ __forceinline__ static double mant(double m) {
+    return __longlong_as_double((__double_as_longlong(m) & 0x800fffffffffffffLL) |
+                                0x3ff0000000000000LL);
+  }
+  __device__ __forceinline__ static double rcp(double x) { return __drcp_rn(x); }
+  __device__ __forceinline__ static void unpack(const V& v, double* o) { o[0] = v.x; o[1] = v.y; }
+  __device__ __forceinline__ static V pack(const double* o) { return make_double2(o[0], o[1]); }
+};
+
+__device__ __forceinline__ double pow2d(int d) { return Tr<double>::pow2(d); }
+
+template <class T> struct ER {
+  T m;
+  int e;
+};
+
+template <class T> __device__ __forceinline__ ER<T> er_zero() { return ER<T>{T(0), ZE}; }
+
+// normalise m * 2^e (m >= 0 finite, normal or zero)
+template <class T> __device__ __forceinline__ ER<T> er_norm(T m, int e) {
+  ER<T> r;
+  bool z = !(m > T(0));
+  r.m = z ? T(0) : Tr<T>::mant(m);
+  r.e = z ? ZE : e + Tr<T>::expo(m);
+  return r;
+}
+
+template <class T> __device__ __forceinline__ ER<T> er_add(ER<T> a, ER<T> b) {
+  int e = max(a.e, b.e);
+  T m = a.m * Tr<T>::pow2(a.e - e) + b.m * Tr<T>::pow2(b.e - e);
+  return er_norm<T>(m, e);
+}
+
+template <class T> __device__ __forceinline__ ER<T> er_mul(ER<T> a, ER<T> b) {
+  return er_norm<T>(a.m * b.m, a.e + b.e);
+}
+
+template <class T> __device__ __forceinline__ ER<T> er_scale(ER<T> a, T s) {  // s > 0 plain
+  return er_norm<T>(a.m * s, a.e);
+}
+
+// value relative to 2^R as double (flushes below 2^-1022)
+template <class T> __device__ __forceinline__ double er_rel(ER<T> a, int R) {
+  return (double)a.m * pow2d(a.e - R);
+}
+
+template <class T> __device__ __forceinline__ ER<T> shfl_up_er(ER<T> a, int d) {
+  ER<T> r;
+  r.m = __shfl_up_sync(FULL, a.m, d);
+  r.e = __shfl_up_sync(FULL, a.e, d);
+  return r;
+}
+template <class T> __device__ __forceinline__ ER<T> shfl_down_er(ER<T> a, int d) {
+  ER<T> r;
+  r.m = __shfl_down_sync(FULL, a.m, d);
+  r.e = __shfl_down_sync(FULL, a.e, d);
+  return r;
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  return v;
+}
+__device__ __forceinline__ int warp_max(int v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(FULL, v, o));
+  return v;
+}
+__device__ __forceinline__ int warp_min(int v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(FULL, v, o));
+  return v;
+}
+
+}  // namespace fs1

@@ -1,0 +1,25 @@
+// fs1_dispatch.h — kernel registry (internal).
+#pragma once
+#include <cuda_runtime.h>
+
+#include "fs1_params.h"
+
+namespace fs1 {
+
+struct PersistEntry {
+  int dtype;  // 0 f32, 1 f64
+  bool logd;
+  int E, W;
+  size_t smem;
+  const void* solve_fn;
+  const void* apply_fn;
+  cudaError_t (*launch_solve)(const PersistParams&, long long grid, cudaStream_t);
+  cudaError_t (*launch_apply)(const PersistParams&, const void* x, void* y, long long grid,
+                              cudaStream_t);
+};
+
+// tables defined in fs1_persist_f32.cu / fs1_persist_f64.cu
+const PersistEntry* persist_table_f32(int* count);
+const PersistEntry* persist_table_f64(int* count);
+
+}  // namespace fs1

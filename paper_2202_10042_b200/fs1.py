@@ -1,0 +1,185 @@
+"""Thin Python face of libfs1 (include/fs1.h): the same entry points, with
+PyTorch tensors for device memory and the current CUDA stream.
+
+Nothing here computes any part of the method; every step runs in the CUDA
+kernels behind the C ABI.  See DESIGN.md §1 for the boundary.
+"""
+from __future__ import annotations
+
+import ctypes
+import dataclasses
+
+import torch
+
+from . import _lib as L
+
+_DT = {torch.float32: L.FS1_F32, torch.float64: L.FS1_F64}
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(device):
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+@dataclasses.dataclass(frozen=True)
+class Spec:
+    ndim: int
+    n: int
+    m: int
+    h1: float
+    h2: float
+    eps: float
+    batch: int
+    dtype: torch.dtype
+    domain: str = "scaling"
+    input_is_log: bool = False
+    itr_max: int = 1000
+    tol: float = 0.0
+    check_interval: int = 1
+    warm_start: bool = False
+
+    def desc(self) -> L.Desc:
+        return L.Desc(ndim=self.ndim, n=self.n, m=self.m, h1=self.h1, h2=self.h2, eps=self.eps,
+                      batch=self.batch, dtype=_DT[self.dtype],
+                      domain=L.FS1_LOG if self.domain == "log" else L.FS1_SCALING,
+                      input_is_log=int(self.input_is_log), itr_max=self.itr_max, tol=self.tol,
+                      check_interval=self.check_interval, warm_start=int(self.warm_start))
+
+
+class Plan:
+    """fs1_plan / fs1_plan_destroy around one problem description."""
+
+    def __init__(self, spec: Spec, device: int = 0):
+        self.spec = spec
+        self.device = device
+        self._h = ctypes.c_void_p()
+        ws = ctypes.c_size_t()
+        d = spec.desc()
+        s = L.lib().fs1_plan(ctypes.byref(d), device, ctypes.byref(self._h), ctypes.byref(ws))
+        if s != L.FS1_OK:
+            raise L.FS1Error(s, "fs1_plan")
+        self.workspace_bytes = ws.value
+        self._ws = None
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            L.lib().fs1_plan_destroy(h)
+            self._h = None
+
+    def info(self) -> dict:
+        pi = L.PlanInfo()
+        s = L.lib().fs1_plan_info(self._h, ctypes.byref(pi))
+        if s != L.FS1_OK:
+            raise L.FS1Error(s, "fs1_plan_info")
+        return {"kernel": pi.kernel.decode(), "chunk": pi.chunk, "threads": pi.threads,
+                "ctas_per_problem": pi.ctas_per_problem, "grid": pi.grid,
+                "smem_bytes": pi.smem_bytes, "workspace_bytes": pi.workspace_bytes}
+
+    def workspace(self):
+        if self.workspace_bytes and self._ws is None:
+            self._ws = torch.empty(self.workspace_bytes + 256, dtype=torch.uint8,
+                                   device=f"cuda:{self.device}")
+        if self._ws is None:
+            return None
+        off = (-self._ws.data_ptr()) % 256
+        return self._ws[off:]
+
+    # raw entry points (tensors must be on this plan's device, contiguous)
+    def solve_into(self, a, b, u, v, iters, err, flags, cost):
+        s = L.lib().fs1_solve(self._h, _ptr(a), _ptr(b), _ptr(u), _ptr(v), _ptr(iters), _ptr(err),
+                              _ptr(flags), _ptr(cost), _ptr(self.workspace()), _stream(self.device))
+        if s != L.FS1_OK:
+            raise L.FS1Error(s, "fs1_solve")
+
+    def cost_into(self, u, v, cost):
+        s = L.lib().fs1_cost(self._h, _ptr(u), _ptr(v), _ptr(cost), _ptr(self.workspace()),
+                             _stream(self.device))
+        if s != L.FS1_OK:
+            raise L.FS1Error(s, "fs1_cost")
+
+    def apply_into(self, x, y):
+        s = L.lib().fs1_apply(self._h, _ptr(x), _ptr(y), _ptr(self.workspace()), _stream(self.device))
+        if s != L.FS1_OK:
+            raise L.FS1Error(s, "fs1_apply")
+
+
+_CACHE: dict = {}
+
+
+def plan(spec: Spec, device: int = 0) -> Plan:
+    key = (spec, device)
+    p = _CACHE.get(key)
+    if p is None:
+        p = _CACHE[key] = Plan(spec, device)
+    return p
+
+
+def _check(t, name, dtype, device, size):
+    if not isinstance(t, torch.Tensor) or t.device.type != "cuda":
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if t.dtype != dtype or t.device.index != device or not t.is_contiguous():
+        raise ValueError(f"{name}: expected contiguous {dtype} on cuda:{device}")
+    if t.numel() % size:
+        raise ValueError(f"{name}: numel {t.numel()} is not a multiple of {size}")
+
+
+def solve(a, b, *, h, eps, itr_max, tol=0.0, domain="scaling", input_is_log=False,
+          check_interval=1, u0=None, v0=None, shape=None, h2=None, want_cost=True):
+    """Batched FS-1 solve.  a, b: CUDA tensors [batch, n] (1D) or [batch, n*m] with
+    shape=(n, m) (2D, column-major).  Returns dict u, v, iters, err, flags, cost."""
+    dev = a.device.index
+    if shape is None:
+        ndim, n, m = 1, a.shape[-1], 1
+    else:
+        ndim, (n, m) = 2, shape
+    size = n * m
+    _check(a, "a", a.dtype, dev, size)
+    _check(b, "b", a.dtype, dev, size)
+    batch = a.numel() // size
+    spec = Spec(ndim=ndim, n=n, m=m, h1=float(h), h2=float(h2 if h2 is not None else (h if ndim == 2 else 0.0)),
+                eps=float(eps), batch=batch, dtype=a.dtype, domain=domain,
+                input_is_log=bool(input_is_log), itr_max=int(itr_max), tol=float(tol),
+                check_interval=int(check_interval), warm_start=u0 is not None)
+    p = plan(spec, dev)
+    if u0 is not None:
+        u, v = u0.clone(), v0.clone()
+    else:
+        u, v = torch.empty_like(a), torch.empty_like(b)
+    iters = torch.empty(batch, dtype=torch.int32, device=a.device)
+    err = torch.empty(batch, dtype=torch.float64, device=a.device)
+    flags = torch.empty(batch, dtype=torch.int32, device=a.device)
+    cost = torch.empty(batch, dtype=torch.float64, device=a.device) if want_cost else None
+    p.solve_into(a, b, u, v, iters, err, flags, cost)
+    return {"u": u, "v": v, "iters": iters, "err": err, "flags": flags, "cost": cost}
+
+
+def cost(u, v, *, h, eps, domain="scaling", shape=None, h2=None):
+    dev = u.device.index
+    ndim, n, m = (1, u.shape[-1], 1) if shape is None else (2, *shape)
+    size = n * m
+    _check(u, "u", u.dtype, dev, size)
+    _check(v, "v", u.dtype, dev, size)
+    batch = u.numel() // size
+    spec = Spec(ndim=ndim, n=n, m=m, h1=float(h), h2=float(h2 if h2 is not None else (h if ndim == 2 else 0.0)),
+                eps=float(eps), batch=batch, dtype=u.dtype, domain=domain, itr_max=0)
+    out = torch.empty(batch, dtype=torch.float64, device=u.device)
+    plan(spec, dev).cost_into(u, v, out)
+    return out
+
+
+def apply(x, *, h, eps, domain="scaling", shape=None, h2=None):
+    """y = K x (scaling) or log K e^x (log) for every vector of x."""
+    dev = x.device.index
+    ndim, n, m = (1, x.shape[-1], 1) if shape is None else (2, *shape)
+    size = n * m
+    _check(x, "x", x.dtype, dev, size)
+    batch = x.numel() // size
+    spec = Spec(ndim=ndim, n=n, m=m, h1=float(h), h2=float(h2 if h2 is not None else (h if ndim == 2 else 0.0)),
+                eps=float(eps), batch=batch, dtype=x.dtype, domain=domain, itr_max=0)
+    y = torch.empty_like(x)
+    plan(spec, dev).apply_into(x, y)
+    return y

@@ -1,0 +1,244 @@
+"""GPU parity of the persistent one-CTA-per-problem kernel against the oracle.
+
+Kernel level (fs1_apply) and solver level (fs1_solve / fs1_cost), scaling and
+log domain, fp32 and fp64, sizes spanning one to many chunks, warps and a
+ragged tail; edge cases; configs 1, 2 and 5 at their full sizes on sampled
+pairs (the launch configuration bench.py times).
+"""
+import math
+
+import numpy as np
+import pytest
+
+import fs1_inputs as gi
+from oracle import dense, sinkhorn
+from tests.gpu_util import TOL, assert_solve_parity, rel, rel_norm
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_2202_10042_b200 import fs1  # noqa: E402
+
+DT = {"f32": torch.float32, "f64": torch.float64}
+
+
+def _cuda(x, dt):
+    return torch.from_numpy(np.ascontiguousarray(x)).to(DT[dt]).cuda()
+
+
+# ------------------------------------------------------------------ kernel apply
+APPLY_N = [1, 2, 3, 31, 33, 100, 257, 1000, 1024, 1500, 2048, 4095, 4096, 8000]
+
+
+@pytest.mark.parametrize("dt", ["f32", "f64"])
+@pytest.mark.parametrize("n", APPLY_N)
+@pytest.mark.parametrize("c", [0.01, 0.2, 1.5])
+def test_apply_scaling(dt, n, c):
+    rng = np.random.default_rng(n)
+    x = rng.uniform(0.1, 1.0, (3, n))
+    xg = _cuda(x, dt)
+    y = fs1.apply(xg, h=c, eps=1.0).double().cpu().numpy()
+    x64 = xg.double().cpu().numpy()
+    ref = np.stack([dense.apply(x64[p], math.exp(-c)) for p in range(3)])
+    tol = 1e-12 if dt == "f64" else 3e-6 / min(1.0, c * 4)
+    assert np.max(np.abs(y - ref) / ref) <= tol
+
+
+@pytest.mark.parametrize("dt", ["f32", "f64"])
+@pytest.mark.parametrize("n", [1, 2, 33, 257, 1000, 1024, 2048, 4096, 8000])
+@pytest.mark.parametrize("c", [0.005, 0.25, 1.0])
+def test_apply_log(dt, n, c):
+    rng = np.random.default_rng(100 + n)
+    X = rng.uniform(-60.0, 10.0, (2, n))
+    X[:, ::7] -= 300.0  # wide dynamic range: needs the extended-range carries
+    xg = _cuda(X, dt)
+    Y = fs1.apply(xg, h=c, eps=1.0, domain="log").double().cpu().numpy()
+    X64 = xg.double().cpu().numpy()
+    ref = np.stack([dense.apply_log(X64[p], c) for p in range(2)])
+    tol = 1e-12 if dt == "f64" else 2e-6
+    assert np.max(np.abs(Y - ref) / np.maximum(np.abs(ref), 1.0)) <= tol
+
+
+# ------------------------------------------------------------------ small solves
+SOLVE_CASES = [
+    # (n, eps, itr, dtype, domain)
+    (1, 0.1, 5, "f64", "scaling"),
+    (2, 0.3, 50, "f64", "scaling"),
+    (37, 0.02, 40, "f64", "scaling"),
+    (1000, 0.01, 60, "f64", "scaling"),
+    (1024, 0.005, 60, "f32", "scaling"),
+    (999, 0.005, 60, "f32", "scaling"),
+    (2000, 0.005, 40, "f32", "scaling"),
+    (300, 0.003, 50, "f32", "log"),
+    (4096, 0.001, 40, "f32", "log"),
+    (3000, 0.001, 40, "f32", "log"),
+    (1000, 0.001, 40, "f64", "log"),
+    (4096, 0.0005, 30, "f64", "log"),
+]
+
+
+@pytest.mark.parametrize("n,eps,itr,dt,dom", SOLVE_CASES)
+def test_solve_small(n, eps, itr, dt, dom):
+    cfg = "c5" if dom == "log" else "c2"
+    P = 3
+    A, B = gi.batch(cfg, range(P), n=n)
+    ag, bg = _cuda(A, dt), _cuda(B, dt)
+    out = fs1.solve(ag, bg, h=1.0 / n, eps=eps, itr_max=itr, domain=dom)
+    ref = sinkhorn.solve(ag.double().cpu().numpy(), bg.double().cpu().numpy(), n=n, h1=1.0 / n,
+                         eps=eps, itr_max=itr, domain="scaling")
+    assert_solve_parity(out, ref, dom, dt)
+    # fs1_cost on the returned state agrees with the fused cost
+    c2 = fs1.cost(out["u"], out["v"], h=1.0 / n, eps=eps, domain=dom).cpu().numpy()
+    np.testing.assert_allclose(c2, out["cost"].cpu().numpy(), rtol=TOL[dt])
+
+
+@pytest.mark.parametrize("dt", ["f32", "f64"])
+def test_log_equals_scaling_where_finite(dt):
+    n, eps = 700, 0.01
+    A, B = gi.batch("c1", range(2), n=n)
+    ag, bg = _cuda(A, dt), _cuda(B, dt)
+    s = fs1.solve(ag, bg, h=1 / n, eps=eps, itr_max=50)
+    lg = fs1.solve(ag, bg, h=1 / n, eps=eps, itr_max=50, domain="log")
+    t = TOL[dt]
+    assert rel_norm(lg["u"].double().cpu().numpy(), np.log(s["u"].double().cpu().numpy())) <= t
+    np.testing.assert_allclose(lg["cost"].cpu().numpy(), s["cost"].cpu().numpy(), rtol=t)
+
+
+def test_log_input_weights():
+    n, eps = 512, 0.002
+    A, B = gi.batch("c5", range(2), n=n)
+    ag, bg = _cuda(A, "f32"), _cuda(B, "f32")
+    lin = fs1.solve(ag, bg, h=1 / n, eps=eps, itr_max=30, domain="log")
+    lg = fs1.solve(torch.log(ag), torch.log(bg), h=1 / n, eps=eps, itr_max=30, domain="log",
+                   input_is_log=True)
+    assert rel_norm(lg["u"].double().cpu().numpy(), lin["u"].double().cpu().numpy()) <= 1e-5
+
+
+def test_zero_weights_log_domain():
+    """a_i = 0 (log -inf) is allowed in the log domain: F_i = -inf, the rest matches."""
+    n, eps = 256, 0.01
+    A, B = gi.batch("c5", range(1), n=n)
+    A[0, 40:90] = 0.0
+    A /= A.sum()
+    ag, bg = _cuda(A, "f64"), _cuda(B, "f64")
+    out = fs1.solve(ag, bg, h=1 / n, eps=eps, itr_max=40, domain="log")
+    with np.errstate(divide="ignore"):
+        ref = sinkhorn.solve(np.log(A), np.log(B), n=n, h1=1 / n, eps=eps, itr_max=40,
+                             domain="log", input_is_log=True)
+    assert_solve_parity(out, ref, "log", "f64")
+
+
+def test_tolerance_stop_and_check_interval():
+    n, eps = 400, 0.02
+    A, B = gi.batch("c1", range(2), n=n)
+    ag, bg = _cuda(A, "f64"), _cuda(B, "f64")
+    for ci in [1, 5]:
+        out = fs1.solve(ag, bg, h=1 / n, eps=eps, itr_max=5000, tol=1e-9, check_interval=ci)
+        ref = sinkhorn.solve(A, B, n=n, h1=1 / n, eps=eps, itr_max=5000, tol=1e-9, check_interval=ci)
+        it = out["iters"].cpu().numpy()
+        assert np.all(np.abs(it - ref["iters"]) <= ci)
+        assert np.all(out["flags"].cpu().numpy() == 1)
+        assert np.all(out["err"].cpu().numpy() <= 1e-9)
+
+
+def test_nonfinite_flag():
+    """Unstabilised scaling domain terminates abnormally; log domain does not."""
+    n = 200
+    x = (np.arange(n) + 0.5) / n
+    a = np.exp(-((x - 0.2) / 0.05) ** 2) + 1e-3
+    b = np.exp(-((x - 0.8) / 0.05) ** 2) + 1e-3
+    a, b = a / a.sum(), b / b.sum()
+    ref = sinkhorn.solve(a, b, n=n, h1=1 / n, eps=5e-4, itr_max=200)
+    out = fs1.solve(_cuda(a[None], "f64"), _cuda(b[None], "f64"), h=1 / n, eps=5e-4, itr_max=200)
+    assert out["flags"].item() == 2 and ref["flags"][0] == 2
+    assert out["iters"].item() == ref["iters"][0]
+    lg = fs1.solve(_cuda(a[None], "f64"), _cuda(b[None], "f64"), h=1 / n, eps=5e-4, itr_max=200,
+                   domain="log")
+    assert lg["flags"].item() == 4 and math.isfinite(lg["cost"].item())
+
+
+def test_warm_start_resume():
+    """solve(k1) then solve(k2, warm) == solve(k1 + k2) (the state is the checkpoint)."""
+    n, eps = 1024, 0.005
+    A, B = gi.batch("c2", range(2), n=n)
+    for dom in ["scaling", "log"]:
+        ag, bg = _cuda(A, "f64"), _cuda(B, "f64")
+        full = fs1.solve(ag, bg, h=1 / n, eps=eps, itr_max=30, domain=dom)
+        h1 = fs1.solve(ag, bg, h=1 / n, eps=eps, itr_max=12, domain=dom)
+        h2 = fs1.solve(ag, bg, h=1 / n, eps=eps, itr_max=18, domain=dom, u0=h1["u"], v0=h1["v"])
+        Fa = full["u"].cpu().numpy()
+        Fb = h2["u"].cpu().numpy()
+        if dom == "scaling":
+            Fa, Fb = np.log(Fa), np.log(Fb)
+        assert rel_norm(Fb, Fa) <= 1e-12
+        np.testing.assert_allclose(h2["cost"].cpu().numpy(), full["cost"].cpu().numpy(), rtol=1e-12)
+
+
+def test_determinism_and_batch_independence():
+    n, eps = 1024, 0.005
+    A, B = gi.batch("c2", range(64), n=n)
+    ag, bg = _cuda(A, "f32"), _cuda(B, "f32")
+    o1 = fs1.solve(ag, bg, h=1 / n, eps=eps, itr_max=40)
+    o2 = fs1.solve(ag, bg, h=1 / n, eps=eps, itr_max=40)
+    assert torch.equal(o1["u"], o2["u"]) and torch.equal(o1["cost"], o2["cost"])
+    sub = fs1.solve(ag[10:13].contiguous(), bg[10:13].contiguous(), h=1 / n, eps=eps, itr_max=40)
+    assert torch.equal(sub["u"], o1["u"][10:13]) and torch.equal(sub["cost"], o1["cost"][10:13])
+
+
+def test_identity_kernel_and_n1():
+    rng = np.random.default_rng(3)
+    a = gi.random_positive(rng, (1, 16))
+    out = fs1.solve(_cuda(a, "f64"), _cuda(a, "f64"), h=1.0, eps=1e-4, itr_max=50, tol=1e-14)
+    assert out["iters"].item() == 1 and out["flags"].item() == 1
+    assert out["err"].item() == 0.0 and out["cost"].item() == 0.0
+    one = torch.ones(4, 1, dtype=torch.float64, device="cuda")
+    o = fs1.solve(one, one, h=1.0, eps=0.1, itr_max=3)
+    assert torch.all(o["cost"] == 0) and torch.all(o["iters"] == 3)
+
+
+# ------------------------------------------------------------------ configs at full size
+def test_config1_full():
+    """C1: N=1000 fp64 scaling, tol 1e-9: replay at the oracle's stopping iteration l*
+    with tol = 0 (R6), and the GPU's own tol-stop lands at l* +- 1."""
+    cfg = gi.CONFIGS["c1"]
+    A, B = gi.batch(cfg, [0])
+    ref = sinkhorn.solve(A, B, n=cfg.n, h1=cfg.h1, eps=cfg.eps, itr_max=cfg.itr_max, tol=cfg.tol)
+    ls = int(ref["iters"][0])
+    ag, bg = _cuda(A, "f64"), _cuda(B, "f64")
+    fixed = fs1.solve(ag, bg, h=cfg.h1, eps=cfg.eps, itr_max=ls)
+    ref_fixed = sinkhorn.solve(A, B, n=cfg.n, h1=cfg.h1, eps=cfg.eps, itr_max=ls)
+    assert_solve_parity(fixed, ref_fixed, "scaling", "f64")
+    own = fs1.solve(ag, bg, h=cfg.h1, eps=cfg.eps, itr_max=cfg.itr_max, tol=cfg.tol)
+    assert abs(own["iters"].item() - ls) <= 1 and own["flags"].item() == 1
+
+
+def test_config2_full_batch_sampled():
+    """C2: 4096 pairs x N=1024 fp32 scaling, 500 iterations, in one launch; sampled pairs
+    against the fp64 dense oracle."""
+    cfg = gi.CONFIGS["c2"]
+    A, B = gi.batch(cfg, range(cfg.batch))
+    ag, bg = _cuda(A, "f32"), _cuda(B, "f32")
+    out = fs1.solve(ag, bg, h=cfg.h1, eps=cfg.eps, itr_max=cfg.itr_max)
+    pairs = [0, 1, 1777, 4095]
+    ref = sinkhorn.solve(ag[pairs].double().cpu().numpy(), bg[pairs].double().cpu().numpy(),
+                         n=cfg.n, h1=cfg.h1, eps=cfg.eps, itr_max=cfg.itr_max)
+    assert_solve_parity(out, ref, "scaling", "f32", pairs=pairs)
+    assert np.all(out["flags"].cpu().numpy() == 4)
+
+
+def test_config5_shard_sampled():
+    """C5: one GPU's shard (8192 pairs x N=4096, fp32 log, 1000 iterations) in one launch;
+    sampled pairs against the fp64 oracle (scaling domain is exact here: max|F| ~ 125 << 709)."""
+    cfg = gi.CONFIGS["c5"]
+    shard = 8192
+    A, B = gi.batch(cfg, range(shard))
+    ag, bg = _cuda(A, "f32"), _cuda(B, "f32")
+    out = fs1.solve(ag, bg, h=cfg.h1, eps=cfg.eps, itr_max=cfg.itr_max, domain="log")
+    pairs = [0, 4321, 8191]
+    ref = sinkhorn.solve(ag[pairs].double().cpu().numpy(), bg[pairs].double().cpu().numpy(),
+                         n=cfg.n, h1=cfg.h1, eps=cfg.eps, itr_max=cfg.itr_max)
+    assert np.all(np.isfinite(ref["F"])) and np.all(ref["flags"] == 4)
+    assert_solve_parity(out, ref, "log", "f32", pairs=pairs)
