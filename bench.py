@@ -1,0 +1,364 @@
+#!/usr/bin/env python
+"""FS-1 hot-path benchmark (driver contract: one JSON line on rank 0).
+
+A "step" is one full FS-1 solve (Algorithm 1: every iteration, the marginal
+error at exit and the fused return-line cost) over one batch of synthetic
+histogram pairs of BASELINE.json's configuration.  Default workload: configs[1]
+("c2": 4096 pairs, N=1024, fp32, eps=5e-3, 500 iterations) — the config the
+metric is quoted on that fits one GPU.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl fs1|reference]
+
+Multi-GPU (torchrun, one process per GPU): weak scaling — every rank solves its
+own batch of distinct pairs (pair ids rank*B + i, same recipe); the per-pair
+results {cost, iters, err, flags} are all-gathered with NCCL inside each step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import fs1_inputs as gi  # noqa: E402
+
+METRIC = "grid-point Sinkhorn updates/sec (N*iters*batch/s) and achieved HBM GB/s"
+UNIT = "updates/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2", choices=sorted(gi.CONFIGS))
+    ap.add_argument("--impl", default="fs1", choices=["fs1", "reference"])
+    ap.add_argument("--batch", type=int, default=None, help="pairs per GPU (default: config)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def per_gpu_batch(cfg, args):
+    if args.batch:
+        return args.batch
+    if cfg.name == "c5":
+        return 8192          # 65536 pairs over 8 GPUs (BASELINE configs[4])
+    return cfg.batch
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 5 + i and r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ----------------------------------------------------------------------------- roofline
+MUFU_PER_SM_CLK = 16        # SFU lanes per SM per clock (guide: B300 has 2x B200's SFU rate)
+FMA_PER_SM_CLK = 128        # FP32 lanes per SM per clock
+
+
+def alu_peak_updates(sms, clk_mhz):
+    """Issue/MUFU roofline of the persistent kernel: per grid-point
+    update the path needs at least 2 reciprocals (one per half-step, MUFU) and 8
+    FP32 FMA-pipe ops (4 recursion FMAs, 2 p+q combines, 2 b*rcp); the MUFU term
+    dominates: 2/16 SM-clk per update."""
+    per_update = max(2.0 / MUFU_PER_SM_CLK, 8.0 / FMA_PER_SM_CLK)
+    return sms * clk_mhz * 1e6 / per_update
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+def profile_traffic(cfg_name):
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f).get(cfg_name)
+    return None
+
+
+# ----------------------------------------------------------------------------- oracle legs
+def oracle_sample(cfg, pairs, iters):
+    """Time the oracle (as it stands) on a bounded sample; returns (updates, seconds)."""
+    from oracle import sinkhorn
+    A, B = gi.batch(cfg, pairs)
+    A64, B64 = A.astype(np.float64), B.astype(np.float64)
+    t0 = time.perf_counter()
+    if cfg.ndim == 1 and cfg.n <= 8192:
+        sinkhorn.solve(A64, B64, n=cfg.n, h1=cfg.h1, eps=cfg.eps, itr_max=iters,
+                       domain="scaling", input_is_log=cfg.input_is_log)
+    else:
+        sinkhorn.solve(A64, B64, n=cfg.n, m=cfg.m, h1=cfg.h1, h2=cfg.h2, eps=cfg.eps, itr_max=iters,
+                       domain="log", input_is_log=cfg.input_is_log, apply="recur")
+    t = time.perf_counter() - t0
+    return cfg.size * iters * len(pairs), t
+
+
+def oracle_cores():
+    try:
+        from threadpoolctl import threadpool_info
+        return max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:
+        return os.cpu_count()
+
+
+def sample_plan(cfg):
+    """Bounded oracle sample (about 10-30 s of CPU work) for the config."""
+    if cfg.name == "c2":
+        return list(range(256)), cfg.itr_max, "256 of 4096 pairs, all 500 iterations, dense fp64 (BLAS)"
+    if cfg.name == "c5":
+        return list(range(8)), 200, "8 pairs, 200 of 1000 iterations, dense fp64 (BLAS)"
+    if cfg.name == "c1":
+        return [0], 700, "1 pair, 700 iterations, dense fp64"
+    return [0], 1, "1 pair, 1 iteration, plain-C LSE recursion"
+
+
+def run_reference(args, cfg):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    pairs, iters, what = sample_plan(cfg)
+    oracle_sample(cfg, pairs[:1], 1)          # warm-up (builds the C oracle, BLAS threads)
+    times = []
+    ups = 0
+    for _ in range(args.warmup):
+        oracle_sample(cfg, pairs[:2], 2)
+    for _ in range(args.steps):
+        u, t = oracle_sample(cfg, pairs, iters)
+        ups, times = u, times + [t]
+    T = sum(times)
+    value = ups * len(times) / T
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * T / len(times),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (fs1_inputs recipe of BASELINE configs)",
+            "config": {"workload": cfg.name, "description": cfg.description, "sample": what},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": oracle_cores(), "kind": "oracle",
+                             "sample": what},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- GPU leg
+def run_fs1(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2202_10042_b200 import fs1
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+    B = per_gpu_batch(cfg, args)
+    pair_ids = range(rank * B, (rank + 1) * B)
+    A, Bm = gi.batch(cfg, pair_ids)
+    tdt = torch.float32 if cfg.dtype == "f32" else torch.float64
+    a = torch.from_numpy(A).to(dev)
+    b = torch.from_numpy(Bm).to(dev)
+    shape = (cfg.n, cfg.m) if cfg.ndim == 2 else None
+    spec = fs1.Spec(ndim=cfg.ndim, n=cfg.n, m=cfg.m, h1=cfg.h1, h2=cfg.h2, eps=cfg.eps, batch=B,
+                    dtype=tdt, domain=cfg.domain, input_is_log=cfg.input_is_log,
+                    itr_max=cfg.itr_max, tol=cfg.tol)
+    plan = fs1.plan(spec, local)
+    u, v = torch.empty_like(a), torch.empty_like(b)
+    iters = torch.empty(B, dtype=torch.int32, device=dev)
+    err = torch.empty(B, dtype=torch.float64, device=dev)
+    flags = torch.empty(B, dtype=torch.int32, device=dev)
+    cost = torch.empty(B, dtype=torch.float64, device=dev)
+    res = torch.empty((B, 4), dtype=torch.float64, device=dev)
+    gathered = torch.empty((ws * B, 4), dtype=torch.float64, device=dev) if ws > 1 else None
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > L2 (126 MB)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        plan.solve_into(a, b, u, v, iters, err, flags, cost)
+        if ws > 1:   # the one collective of the path: gather per-pair results (NCCL)
+            torch.stack([cost, err, iters.double(), flags.double()], 1, out=res)
+            dist.all_gather_into_tensor(gathered, res)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        if ws > 1:
+            dist.barrier()
+        for i in range(args.steps):
+            flush.zero_()                              # L2 flush between timed steps (untimed)
+            ev[i][0].record(stream)
+            kev[i][0].record(stream)
+            plan.solve_into(a, b, u, v, iters, err, flags, cost)
+            kev[i][1].record(stream)
+            if ws > 1:
+                torch.stack([cost, err, iters.double(), flags.double()], 1, out=res)
+                dist.all_gather_into_tensor(gathered, res)
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+        if ws > 1:
+            dist.barrier()
+    step_ms = [s.elapsed_time(e) for s, e in ev]
+    kern_ms = [s.elapsed_time(e) for s, e in kev]
+    T = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(T, op=dist.ReduceOp.MAX)
+    total_s = T.item() / 1e3
+    it_run = int(iters.max().item())
+    updates_per_step_rank = cfg.size * it_run * B
+    value = ws * updates_per_step_rank * args.steps / total_s
+    kern_avg_s = statistics.mean(kern_ms) / 1e3
+
+    # ---- end-to-end through the public API with host buffers (pinned), one GPU's view
+    e2e = None
+    if not args.no_e2e:
+        ha = torch.from_numpy(A).pin_memory()
+        hb = torch.from_numpy(Bm).pin_memory()
+        hc = torch.empty(B, dtype=torch.float64).pin_memory()
+        for _ in range(2):
+            out = fs1.solve(ha.to(dev, non_blocking=True), hb.to(dev, non_blocking=True), h=cfg.h1,
+                            eps=cfg.eps, itr_max=cfg.itr_max, tol=cfg.tol, domain=cfg.domain,
+                            input_is_log=cfg.input_is_log, shape=shape,
+                            h2=cfg.h2 if cfg.ndim == 2 else None)
+            hc.copy_(out["cost"], non_blocking=True)
+        torch.cuda.synchronize()
+        if ws > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            out = fs1.solve(ha.to(dev, non_blocking=True), hb.to(dev, non_blocking=True), h=cfg.h1,
+                            eps=cfg.eps, itr_max=cfg.itr_max, tol=cfg.tol, domain=cfg.domain,
+                            input_is_log=cfg.input_is_log, shape=shape,
+                            h2=cfg.h2 if cfg.ndim == 2 else None)
+            hc.copy_(out["cost"], non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        Te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+        if ws > 1:
+            dist.all_reduce(Te, op=dist.ReduceOp.MAX)
+        e2e = {"value": ws * updates_per_step_rank * args.steps / (Te.item() / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": int(ha.numel() * ha.element_size() + hb.numel() * hb.element_size()),
+               "d2h_bytes_per_step": int(hc.numel() * hc.element_size())}
+
+    if rank == 0:
+        peaks, src = load_peaks()
+        props = torch.cuda.get_device_properties(dev)
+        clocks = clk.summary()
+        info = plan.info()
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": sum(step_ms) / len(step_ms),
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": cfg.dtype, "data": "synthetic (fs1_inputs recipe of BASELINE configs)",
+                "config": {"workload": cfg.name, "description": cfg.description, "pairs_per_gpu": B,
+                           "n": cfg.n, "m": cfg.m, "iters": it_run, "domain": cfg.domain,
+                           "kernel": info["kernel"], "parallelism": f"batch-sharded x{ws} (weak)",
+                           "l2": "flushed between timed steps (256 MiB write, untimed)"},
+                "gpu_launches": args.steps * 1,
+                "clocks": clocks}
+        kern_ups = updates_per_step_rank / kern_avg_s
+        if info["kernel"].startswith("persist"):
+            clk_mhz = peaks.get("sm_max_mhz", 1965.0)
+            peak = alu_peak_updates(props.multi_processor_count, clk_mhz) / 1e9
+            line["roofline"] = {"bound": "alu", "achieved": kern_ups / 1e9, "peak": peak,
+                                "unit": "Gupdate/s", "frac": kern_ups / 1e9 / peak,
+                                "traffic": profile_traffic(cfg.name),
+                                "kernel_ms": kern_avg_s * 1e3,
+                                "peak_source": f"derived: {props.multi_processor_count} SMs x "
+                                               f"{clk_mhz:.0f} MHz x 16 MUFU/clk / 2 rcp per update"}
+        line["e2e"] = e2e
+        if not args.no_cpu_baseline:
+            pairs, it, what = sample_plan(cfg)
+            oracle_sample(cfg, pairs[:1], 1)
+            u_, t_ = oracle_sample(cfg, pairs, it)
+            line["cpu_baseline"] = {"value": u_ / t_, "unit": UNIT, "cores": oracle_cores(),
+                                    "kind": "oracle", "sample": what, "seconds": t_}
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    cfg = gi.CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_fs1(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -59,7 +59,9 @@ CONFIGS = {
     "c1": Config("c1", 1, 1000, 1, 1, "f64", "scaling", 1e-2, 2000, 1e-9, False,
                  "1D N=1000 on [0,1], h=1/N, one pair fp64, 2-component Gaussian mixtures "
                  "+1e-6 floor, eps=1e-2, 2000 iters or marginal L1 err <= 1e-9"),
-    "c2": Config("c2", 1, 1024, 1, 4096, "f32", "scaling", 5e-3, 500, 0.0, False,
+    # domain: the fp32 scaling domain overflows on some pairs of this config (max |log phi|
+    # reaches ~80 of fp32's 88.7 within 64 pairs), so it runs in the log domain (R14)
+    "c2": Config("c2", 1, 1024, 1, 4096, "f32", "log", 5e-3, 500, 0.0, False,
                  "batch 4096 pairs, 1D N=1024 fp32, Dirichlet(1) smoothed by width-5 box, "
                  "eps=5e-3, 500 iters"),
     "c3": Config("c3", 1, 1 << 24, 1, 1, "f64", "log", 1e-4, 1000, 0.0, True,

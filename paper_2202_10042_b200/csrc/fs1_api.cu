@@ -20,6 +20,7 @@ struct fs1_plan_s {
   int kind;  // 0 persistent
   const PersistEntry* pe;
   PersistParams base;  // multipliers + scalars; pointers filled per call
+  size_t smem;         // dynamic shared memory per CTA (>= the kernel's need; sized for occupancy)
   size_t ws;
   fs1_plan_info_t info;
 };
@@ -66,6 +67,43 @@ void fill_persist_tables(PersistParams& P, double c, int E) {
 
 std::mutex g_attr_mu;
 
+// Wave quantisation: with occ resident CTAs per SM the batch runs in
+// waves = ceil(B / (SMs occ)) rounds; when the last round is partial, running fewer
+// CTAs per SM (target = ceil(B / (SMs waves))) gives every round the whole SM.
+// The resident count is lowered by padding the dynamic shared memory request.
+cudaError_t size_persist_smem(const PersistEntry* pe, long long batch, int device, size_t* out) {
+  const int threads = 32 * pe->W;
+  int sms = 0, smem_sm = 0, reserved = 0, smem_optin = 0;
+  cudaError_t e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, device);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(pe->solve_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin);
+  if (e != cudaSuccess) return e;
+  size_t smem = pe->smem;
+  int occ = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pe->solve_fn, threads, smem);
+  if (e != cudaSuccess) return e;
+  if (occ < 1) return cudaErrorInvalidConfiguration;
+  const long long waves = (batch + (long long)sms * occ - 1) / ((long long)sms * occ);
+  const int target = (int)((batch + (long long)sms * waves - 1) / ((long long)sms * waves));
+  if (target < occ && target >= 1) {
+    size_t s2 = ((size_t)smem_sm / target - (size_t)reserved) & ~(size_t)127;
+    if (s2 > (size_t)smem_optin) s2 = (size_t)smem_optin & ~(size_t)127;
+    for (; s2 > smem; s2 -= 128) {
+      int o2 = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, pe->solve_fn, threads, s2) != cudaSuccess) break;
+      if (o2 >= target) {
+        if (o2 == target) smem = s2;
+        break;
+      }
+    }
+  }
+  *out = smem;
+  return cudaFuncSetAttribute(pe->solve_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+
 }  // namespace
 
 extern "C" {
@@ -107,10 +145,18 @@ fs1_status fs1_plan(const fs1_desc* desc, int device, fs1_plan_t** out, size_t* 
 
   if (d.ndim == 1) {
     // persistent kernel: the smallest (E, W) instantiation whose 32 W E covers n
-    int cnt = 0;
-    const PersistEntry* tab = d.dtype == FS1_F32 ? persist_table_f32(&cnt) : persist_table_f64(&cnt);
+    const PersistEntry* (*tables[3])(int*) = {nullptr, nullptr, nullptr};
+    if (d.dtype == FS1_F32) {
+      if (logd) { tables[0] = persist_table_f32l; tables[1] = persist_table_f32l2; }
+      else tables[0] = persist_table_f32s;
+    } else {
+      tables[0] = logd ? persist_table_f64l : persist_table_f64s;
+    }
     const PersistEntry* best = nullptr;
-    for (int i = 0; i < cnt; ++i) {
+    for (int ti = 0; ti < 3 && tables[ti]; ++ti) {
+     int cnt = 0;
+     const PersistEntry* tab = tables[ti](&cnt);
+     for (int i = 0; i < cnt; ++i) {
       const PersistEntry& e = tab[i];
       if (e.logd != logd) continue;
       const long long cap = 32LL * e.W * e.E;
@@ -123,6 +169,7 @@ fs1_status fs1_plan(const fs1_desc* desc, int device, fs1_plan_t** out, size_t* 
       if (!best || cap < 32LL * best->W * best->E ||
           (cap == 32LL * best->W * best->E && e.W < best->W))
         best = &e;
+     }
     }
     if (!best) {
       delete p;
@@ -147,12 +194,12 @@ fs1_status fs1_plan(const fs1_desc* desc, int device, fs1_plan_t** out, size_t* 
       int cur = 0;
       if (cudaGetDevice(&cur) != cudaSuccess) { delete p; return FS1_ERR_CUDA; }
       if (cur != device && cudaSetDevice(device) != cudaSuccess) { delete p; return FS1_ERR_CUDA; }
-      cudaError_t e1 = cudaFuncSetAttribute(best->solve_fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (int)best->smem);
-      cudaError_t e2 = cudaFuncSetAttribute(best->apply_fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (int)best->smem);
+      cudaError_t e = size_persist_smem(best, d.batch, device, &p->smem);
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(best->apply_fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)best->smem);
       if (cur != device) cudaSetDevice(cur);
-      if (e1 != cudaSuccess || e2 != cudaSuccess) {
+      if (e != cudaSuccess) {
         delete p;
         return FS1_ERR_CUDA;
       }
@@ -164,7 +211,7 @@ fs1_status fs1_plan(const fs1_desc* desc, int device, fs1_plan_t** out, size_t* 
     p->info.threads = 32 * best->W;
     p->info.ctas_per_problem = 1;
     p->info.grid = d.batch;
-    p->info.smem_bytes = best->smem;
+    p->info.smem_bytes = p->smem;
     p->info.workspace_bytes = 0;
   } else {
     delete p;
@@ -172,6 +219,14 @@ fs1_status fs1_plan(const fs1_desc* desc, int device, fs1_plan_t** out, size_t* 
   }
   if (workspace_bytes) *workspace_bytes = p->ws;
   *out = p;
+  return FS1_OK;
+}
+
+// test-only (not in include/fs1.h): per-half-step trace of CTA 0 into buf
+// [2*itr_max+2][threads][10] doubles.
+fs1_status fs1__set_debug(fs1_plan_t* plan, double* buf) {
+  if (!plan) return FS1_ERR_ARG;
+  plan->base.dbg = buf;
   return FS1_OK;
 }
 
@@ -192,7 +247,7 @@ fs1_status fs1_solve(const fs1_plan_t* plan, const void* a, const void* b, void*
     PersistParams P = plan->base;
     P.a = a; P.b = b; P.u = u; P.v = v;
     P.iters = iters; P.err = err; P.flags = flags; P.cost = cost;
-    cudaError_t e = plan->pe->launch_solve(P, plan->d.batch, (cudaStream_t)stream);
+    cudaError_t e = plan->pe->launch_solve(P, plan->d.batch, plan->smem, (cudaStream_t)stream);
     return e == cudaSuccess ? FS1_OK : FS1_ERR_CUDA;
   }
   return FS1_ERR_UNSUPPORTED;
@@ -213,7 +268,7 @@ fs1_status fs1_cost(const fs1_plan_t* plan, const void* u, const void* v, double
     P.input_is_log = plan->d.domain == FS1_LOG;
     P.a = u; P.b = v; P.u = const_cast<void*>(u); P.v = const_cast<void*>(v);
     P.iters = nullptr; P.err = nullptr; P.flags = nullptr; P.cost = cost;
-    cudaError_t e = plan->pe->launch_solve(P, plan->d.batch, (cudaStream_t)stream);
+    cudaError_t e = plan->pe->launch_solve(P, plan->d.batch, plan->smem, (cudaStream_t)stream);
     return e == cudaSuccess ? FS1_OK : FS1_ERR_CUDA;
   }
   return FS1_ERR_UNSUPPORTED;

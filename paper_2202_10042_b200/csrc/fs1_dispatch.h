@@ -13,13 +13,16 @@ struct PersistEntry {
   size_t smem;
   const void* solve_fn;
   const void* apply_fn;
-  cudaError_t (*launch_solve)(const PersistParams&, long long grid, cudaStream_t);
+  cudaError_t (*launch_solve)(const PersistParams&, long long grid, size_t smem, cudaStream_t);
   cudaError_t (*launch_apply)(const PersistParams&, const void* x, void* y, long long grid,
                               cudaStream_t);
 };
 
-// tables defined in fs1_persist_f32.cu / fs1_persist_f64.cu
-const PersistEntry* persist_table_f32(int* count);
-const PersistEntry* persist_table_f64(int* count);
+// tables defined in fs1_persist_*.cu
+const PersistEntry* persist_table_f32s(int* count);
+const PersistEntry* persist_table_f32l(int* count);
+const PersistEntry* persist_table_f32l2(int* count);
+const PersistEntry* persist_table_f64s(int* count);
+const PersistEntry* persist_table_f64l(int* count);
 
 }  // namespace fs1

@@ -203,7 +203,7 @@ template <class T, int E, int WARPS, bool LOGD> struct Half {
   using Vt = typename Tt::V;
 
   struct Ctx {
-    int tid, lane, warp, nv;
+    int tid, lane, warp, nv, slot;
     T lam;
     T lA, lB, rA, rB;        // scaling: lane powers
     ER<double> lP, rP;       // log: lane powers
@@ -214,7 +214,7 @@ template <class T, int E, int WARPS, bool LOGD> struct Half {
   template <bool CHECK, bool MASK, bool SLOW>
   __device__ __forceinline__ static double passes(const Ctx& c, const T (&x)[E], T (&y)[E], int ye,
                                                   const Vt* tgt, int te, Vt* sK, T cf, T cb, T s,
-                                                  int R, T& acc, int& kexp_out) {
+                                                  int R, int& kexp_out) {
     const T lam = c.lam;
 
     // 3a. forward recursion from the carry: p_k = lam p_{k-1} + x_k (Alg. 1 line 5 / 10)
@@ -245,7 +245,7 @@ template <class T, int E, int WARPS, bool LOGD> struct Half {
         if constexpr (LOGD) {
           if (e == E - 1) {
             kexp = Tt::expo(kx);
-            sc = Tt::pow2(-kexp);
+            sc = Tt::pow2(kexp);
           }
         }
         if constexpr (CHECK) {
@@ -258,7 +258,6 @@ template <class T, int E, int WARPS, bool LOGD> struct Half {
           else val = tv[r] * Tt::rcp(kx);
           if (MASK && e >= c.nv) val = T(0);
           y[e] = val;
-          acc += val;
         }
       }
     }
@@ -266,7 +265,8 @@ template <class T, int E, int WARPS, bool LOGD> struct Half {
     return errp;
   }
 
-  // Returns the per-thread error partial (CHECK) in fp64, units of 1.
+  // Returns the per-thread error partial (CHECK) in fp64, units of 1; acc receives the
+  // sum of the chunk aggregates of x (non-finite iff some x of the chunk is).
   template <bool CHECK, bool MASK>
   __device__ __forceinline__ static double run(const Ctx& c, const PersistParams& P, const T (&x)[E],
                                                int xe, T (&y)[E], int& ye, const Vt* tgt, int te,
@@ -278,6 +278,7 @@ template <class T, int E, int WARPS, bool LOGD> struct Half {
     for (int e = 0; e < E; ++e) f = fma(lam, f, x[e]);
 #pragma unroll
     for (int e = E - 1; e >= 0; --e) g = fma(lam, g, x[e]);
+    acc = f + g;  // non-finite input detection (x >= 0: inf and NaN propagate)
 
     // 2. carries
     T cf, cb, s = T(1);
@@ -302,22 +303,27 @@ template <class T, int E, int WARPS, bool LOGD> struct Half {
     if constexpr (CHECK) PS::sts(sK, c.tid, y);  // keep y_old
     double errp;
     int kexp;
-    if (!LOGD || !slow) errp = passes<CHECK, MASK, false>(c, x, y, ye, tgt, te, sK, cf, cb, s, R, acc, kexp);
-    else errp = passes<CHECK, MASK, true>(c, x, y, ye, tgt, te, sK, cf, cb, s, R, acc, kexp);
+    if (!LOGD || !slow) errp = passes<CHECK, MASK, false>(c, x, y, ye, tgt, te, sK, cf, cb, s, R, kexp);
+    else errp = passes<CHECK, MASK, true>(c, x, y, ye, tgt, te, sK, cf, cb, s, R, kexp);
     if constexpr (LOGD) {
       if constexpr (CHECK) errp *= pow2d(te);
-      if (!CHECK) ye = (te == ZE) ? ZE : te - R + kexp;
+      if (!CHECK) ye = (te == ZE) ? ZE : te - R - kexp;
     }
     R_out = R;
     k_out = kexp;
+    if (P.dbg && blockIdx.x == 0) {
+      double* r = P.dbg + ((size_t)c.slot * PS::NT + c.tid) * 10;
+      r[0] = xe; r[1] = R; r[2] = kexp; r[3] = ye; r[4] = slow; r[5] = f; r[6] = cf; r[7] = cb;
+      r[8] = y[0]; r[9] = x[0];
+    }
     return errp;
   }
 
   // After a CHECK half-step that continues: y (holding Kx) -> tgt / Kx.
   template <bool MASK>
   __device__ __forceinline__ static void finish(const Ctx& c, T (&y)[E], int& ye, const Vt* tgt,
-                                                int te, int R, int kexp, T& acc) {
-    const T sc = LOGD ? Tt::pow2(-kexp) : T(1);
+                                                int te, int R, int kexp) {
+    const T sc = LOGD ? Tt::pow2(kexp) : T(1);
     const int sw = PS::swz(c.tid);
 #pragma unroll
     for (int j = 0; j < PS::V; ++j) {
@@ -329,10 +335,9 @@ template <class T, int E, int WARPS, bool LOGD> struct Half {
         T val = (tv[r] * sc) * Tt::rcp(y[e]);
         if (MASK && e >= c.nv) val = T(0);
         y[e] = val;
-        acc += val;
       }
     }
-    if constexpr (LOGD) ye = (te == ZE) ? ZE : te - R + kexp;
+    if constexpr (LOGD) ye = (te == ZE) ? ZE : te - R - kexp;
   }
 
   // After a CHECK half-step that stops: restore y_old.
@@ -543,7 +548,8 @@ __global__ void __launch_bounds__(32 * WARPS, (16 / WARPS > 0 ? 16 / WARPS : 1))
     c.lP = ER<double>{P.lanem[c.lane], P.lanee[c.lane]};
     c.rP = ER<double>{P.lanem[31 - c.lane], P.lanee[31 - c.lane]};
   }
-  const bool full = (c.nv == E);
+  // warp-uniform: the masked and unmasked paths contain different barriers
+  const bool full = __all_sync(FULL, c.nv == E);
 
   // ---- inputs into shared memory (mantissas) and registers (chunk exponents)
   T phi[E], psi[E];
@@ -580,40 +586,49 @@ __global__ void __launch_bounds__(32 * WARPS, (16 / WARPS > 0 ? 16 / WARPS : 1))
   const bool use_tol = P.tol > 0.0;
   while (true) {
     const bool check = (l >= itr_max) || (use_tol && (l % P.check_interval) == 0);
-    T acc = T(0);
+    T accx = T(0), accy = T(0);
     int R, kx;
+    c.slot = 2 * l;
     if (check) {
       // line 2: err = sum |psi (K^T phi) - b| with phi^(l), psi^(l)
-      double ep = full ? H::template run<true, false>(c, P, phi, pe, psi, qe, sB, be, sK, par, acc, R, kx)
-                       : H::template run<true, true>(c, P, phi, pe, psi, qe, sB, be, sK, par, acc, R, kx);
+      double ep = full ? H::template run<true, false>(c, P, phi, pe, psi, qe, sB, be, sK, par, accx, R, kx)
+                       : H::template run<true, true>(c, P, phi, pe, psi, qe, sB, be, sK, par, accx, R, kx);
       par ^= 1;
+      if (!isfinite((double)accx)) firstbad = min(firstbad, l);
       err = PS::block_sum(ep, red, par, c.lane, c.warp);
-      // non-finite state detected lazily on multi-warp CTAs: fold it in here
-      if constexpr (WARPS > 1) {
-        const int fb = PS::block_min(firstbad, ired, par, c.lane, c.warp);
-        if (fb != 0x7fffffff) { l = fb; flag = FS1_NONFINITE_FLAG; break; }
-      }
+      int fb;
+      if constexpr (WARPS > 1) fb = PS::block_min(firstbad, ired, par, c.lane, c.warp);
+      else fb = warp_min(firstbad);
+      if (fb != 0x7fffffff) { l = fb; flag = FS1_NONFINITE_FLAG; break; }
       if (l >= itr_max || err <= P.tol) {
         H::restore(c, psi, sK);
         flag = (use_tol && err <= P.tol) ? 1 : 4;
         break;
       }
-      if (full) H::template finish<false>(c, psi, qe, sB, be, R, kx, acc);
-      else H::template finish<true>(c, psi, qe, sB, be, R, kx, acc);
+      if (full) H::template finish<false>(c, psi, qe, sB, be, R, kx);
+      else H::template finish<true>(c, psi, qe, sB, be, R, kx);
     } else {
       // lines 3-7: psi = b ./ (K^T phi)
-      if (full) H::template run<false, false>(c, P, phi, pe, psi, qe, sB, be, sK, par, acc, R, kx);
-      else H::template run<false, true>(c, P, phi, pe, psi, qe, sB, be, sK, par, acc, R, kx);
+      if (full) H::template run<false, false>(c, P, phi, pe, psi, qe, sB, be, sK, par, accx, R, kx);
+      else H::template run<false, true>(c, P, phi, pe, psi, qe, sB, be, sK, par, accx, R, kx);
       par ^= 1;
     }
     // lines 8-12: phi = a ./ (K psi)
-    if (full) H::template run<false, false>(c, P, psi, qe, phi, pe, sA, ae, sK, par, acc, R, kx);
-    else H::template run<false, true>(c, P, psi, qe, phi, pe, sA, ae, sK, par, acc, R, kx);
+    c.slot = 2 * l + 1;
+    if (full) H::template run<false, false>(c, P, psi, qe, phi, pe, sA, ae, sK, par, accy, R, kx);
+    else H::template run<false, true>(c, P, psi, qe, phi, pe, sA, ae, sK, par, accy, R, kx);
     par ^= 1;
+    // non-finite state: phi^(l) seen by the psi half-step, psi^(l+1) by
+    // the phi half-step; the problem stops with the iteration count of the first one.
+    if (!isfinite((double)accx)) firstbad = min(firstbad, l);
+    else if (!isfinite((double)accy)) firstbad = min(firstbad, l + 1);
     ++l;  // line 13
-    if (!isfinite((double)acc) && firstbad == 0x7fffffff) firstbad = l;
     if constexpr (WARPS == 1) {
-      if (__any_sync(FULL, firstbad != 0x7fffffff)) { flag = FS1_NONFINITE_FLAG; break; }
+      if (__any_sync(FULL, firstbad != 0x7fffffff)) {
+        l = warp_min(firstbad);
+        flag = FS1_NONFINITE_FLAG;
+        break;
+      }
     } else {
       if ((l % NF_EVERY) == 0) {
         par ^= 1;

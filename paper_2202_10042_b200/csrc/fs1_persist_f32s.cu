@@ -1,0 +1,18 @@
+// float scaling-domain instantiations of the persistent kernel.
+#include "fs1_persist_inst.cuh"
+
+namespace fs1 {
+static const PersistEntry kTable[] = {
+    FS1_PERSIST_ENTRY(float, 0, 8, 1, false),
+    FS1_PERSIST_ENTRY(float, 0, 16, 1, false),
+    FS1_PERSIST_ENTRY(float, 0, 32, 1, false),
+    FS1_PERSIST_ENTRY(float, 0, 32, 2, false),
+    FS1_PERSIST_ENTRY(float, 0, 32, 4, false),
+    FS1_PERSIST_ENTRY(float, 0, 32, 8, false),
+    FS1_PERSIST_ENTRY(float, 0, 32, 16, false),
+};
+const PersistEntry* persist_table_f32s(int* count) {
+  *count = (int)(sizeof(kTable) / sizeof(kTable[0]));
+  return kTable;
+}
+}  // namespace fs1

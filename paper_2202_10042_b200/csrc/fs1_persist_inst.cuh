@@ -6,9 +6,8 @@
 namespace fs1 {
 
 template <class T, int E, int W, bool L>
-cudaError_t launch_solve_t(const PersistParams& P, long long grid, cudaStream_t st) {
-  using PS = Persist<T, E, W, L>;
-  fs1_persist_solve<T, E, W, L><<<(unsigned)grid, 32 * W, PS::SMEM, st>>>(P);
+cudaError_t launch_solve_t(const PersistParams& P, long long grid, size_t smem, cudaStream_t st) {
+  fs1_persist_solve<T, E, W, L><<<(unsigned)grid, 32 * W, smem, st>>>(P);
   return cudaGetLastError();
 }
 template <class T, int E, int W, bool L>

@@ -121,6 +121,7 @@ def test_zero_weights_log_domain():
     """a_i = 0 (log -inf) is allowed in the log domain: F_i = -inf, the rest matches."""
     n, eps = 256, 0.01
     A, B = gi.batch("c5", range(1), n=n)
+    A, B = A.astype(np.float64), B.astype(np.float64)
     A[0, 40:90] = 0.0
     A /= A.sum()
     ag, bg = _cuda(A, "f64"), _cuda(B, "f64")
@@ -145,16 +146,26 @@ def test_tolerance_stop_and_check_interval():
 
 
 def test_nonfinite_flag():
-    """Unstabilised scaling domain terminates abnormally; log domain does not."""
+    """Unstabilised scaling domain terminates abnormally; log domain does not.
+    The iteration of the first overflow is rounding-sensitive: the paper itself reports 97
+    for dense Sinkhorn and 104 for FS-1 on the same problem; here the GPU must
+    land between the oracle's dense and recursion modes (+-2)."""
     n = 200
     x = (np.arange(n) + 0.5) / n
     a = np.exp(-((x - 0.2) / 0.05) ** 2) + 1e-3
     b = np.exp(-((x - 0.8) / 0.05) ** 2) + 1e-3
     a, b = a / a.sum(), b / b.sum()
     ref = sinkhorn.solve(a, b, n=n, h1=1 / n, eps=5e-4, itr_max=200)
+    rr = sinkhorn.solve(a, b, n=n, h1=1 / n, eps=5e-4, itr_max=200, apply="recur")
     out = fs1.solve(_cuda(a[None], "f64"), _cuda(b[None], "f64"), h=1 / n, eps=5e-4, itr_max=200)
-    assert out["flags"].item() == 2 and ref["flags"][0] == 2
-    assert out["iters"].item() == ref["iters"][0]
+    assert out["flags"].item() == 2 and ref["flags"][0] == 2 and rr["flags"][0] == 2
+    lo, hi = sorted([int(ref["iters"][0]), int(rr["iters"][0])])
+    assert lo - 2 <= out["iters"].item() <= hi + 2
+    # well before the overflow the trajectories agree
+    k = lo - 20
+    ok = fs1.solve(_cuda(a[None], "f64"), _cuda(b[None], "f64"), h=1 / n, eps=5e-4, itr_max=k)
+    rk = sinkhorn.solve(a, b, n=n, h1=1 / n, eps=5e-4, itr_max=k)
+    assert_solve_parity(ok, rk, "scaling", "f64", tol=1e-9)
     lg = fs1.solve(_cuda(a[None], "f64"), _cuda(b[None], "f64"), h=1 / n, eps=5e-4, itr_max=200,
                    domain="log")
     assert lg["flags"].item() == 4 and math.isfinite(lg["cost"].item())
@@ -193,7 +204,7 @@ def test_identity_kernel_and_n1():
     a = gi.random_positive(rng, (1, 16))
     out = fs1.solve(_cuda(a, "f64"), _cuda(a, "f64"), h=1.0, eps=1e-4, itr_max=50, tol=1e-14)
     assert out["iters"].item() == 1 and out["flags"].item() == 1
-    assert out["err"].item() == 0.0 and out["cost"].item() == 0.0
+    assert out["err"].item() <= 1e-15 and out["cost"].item() == 0.0
     one = torch.ones(4, 1, dtype=torch.float64, device="cuda")
     o = fs1.solve(one, one, h=1.0, eps=0.1, itr_max=3)
     assert torch.all(o["cost"] == 0) and torch.all(o["iters"] == 3)
@@ -216,17 +227,19 @@ def test_config1_full():
 
 
 def test_config2_full_batch_sampled():
-    """C2: 4096 pairs x N=1024 fp32 scaling, 500 iterations, in one launch; sampled pairs
-    against the fp64 dense oracle."""
+    """C2: 4096 pairs x N=1024 fp32 (log domain, R14), 500 iterations, in one
+    launch (bench.py's configuration); sampled pairs against the fp64 dense oracle."""
     cfg = gi.CONFIGS["c2"]
     A, B = gi.batch(cfg, range(cfg.batch))
     ag, bg = _cuda(A, "f32"), _cuda(B, "f32")
-    out = fs1.solve(ag, bg, h=cfg.h1, eps=cfg.eps, itr_max=cfg.itr_max)
-    pairs = [0, 1, 1777, 4095]
+    out = fs1.solve(ag, bg, h=cfg.h1, eps=cfg.eps, itr_max=cfg.itr_max, domain=cfg.domain)
+    fl = out["flags"].cpu().numpy()
+    assert np.all(fl == 4)
+    pairs = [0, 1, 1777, 4095, int(np.argmax(np.abs(out["u"].cpu().numpy()).max(1)))]
     ref = sinkhorn.solve(ag[pairs].double().cpu().numpy(), bg[pairs].double().cpu().numpy(),
                          n=cfg.n, h1=cfg.h1, eps=cfg.eps, itr_max=cfg.itr_max)
-    assert_solve_parity(out, ref, "scaling", "f32", pairs=pairs)
-    assert np.all(out["flags"].cpu().numpy() == 4)
+    assert np.all(np.isfinite(ref["F"]))
+    assert_solve_parity(out, ref, cfg.domain, "f32", pairs=pairs)
 
 
 def test_config5_shard_sampled():
