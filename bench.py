@@ -338,6 +338,19 @@ def run_fs1(args, cfg):
                                 "kernel_ms": kern_avg_s * 1e3,
                                 "peak_source": f"derived: {props.multi_processor_count} SMs x "
                                                f"{clk_mhz:.0f} MHz x 16 MUFU/clk / 2 rcp per update"}
+        if info["kernel"].startswith("stream"):
+            # HBM roofline: SURVEY.md §8(d)'s 6 words per update (read x,
+            # tgt and write y in both half-steps) x N x iterations; the once-per-solve
+            # prologue, exit check, cost and epilogue passes (16 words per point) are
+            # real traffic but not counted, so the fraction is conservative.
+            wb = 8 if cfg.dtype == "f64" else 4
+            alg = 6 * wb * cfg.size * it_run
+            peak = peaks.get("hbm_gbs", 6650.0)
+            ach = alg / kern_avg_s / 1e9
+            line["roofline"] = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                                "frac": ach / peak, "traffic": profile_traffic(cfg.name),
+                                "kernel_ms": kern_avg_s * 1e3, "algorithmic_bytes_per_launch": alg,
+                                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({src})"}
         line["e2e"] = e2e
         if not args.no_cpu_baseline:
             pairs, it, what = sample_plan(cfg)

@@ -22,6 +22,13 @@
  *                         Q'_N = 0, Q'_k = lam (Q'_{k+1} + t_{k+1}) (t = inclusive backward sum)
  *                       (W x)_k = h (P'_k + Q'_k).  SURVEY.md §8(c) Q7 / DESIGN.md R7.
  *
+ * Precision: the log-sum-exp sweeps accumulate in x87 extended precision
+ * (long double, 64-bit significand).  In fp64 the sequential LSE recursion
+ * drifts by ~ulp(|R|) per step over its memory 1/(1 - lambda): at config 3
+ * (|F| ~ 1e4, 1/(1-lambda) ~ 1700) that is ~2e-9 relative in e^R, above the
+ * 1e-10 parity gate it has to certify (R24).  The recursion itself is
+ * unchanged; only its accumulator is wider.  Results are rounded to fp64.
+ *
  * Every routine works on `lines` independent lines of `n` points with element
  * stride `stride` and line stride `lstride` (2D: axis 1 = columns, contiguous;
  * axis 2 = rows, stride N; PAPER.md:244-255 column-major flattening).
@@ -31,11 +38,13 @@
 #include <math.h>
 #include <stdlib.h>
 
-static double lae(double a, double b) {           /* log(e^a + e^b) */
+typedef long double ld;
+
+static ld lae(ld a, ld b) {                        /* log(e^a + e^b), extended */
   if (a == -INFINITY) return b;
   if (b == -INFINITY) return a;
-  double m = a > b ? a : b;
-  return m + log1p(exp(-fabs(a - b)));
+  ld m = a > b ? a : b;
+  return m + log1pl(expl(-fabsl(a - b)));
 }
 
 void fs1o_sweep_scaling(const double* x, long n, long stride, long lines, long lstride,
@@ -65,16 +74,17 @@ void fs1o_sweep_log(const double* X, long n, long stride, long lines, long lstri
   for (long l = 0; l < lines; ++l) {
     const double* xl = X + l * lstride;
     double* yl = Y + l * lstride;
-    double* r = (double*)malloc(sizeof(double) * n);
-    double* s = (double*)malloc(sizeof(double) * n);
+    ld* r = (ld*)malloc(sizeof(ld) * n);
+    ld* s = (ld*)malloc(sizeof(ld) * n);
+    const ld C = (ld)c;
     r[0] = xl[0];
     s[n - 1] = -INFINITY;
     for (long i = 1; i <= n - 1; ++i) {
-      r[i] = lae(r[i - 1] - c, xl[i * stride]);
+      r[i] = lae(r[i - 1] - C, (ld)xl[i * stride]);
       long k = n - 1 - i;
-      s[k] = -c + lae(s[k + 1], xl[(k + 1) * stride]);
+      s[k] = -C + lae(s[k + 1], (ld)xl[(k + 1) * stride]);
     }
-    for (long i = 0; i < n; ++i) yl[i * stride] = lae(r[i], s[i]);
+    for (long i = 0; i < n; ++i) yl[i * stride] = (double)lae(r[i], s[i]);
     free(r);
     free(s);
   }
@@ -86,20 +96,21 @@ void fs1o_wsweep_log(const double* X, long n, long stride, long lines, long lstr
   for (long l = 0; l < lines; ++l) {
     const double* xl = X + l * lstride;
     double* yl = Y + l * lstride;
-    double* p = (double*)malloc(sizeof(double) * n);   /* log inclusive forward sums  */
-    double* t = (double*)malloc(sizeof(double) * n);   /* log inclusive backward sums */
-    double* P = (double*)malloc(sizeof(double) * n);   /* log P'                       */
-    double* Q = (double*)malloc(sizeof(double) * n);   /* log Q'                       */
+    ld* p = (ld*)malloc(sizeof(ld) * n);   /* log inclusive forward sums  */
+    ld* t = (ld*)malloc(sizeof(ld) * n);   /* log inclusive backward sums */
+    ld* P = (ld*)malloc(sizeof(ld) * n);   /* log P'                       */
+    ld* Q = (ld*)malloc(sizeof(ld) * n);   /* log Q'                       */
+    const ld C = (ld)c;
     p[0] = xl[0];
-    for (long i = 1; i < n; ++i) p[i] = lae(p[i - 1] - c, xl[i * stride]);
+    for (long i = 1; i < n; ++i) p[i] = lae(p[i - 1] - C, (ld)xl[i * stride]);
     t[n - 1] = xl[(n - 1) * stride];
-    for (long i = n - 2; i >= 0; --i) t[i] = lae(t[i + 1] - c, xl[i * stride]);
+    for (long i = n - 2; i >= 0; --i) t[i] = lae(t[i + 1] - C, (ld)xl[i * stride]);
     P[0] = -INFINITY;
-    for (long i = 1; i < n; ++i) P[i] = -c + lae(P[i - 1], p[i - 1]);
+    for (long i = 1; i < n; ++i) P[i] = -C + lae(P[i - 1], p[i - 1]);
     Q[n - 1] = -INFINITY;
-    for (long i = n - 2; i >= 0; --i) Q[i] = -c + lae(Q[i + 1], t[i + 1]);
-    double lh = log(h);
-    for (long i = 0; i < n; ++i) yl[i * stride] = lh + lae(P[i], Q[i]);
+    for (long i = n - 2; i >= 0; --i) Q[i] = -C + lae(Q[i + 1], t[i + 1]);
+    ld lh = logl((ld)h);
+    for (long i = 0; i < n; ++i) yl[i * stride] = (double)(lh + lae(P[i], Q[i]));
     free(p);
     free(t);
     free(P);
@@ -109,10 +120,10 @@ void fs1o_wsweep_log(const double* X, long n, long stride, long lines, long lstr
 
 /* sum_k exp(A_k + B_k) over n entries, in fp64 (cost and error reductions). */
 double fs1o_sum_exp2(const double* A, const double* B, long n) {
-  double s = 0.0;
+  ld s = 0.0L;
   for (long i = 0; i < n; ++i) {
-    double v = A[i] + B[i];
-    if (v != -INFINITY) s += exp(v);
+    ld v = (ld)A[i] + (ld)B[i];
+    if (v != -INFINITY) s += expl(v);
   }
-  return s;
+  return (double)s;
 }

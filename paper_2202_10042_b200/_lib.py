@@ -84,5 +84,9 @@ def lib():
         L.fs1_status_string.argtypes = [st]
         L.fs1_status_string.restype = ctypes.c_char_p
         L.fs1_abi_version.restype = ctypes.c_int
+        # test-only: plan with a forced kernel family (1 persistent, 2 streaming)
+        L.fs1__plan_kind.argtypes = [ctypes.POINTER(Desc), ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp),
+                                     ctypes.POINTER(ctypes.c_size_t)]
+        L.fs1__plan_kind.restype = st
         _lib = L
     return _lib

@@ -5,6 +5,7 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <algorithm>
 #include <mutex>
 #include <new>
 
@@ -20,6 +21,9 @@ struct fs1_plan_s {
   int kind;  // 0 persistent
   const PersistEntry* pe;
   PersistParams base;  // multipliers + scalars; pointers filled per call
+  const StreamEntry* se;
+  StreamParams sbase;  // K2: scalars + multiplier tables; pointers filled per call
+  int grid;            // K2: co-resident CTAs
   size_t smem;         // dynamic shared memory per CTA (>= the kernel's need; sized for occupancy)
   size_t ws;
   fs1_plan_info_t info;
@@ -28,6 +32,123 @@ struct fs1_plan_s {
 namespace {
 
 constexpr int KIND_PERSIST = 0;
+constexpr int KIND_STREAM = 1;
+void er_pow(long double c, long double L, double* m, int* e);
+constexpr int TILE = 256;
+
+size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+// workspace of the streaming kernel: 5 mantissa vectors + grid scratch
+struct StreamWs {
+  size_t Am, Bm, Pm, Qm0, Qm1, gtot, gtote, gtot2, gtot2e, bar, total;
+};
+StreamWs stream_ws(long long npad, int G) {
+  StreamWs w;
+  size_t o = 0;
+  const size_t v = al256((size_t)npad * 8);
+  w.Am = o; o += v;
+  w.Bm = o; o += v;
+  w.Pm = o; o += v;
+  w.Qm0 = o; o += v;
+  w.Qm1 = o; o += v;
+  w.gtot = o; o += al256((size_t)2 * G * 4 * 8);
+  w.gtote = o; o += al256((size_t)2 * G * 4 * 4);
+  w.gtot2 = o; o += al256((size_t)G * 8 * 8);
+  w.gtot2e = o; o += al256((size_t)G * 8 * 4);
+  w.bar = o; o += 256;
+  w.total = o;
+  return w;
+}
+
+void fill_stream_tables(StreamParams& P, double c) {
+  const long double C = (long double)c;
+  for (int k = 0; k < 5; ++k) P.lvd[k] = (double)expl(-C * (long double)(8 << k));
+  for (int l = 0; l < 32; ++l) P.lanepow[l] = (double)expl(-C * (long double)(8 * l));
+  for (int j = 0; j < 20; ++j) er_pow(C, (long double)TILE * (long double)(1LL << j), &P.t2m[j], &P.t2e[j]);
+}
+
+// Plan the K2 streaming kernel: G = SMs (one CTA per SM), the deepest TMA ring that
+// fits next to the per-tile tables.
+fs1_status plan_stream(fs1_plan_s* p, int device) {
+  const fs1_desc& d = p->d;
+  if (d.ndim != 1 || d.dtype != FS1_F64) return FS1_ERR_UNSUPPORTED;
+  int sms = 0, optin = 0;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return FS1_ERR_CUDA;
+  if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device) != cudaSuccess)
+    return FS1_ERR_CUDA;
+  const long long ntiles = (d.n + TILE - 1) / TILE;
+  if (ntiles > (1LL << 30)) return FS1_ERR_UNSUPPORTED;
+  const int G = (int)std::min<long long>(sms, ntiles);
+  const int ntmax = (int)((ntiles + G - 1) / G);
+  int cnt = 0;
+  const StreamEntry* tab = stream_table(&cnt);
+  const StreamEntry* best = nullptr;
+  size_t smem = 0;
+  for (int i = 0; i < cnt; ++i) {
+    const size_t need = stream_smem(tab[i].NW, tab[i].S, ntmax);
+    if (need <= (size_t)optin) { best = &tab[i]; smem = need; break; }
+  }
+  if (!best) return FS1_ERR_UNSUPPORTED;
+  if (cudaFuncSetAttribute(best->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return FS1_ERR_CUDA;
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, best->fn, 32 * best->NW, smem) != cudaSuccess)
+    return FS1_ERR_CUDA;
+  if (occ < 1) return FS1_ERR_UNSUPPORTED;
+  p->kind = KIND_STREAM;
+  p->se = best;
+  p->grid = G;
+  p->smem = smem;
+  StreamParams& P = p->sbase;
+  memset(&P, 0, sizeof(P));
+  P.n = d.n;
+  P.npad = ntiles * TILE;
+  P.ntiles = (int)ntiles;
+  P.G = G;
+  P.ntmax = ntmax;
+  P.lam = exp(-d.h1 / d.eps);
+  P.h = d.h1;
+  P.tol = d.tol;
+  P.itr_max = d.itr_max;
+  P.check_interval = d.check_interval;
+  P.warm = d.warm_start;
+  P.input_is_log = d.domain == FS1_LOG ? d.input_is_log : 0;
+  P.logd = d.domain == FS1_LOG;
+  fill_stream_tables(P, d.h1 / d.eps);
+  p->ws = stream_ws(P.npad, G).total;
+  snprintf(p->info.kernel, sizeof(p->info.kernel), "stream_f64_%s_NW%d_S%d", P.logd ? "log" : "scaling",
+           best->NW, best->S);
+  p->info.chunk = 8;
+  p->info.threads = 32 * best->NW;
+  p->info.ctas_per_problem = G;
+  p->info.grid = G;
+  p->info.smem_bytes = smem;
+  p->info.workspace_bytes = p->ws;
+  return FS1_OK;
+}
+
+StreamParams stream_params(const fs1_plan_s* p, void* ws) {
+  StreamParams P = p->sbase;
+  const StreamWs w = stream_ws(P.npad, P.G);
+  char* b = (char*)ws;
+  P.Am = (double*)(b + w.Am);
+  P.Bm = (double*)(b + w.Bm);
+  P.Pm = (double*)(b + w.Pm);
+  P.Qm0 = (double*)(b + w.Qm0);
+  P.Qm1 = (double*)(b + w.Qm1);
+  P.gtot = (double*)(b + w.gtot);
+  P.gtote = (int*)(b + w.gtote);
+  P.gtot2 = (double*)(b + w.gtot2);
+  P.gtot2e = (int*)(b + w.gtot2e);
+  P.bar = (unsigned*)(b + w.bar);
+  return P;
+}
+
+fs1_status launch_stream(const fs1_plan_s* p, StreamParams& P, cudaStream_t st) {
+  if (cudaMemsetAsync(P.bar, 0, 2 * sizeof(unsigned), st) != cudaSuccess) return FS1_ERR_CUDA;
+  const cudaError_t e = p->se->launch(P, p->grid, p->smem, st);
+  return e == cudaSuccess ? FS1_OK : FS1_ERR_CUDA;
+}
 
 // lambda^L as (mantissa in [1,2), exponent), from log2(lambda^L) = -L c / ln 2 in long double.
 void er_pow(long double c, long double L, double* m, int* e) {
@@ -122,7 +243,8 @@ const char* fs1_status_string(fs1_status s) {
   return "FS1_?: unknown status";
 }
 
-fs1_status fs1_plan(const fs1_desc* desc, int device, fs1_plan_t** out, size_t* workspace_bytes) {
+static fs1_status plan_impl(const fs1_desc* desc, int device, int force, fs1_plan_t** out,
+                            size_t* workspace_bytes) {
   if (!desc || !out) return FS1_ERR_ARG;
   *out = nullptr;
   const fs1_desc& d = *desc;
@@ -143,7 +265,15 @@ fs1_status fs1_plan(const fs1_desc* desc, int device, fs1_plan_t** out, size_t* 
   const bool logd = d.domain == FS1_LOG;
   const double c = d.h1 / d.eps;
 
-  if (d.ndim == 1) {
+  if (d.ndim == 1 && force == 2) {
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    int cur = 0;
+    if (cudaGetDevice(&cur) != cudaSuccess) { delete p; return FS1_ERR_CUDA; }
+    if (cur != device && cudaSetDevice(device) != cudaSuccess) { delete p; return FS1_ERR_CUDA; }
+    const fs1_status st = plan_stream(p, device);
+    if (cur != device) cudaSetDevice(cur);
+    if (st != FS1_OK) { delete p; return st; }
+  } else if (d.ndim == 1) {
     // persistent kernel: the smallest (E, W) instantiation whose 32 W E covers n
     const PersistEntry* (*tables[3])(int*) = {nullptr, nullptr, nullptr};
     if (d.dtype == FS1_F32) {
@@ -172,8 +302,18 @@ fs1_status fs1_plan(const fs1_desc* desc, int device, fs1_plan_t** out, size_t* 
      }
     }
     if (!best) {
-      delete p;
-      return FS1_ERR_UNSUPPORTED;
+      // too large for one CTA: the multi-CTA streaming kernel (fp64)
+      if (force == 1) { delete p; return FS1_ERR_UNSUPPORTED; }
+      std::lock_guard<std::mutex> lk(g_attr_mu);
+      int cur = 0;
+      if (cudaGetDevice(&cur) != cudaSuccess) { delete p; return FS1_ERR_CUDA; }
+      if (cur != device && cudaSetDevice(device) != cudaSuccess) { delete p; return FS1_ERR_CUDA; }
+      const fs1_status st = plan_stream(p, device);
+      if (cur != device) cudaSetDevice(cur);
+      if (st != FS1_OK) { delete p; return st; }
+      if (workspace_bytes) *workspace_bytes = p->ws;
+      *out = p;
+      return FS1_OK;
     }
     p->kind = KIND_PERSIST;
     p->pe = best;
@@ -222,6 +362,17 @@ fs1_status fs1_plan(const fs1_desc* desc, int device, fs1_plan_t** out, size_t* 
   return FS1_OK;
 }
 
+fs1_status fs1_plan(const fs1_desc* desc, int device, fs1_plan_t** out, size_t* workspace_bytes) {
+  return plan_impl(desc, device, 0, out, workspace_bytes);
+}
+
+// test-only (not in include/fs1.h): plan with a forced kernel family
+// (kind 1 persistent, 2 streaming) so the parity tests reach K2 at small n.
+fs1_status fs1__plan_kind(const fs1_desc* desc, int device, int kind, fs1_plan_t** out,
+                          size_t* workspace_bytes) {
+  return plan_impl(desc, device, kind, out, workspace_bytes);
+}
+
 // test-only (not in include/fs1.h): per-half-step trace of CTA 0 into buf
 // [2*itr_max+2][threads][10] doubles.
 fs1_status fs1__set_debug(fs1_plan_t* plan, double* buf) {
@@ -250,6 +401,22 @@ fs1_status fs1_solve(const fs1_plan_t* plan, const void* a, const void* b, void*
     cudaError_t e = plan->pe->launch_solve(P, plan->d.batch, plan->smem, (cudaStream_t)stream);
     return e == cudaSuccess ? FS1_OK : FS1_ERR_CUDA;
   }
+  if (plan->kind == KIND_STREAM) {
+    if (plan->d.domain != FS1_LOG) return FS1_ERR_UNSUPPORTED;
+    // one cooperative launch per problem, in order on the stream (shared workspace)
+    for (long long k = 0; k < plan->d.batch; ++k) {
+      StreamParams P = stream_params(plan, workspace);
+      const long long o = k * plan->d.n;
+      P.a = (const double*)a + o; P.b = (const double*)b + o;
+      P.u = (double*)u + o; P.v = (double*)v + o;
+      P.iters = iters ? iters + k : nullptr; P.err = err ? err + k : nullptr;
+      P.flags = flags ? flags + k : nullptr; P.cost = cost ? cost + k : nullptr;
+      P.mode = 0;
+      const fs1_status st = launch_stream(plan, P, (cudaStream_t)stream);
+      if (st != FS1_OK) return st;
+    }
+    return FS1_OK;
+  }
   return FS1_ERR_UNSUPPORTED;
 }
 
@@ -271,6 +438,18 @@ fs1_status fs1_cost(const fs1_plan_t* plan, const void* u, const void* v, double
     cudaError_t e = plan->pe->launch_solve(P, plan->d.batch, plan->smem, (cudaStream_t)stream);
     return e == cudaSuccess ? FS1_OK : FS1_ERR_CUDA;
   }
+  if (plan->kind == KIND_STREAM) {
+    for (long long k = 0; k < plan->d.batch; ++k) {
+      StreamParams P = stream_params(plan, workspace);
+      const long long o = k * plan->d.n;
+      P.u = (double*)const_cast<void*>(u) + o; P.v = (double*)const_cast<void*>(v) + o;
+      P.cost = cost + k;
+      P.mode = 2;
+      const fs1_status st = launch_stream(plan, P, (cudaStream_t)stream);
+      if (st != FS1_OK) return st;
+    }
+    return FS1_OK;
+  }
   return FS1_ERR_UNSUPPORTED;
 }
 
@@ -280,6 +459,17 @@ fs1_status fs1_apply(const fs1_plan_t* plan, const void* x, void* y, void* works
   if (plan->kind == KIND_PERSIST) {
     cudaError_t e = plan->pe->launch_apply(plan->base, x, y, plan->d.batch, (cudaStream_t)stream);
     return e == cudaSuccess ? FS1_OK : FS1_ERR_CUDA;
+  }
+  if (plan->kind == KIND_STREAM) {
+    for (long long k = 0; k < plan->d.batch; ++k) {
+      StreamParams P = stream_params(plan, workspace);
+      const long long o = k * plan->d.n;
+      P.x = (const double*)x + o; P.y = (double*)y + o;
+      P.mode = 1;
+      const fs1_status st = launch_stream(plan, P, (cudaStream_t)stream);
+      if (st != FS1_OK) return st;
+    }
+    return FS1_OK;
   }
   return FS1_ERR_UNSUPPORTED;
 }

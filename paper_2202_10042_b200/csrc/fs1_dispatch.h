@@ -25,4 +25,13 @@ const PersistEntry* persist_table_f32l2(int* count);
 const PersistEntry* persist_table_f64s(int* count);
 const PersistEntry* persist_table_f64l(int* count);
 
+// K2 streaming kernel (fs1_stream.cu)
+struct StreamEntry {
+  int NW, S;
+  const void* fn;
+  cudaError_t (*launch)(const StreamParams&, int grid, size_t smem, cudaStream_t);
+};
+const StreamEntry* stream_table(int* count);
+size_t stream_smem(int NW, int S, int ntmax);
+
 }  // namespace fs1

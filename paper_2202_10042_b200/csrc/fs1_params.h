@@ -42,4 +42,50 @@ struct PersistParams {
   int lanee[32];
 };
 
+
+// Multi-CTA HBM-streaming kernel (K2 in SURVEY.md §2.2), fp64, one problem per launch.
+// The state lives in the workspace as mantissas with one binary exponent per 256-point
+// tile; tile exponents and scan tables stay in shared memory of
+// the CTA that owns the tile range for the whole solve.
+struct StreamParams {
+  const void* a;     // [n] histograms (fp64; log-weights when input_is_log)
+  const void* b;
+  void* u;           // [n] out (in when warm): F = log phi (or phi for the apply/scaling views)
+  void* v;
+  int32_t* iters;
+  double* err;
+  int32_t* flags;
+  double* cost;
+  const void* x;     // apply: input  [n]
+  void* y;           // apply: output [n]
+  double* Am;        // workspace mantissas [npad]
+  double* Bm;
+  double* Pm;        // phi state
+  double* Qm0;       // psi state, ping-pong pair (check iterations keep psi^(l))
+  double* Qm1;
+  double* gtot;      // [2 parity][G][4]: forward total m, backward total m, err, cost
+  int* gtote;        // [2 parity][G][4]: forward total e, backward total e, flag, cost e
+  double* gtot2;     // [G][8] cost-phase range totals (p, P', t, Q') m
+  int* gtot2e;       // [G][8]
+  unsigned* bar;     // grid barrier {count, generation}
+  long long n;
+  long long npad;    // ntiles * 256
+  int ntiles;
+  int G;             // CTAs (co-resident)
+  int ntmax;         // max tiles per CTA
+  double lam;
+  double h;
+  double tol;
+  int itr_max;
+  int check_interval;
+  int warm;
+  int input_is_log;
+  int mode;          // 0 solve, 1 apply, 2 cost
+  int logd;          // 1: u, v, x, y are logs; 0: linear
+  double lvd[5];     // lambda^{8 * 2^k}
+  double lanepow[32];  // lambda^{8 l}
+  double t2m[20];    // lambda^{256 * 2^j} as mantissa in [1,2) ...
+  int t2e[20];       // ... and binary exponent (Remark 3.3: never formed alone in fp64)
+};
+
 }  // namespace fs1

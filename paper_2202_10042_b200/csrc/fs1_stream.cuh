@@ -1,0 +1,1140 @@
+// fs1_stream.cuh — K2: the multi-CTA HBM-streaming FS-1 kernel for one large 1D
+// problem (fp64, log domain; N = 2^24).
+//
+// The whole solve (Algorithm 1) is ONE cooperative launch of G
+// co-resident CTAs (one per SM).  CTA r owns the contiguous tile range
+// [T0_r, T1_r) of 256-point tiles for every vector and every half-step, so the
+// per-tile scan tables and tile exponents of the vectors it produces stay in its
+// shared memory; only 2 extended-range words per CTA cross the grid per
+// half-step.  One half-step x -> y = tgt ./ (K x) (Alg. 1 lines 3-7 / 8-12):
+//
+//  [A] after the grid barrier: warp 0 folds the other CTAs' range totals of x
+//      into this range's external forward/backward carries; every tile's full
+//      carries = local exclusive carries (made by this CTA when it produced x)
+//      + lambda^{256 i} x external carry;
+//  [B] each warp streams its tiles: 1D TMA bulk copies (cp.async.bulk, mbarrier
+//      complete_tx) of x and tgt into a private S-stage shared-memory ring, a
+//      conflict-free XOR-swizzled read into registers (8 points per lane), lane
+//      Horner aggregates, a 5-level warp shuffle scan, the forward and backward
+//      recursions of Eq. "recursion" from the exact carries,
+//      y = tgt * rcp(p + lambda t), one exact power-of-two renormalisation of the
+//      output tile, the output tile's scan totals, and a TMA bulk store of y;
+//  [C] a block scan of the produced tiles' totals gives their local exclusive
+//      carries (kept for the next half-step) and this range's totals, which are
+//      published before the grid barrier.
+//
+// Per update the kernel reads x, tgt and writes y once per half-step: 48 B per
+// grid-point update in fp64 (+8 B on check iterations for psi^(l)), the
+// algorithmic minimum of SURVEY.md §8(d).  Values are mantissas with one binary
+// exponent per tile: the log domain costs one exp per point at
+// load and one log at store per solve, none per iteration.
+#pragma once
+#include <math.h>
+#include <stdint.h>
+
+#include "fs1_common.cuh"
+#include "fs1_params.h"
+
+namespace fs1 {
+namespace stm {
+
+constexpr int E = 8;                // points per lane
+constexpr int TILE = 32 * E;        // points per warp tile
+constexpr int TBYTES = TILE * 8;    // bytes per fp64 tile
+constexpr int LIM = 600;            // carries up to 2^LIM above a tile keep the tile's exponent
+constexpr int MODE_SOLVE = 0, MODE_APPLY = 1, MODE_COST = 2;
+constexpr double LN2_HI = 6.93147180369123816490e-01;  // Cody-Waite split of ln 2
+constexpr double LN2_LO = 1.90821492927058770002e-10;
+constexpr double INV_LN2 = 1.44269504088896338700e+00;
+
+// ------------------------------------------------------------------ shared layout
+struct Layout {
+  size_t stage, outb, mbar, pwm, pwe, ax, bx, px, qx0, qx1, pfm, pbm, pfe, pbe, qfm, qbm, qfe,
+      qbe, cfr, cbr, rr, errt, redm, rede, total;
+};
+
+__host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~(size_t)15; }
+
+__host__ __device__ inline Layout layout(int NW, int S, int ntmax) {
+  Layout L;
+  size_t o = 0;
+  const size_t nt = (size_t)ntmax + 1;
+  L.stage = o; o = al16(o + (size_t)NW * S * 2 * TBYTES);
+  L.outb = o;  o = al16(o + (size_t)NW * 2 * TBYTES);
+  L.mbar = o;  o = al16(o + (size_t)NW * S * 8);
+  L.pwm = o;   o = al16(o + nt * 8);
+  L.pfm = o;   o = al16(o + nt * 8);
+  L.pbm = o;   o = al16(o + nt * 8);
+  L.qfm = o;   o = al16(o + nt * 8);
+  L.qbm = o;   o = al16(o + nt * 8);
+  L.cfr = o;   o = al16(o + nt * 8);
+  L.cbr = o;   o = al16(o + nt * 8);
+  L.errt = o;  o = al16(o + nt * 8);
+  L.redm = o;  o = al16(o + 16 * 64 * 8);
+  L.pwe = o;   o = al16(o + nt * 4);
+  L.ax = o;    o = al16(o + nt * 4);
+  L.bx = o;    o = al16(o + nt * 4);
+  L.px = o;    o = al16(o + nt * 4);
+  L.qx0 = o;   o = al16(o + nt * 4);
+  L.qx1 = o;   o = al16(o + nt * 4);
+  L.pfe = o;   o = al16(o + nt * 4);
+  L.pbe = o;   o = al16(o + nt * 4);
+  L.qfe = o;   o = al16(o + nt * 4);
+  L.qbe = o;   o = al16(o + nt * 4);
+  L.rr = o;    o = al16(o + nt * 4);
+  L.rede = o;  o = al16(o + 16 * 64 * 4);
+  L.total = o;
+  return L;
+}
+
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ unsigned su32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned cnt) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(cnt) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(su32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* b) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          su32(dst)),
+      "l"(src), "r"(bytes), "r"(su32(b))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(su32(src)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() {
+  asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async() { asm volatile("fence.proxy.async;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Grid-wide barrier of the co-resident CTAs (cooperative launch guarantees
+// residency).  bar[0] counts arrivals, bar[1] is the generation.
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned G, unsigned& gen) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    fence_async();
+    __threadfence();
+    const unsigned g = gen;
+    const unsigned prev = atomicAdd(bar, 1u);
+    if (prev == G - 1) {
+      atomicExch(bar, 0u);
+      __threadfence();
+      st_release(bar + 1, g + 1);
+    } else {
+      while (ld_acquire(bar + 1) == g) __nanosleep(20);
+    }
+    __threadfence();
+    fence_async();
+  }
+  ++gen;
+  __syncthreads();
+}
+
+// ------------------------------------------------------------------ swizzled tiles
+// Lane l owns points [8l, 8l+8) of a tile = 4 double2 chunks at 16-byte slots
+// 4l..4l+3.  Instruction j touches chunk j ^ sw(l), sw = (l>>1)&3: the 8 lanes of
+// a 128-bit phase then hit 8 distinct 16-byte bank groups (no conflicts); two
+// conditional swaps restore the natural order in registers.
+__device__ __forceinline__ void csw(double2& a, double2& b, bool c) {
+  const double2 x = a, y = b;
+  a.x = c ? y.x : x.x; a.y = c ? y.y : x.y;
+  b.x = c ? x.x : y.x; b.y = c ? x.y : y.y;
+}
+__device__ __forceinline__ void lds_tile(const double* base, int lane, double (&v)[E]) {
+  const int sw = (lane >> 1) & 3;
+  const double2* p = reinterpret_cast<const double2*>(base) + lane * 4;
+  double2 r0 = p[0 ^ sw], r1 = p[1 ^ sw], r2 = p[2 ^ sw], r3 = p[3 ^ sw];
+  csw(r0, r1, sw & 1); csw(r2, r3, sw & 1);
+  csw(r0, r2, sw & 2); csw(r1, r3, sw & 2);
+  v[0] = r0.x; v[1] = r0.y; v[2] = r1.x; v[3] = r1.y;
+  v[4] = r2.x; v[5] = r2.y; v[6] = r3.x; v[7] = r3.y;
+}
+__device__ __forceinline__ void sts_tile(double* base, int lane, const double (&v)[E]) {
+  const int sw = (lane >> 1) & 3;
+  double2 r0 = make_double2(v[0], v[1]), r1 = make_double2(v[2], v[3]);
+  double2 r2 = make_double2(v[4], v[5]), r3 = make_double2(v[6], v[7]);
+  csw(r0, r2, sw & 2); csw(r1, r3, sw & 2);
+  csw(r0, r1, sw & 1); csw(r2, r3, sw & 1);
+  double2* p = reinterpret_cast<double2*>(base) + lane * 4;
+  p[0 ^ sw] = r0; p[1 ^ sw] = r1; p[2 ^ sw] = r2; p[3 ^ sw] = r3;
+}
+// plain blocked global access (prologue / epilogue / cost phase)
+__device__ __forceinline__ void ldg_tile(const double* g, int lane, double (&v)[E]) {
+  const double2* p = reinterpret_cast<const double2*>(g + lane * E);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const double2 t = __ldcg(p + j);
+    v[2 * j] = t.x;
+    v[2 * j + 1] = t.y;
+  }
+}
+__device__ __forceinline__ void stg_tile(double* g, int lane, const double (&v)[E]) {
+  double2* p = reinterpret_cast<double2*>(g + lane * E);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) p[j] = make_double2(v[2 * j], v[2 * j + 1]);
+}
+
+// ------------------------------------------------------------------ context
+struct Ctx {
+  int tid, lane, warp, NT, NW;
+  int r, T0, nt;
+  double* stage;
+  double* outb;
+  uint64_t* mbar;
+  double* pwm;
+  int* pwe;
+  int* AX;
+  int* BX;
+  int* PX;
+  int* QX[2];
+  double *PFm, *PBm, *QFm, *QBm;
+  int *PFe, *PBe, *QFe, *QBe;
+  double* cfr;
+  double* cbr;
+  int* Rr;
+  double* errt;
+  double* redm;
+  int* rede;
+  unsigned phase;
+  unsigned gen;
+};
+
+__device__ __forceinline__ ER<double> pw(const Ctx& c, int k) { return ER<double>{c.pwm[k], c.pwe[k]}; }
+__device__ __forceinline__ ER<double> er_fma(ER<double> a, ER<double> b, ER<double> d) {
+  return er_add(er_mul(a, b), d);
+}
+// lambda^{256 k} for any k by binary decomposition (host-formed lambda^{256 2^j})
+__device__ __forceinline__ ER<double> pow_tiles(const StreamParams& P, long long k) {
+  ER<double> r{1.0, 0};
+  for (int j = 0; j < 20 && k; ++j, k >>= 1)
+    if (k & 1) r = er_mul(r, ER<double>{P.t2m[j], P.t2e[j]});
+  return r;
+}
+__device__ __forceinline__ long long range_T0(const StreamParams& P, int r) {
+  return (long long)r * P.ntiles / P.G;
+}
+__device__ __forceinline__ ER<double> warp_er_sum(ER<double> a) {
+  const int M = warp_max(a.m > 0.0 ? a.e : ZE);
+  double s = (a.m > 0.0) ? a.m * pow2d(max(a.e - M, -1100)) : 0.0;
+  s = warp_sum(s);
+  return er_norm<double>(s, M);
+}
+__device__ __forceinline__ int expo_d(double m) { return Tr<double>::expo(m); }
+
+// ---------------------------------------------------------------- tile aggregates
+// Lane Horner aggregates and the warp scan of a tile held 8 points per lane.
+// Returns the inclusive scans: Fi (forward, lane 31 = tile total at the tile end),
+// Gi (backward, lane 0 = tile total at the tile start).
+__device__ __forceinline__ void tile_scan_lanes(const StreamParams& P, int lane, const double (&v)[E],
+                                                double& Fi, double& Gi) {
+  const double lam = P.lam;
+  double f = 0.0, g = 0.0;
+#pragma unroll
+  for (int e = 0; e < E; ++e) f = fma(lam, f, v[e]);
+#pragma unroll
+  for (int e = E - 1; e >= 0; --e) g = fma(lam, g, v[e]);
+  Fi = f;
+  Gi = g;
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    const int d = 1 << k;
+    const double up = __shfl_up_sync(FULL, Fi, d);
+    const double dn = __shfl_down_sync(FULL, Gi, d);
+    if (lane >= d) Fi = fma(P.lvd[k], up, Fi);
+    if (lane + d < 32) Gi = fma(P.lvd[k], dn, Gi);
+  }
+}
+
+// Store the tile totals of a produced tile (exponent Y) into the table at i.
+__device__ __forceinline__ void put_totals(int lane, double Fi, double Gi, int Y, double* Fm, int* Fe,
+                                           double* Bm, int* Be, int i) {
+  if (lane == 31) {
+    const ER<double> t = er_norm<double>(Fi, Y);
+    Fm[i] = t.m;
+    Fe[i] = t.e;
+  }
+  if (lane == 0) {
+    const ER<double> t = er_norm<double>(Gi, Y);
+    Bm[i] = t.m;
+    Be[i] = t.e;
+  }
+}
+
+// ---------------------------------------------------------------- block tile scan
+// In: F/B hold per-tile totals (forward at the tile end, backward at the tile start).
+// Out (in place): exclusive local carries CFloc_i = sum_{i'<i} lambda^{256(i-1-i')} FT_i',
+// CBloc_i = sum_{i'>i} lambda^{256(i'-i-1)} GT_i'; returns the range totals.
+__device__ void block_tile_scan(Ctx& c, double* Fm, int* Fe, double* Bm, int* Be, ER<double>& totF,
+                                ER<double>& totB) {
+  const int nt = c.nt, NT = c.NT, lane = c.lane, warp = c.warp;
+  const int q = (nt + NT - 1) / NT;
+  const int i0 = min(nt, c.tid * q), i1 = min(nt, i0 + q);
+  const ER<double> L1 = pw(c, 1);
+  ER<double> f = er_zero<double>(), g = er_zero<double>();
+  for (int i = i0; i < i1; ++i) f = er_fma(f, L1, ER<double>{Fm[i], Fe[i]});
+  for (int i = i1 - 1; i >= i0; --i) g = er_fma(g, L1, ER<double>{Bm[i], Be[i]});
+  int sF = i1 - i0, sG = i1 - i0;
+  ER<double> F = f, G = g;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const ER<double> uf = shfl_up_er(F, d);
+    const int us = __shfl_up_sync(FULL, sF, d);
+    const ER<double> dg = shfl_down_er(G, d);
+    const int ds = __shfl_down_sync(FULL, sG, d);
+    if (lane >= d) { F = er_fma(uf, pw(c, sF), F); sF += us; }
+    if (lane + d < 32) { G = er_fma(dg, pw(c, sG), G); sG += ds; }
+  }
+  ER<double> eF = shfl_up_er(F, 1);
+  int esF = __shfl_up_sync(FULL, sF, 1);
+  ER<double> eG = shfl_down_er(G, 1);
+  int esG = __shfl_down_sync(FULL, sG, 1);
+  if (lane == 0) { eF = er_zero<double>(); esF = 0; }
+  if (lane == 31) { eG = er_zero<double>(); esG = 0; }
+  double* wFm = c.redm;
+  double* wGm = c.redm + 64;
+  int* wFe = c.rede;
+  int* wGe = c.rede + 64;
+  int* wFs = c.rede + 128;
+  int* wGs = c.rede + 192;
+  __syncthreads();  // scratch reuse
+  if (lane == 31) { wFm[warp] = F.m; wFe[warp] = F.e; wFs[warp] = sF; }
+  if (lane == 0) { wGm[warp] = G.m; wGe[warp] = G.e; wGs[warp] = sG; }
+  __syncthreads();
+  ER<double> cw = er_zero<double>(), cg = er_zero<double>();
+  for (int w = 0; w < warp; ++w) cw = er_fma(cw, pw(c, wFs[w]), ER<double>{wFm[w], wFe[w]});
+  for (int w = c.NW - 1; w > warp; --w) cg = er_fma(cg, pw(c, wGs[w]), ER<double>{wGm[w], wGe[w]});
+  ER<double> cf = er_fma(cw, pw(c, esF), eF);
+  ER<double> cb = er_fma(cg, pw(c, esG), eG);
+  for (int i = i0; i < i1; ++i) {
+    const ER<double> t{Fm[i], Fe[i]};
+    Fm[i] = cf.m; Fe[i] = cf.e;
+    cf = er_fma(cf, L1, t);
+  }
+  for (int i = i1 - 1; i >= i0; --i) {
+    const ER<double> t{Bm[i], Be[i]};
+    Bm[i] = cb.m; Be[i] = cb.e;
+    cb = er_fma(cb, L1, t);
+  }
+  __syncthreads();
+  if (c.tid == NT - 1) { wFm[0] = cf.m; wFe[0] = cf.e; }
+  if (c.tid == 0) { wGm[0] = cb.m; wGe[0] = cb.e; }
+  __syncthreads();
+  totF = ER<double>{wFm[0], wFe[0]};
+  totB = ER<double>{wGm[0], wGe[0]};
+  __syncthreads();
+}
+
+// Deterministic block sum (fixed tree) of per-tile ER values vm/ve[0..nt).
+__device__ ER<double> block_er_sum(Ctx& c, const double* vm, const int* ve) {
+  const int nt = c.nt, NT = c.NT;
+  const int q = (nt + NT - 1) / NT;
+  const int i0 = min(nt, c.tid * q), i1 = min(nt, i0 + q);
+  ER<double> s = er_zero<double>();
+  for (int i = i0; i < i1; ++i) s = er_add(s, ER<double>{vm[i], ve[i]});
+  s = warp_er_sum(s);
+  __syncthreads();
+  if (c.lane == 0) { c.redm[c.warp] = s.m; c.rede[c.warp] = s.e; }
+  __syncthreads();
+  ER<double> t = er_zero<double>();
+  for (int w = 0; w < c.NW; ++w) t = er_add(t, ER<double>{c.redm[w], c.rede[w]});
+  __syncthreads();
+  return t;
+}
+
+// ---------------------------------------------------------------- external carries
+// Warp 0: fold the other ranges' totals (slot par) into this range's carries.
+__device__ void ext_carries(Ctx& c, const StreamParams& P, int par, ER<double>& CFx, ER<double>& CBx) {
+  const double* gt = P.gtot + (size_t)par * P.G * 4;
+  const int* ge = P.gtote + (size_t)par * P.G * 4;
+  const int r = c.r, lane = c.lane;
+  // forward: ranges [0, r)
+  {
+    const int q = (r + 31) / 32;
+    const int s0 = min(r, lane * q), s1 = min(r, s0 + q);
+    ER<double> acc = er_zero<double>();
+    for (int k = s0; k < s1; ++k) {
+      const int len = (int)(range_T0(P, k + 1) - range_T0(P, k));
+      acc = er_fma(acc, pw(c, len), ER<double>{__ldcg(gt + 4 * k), __ldcg(ge + 4 * k)});
+    }
+    if (s1 > s0) acc = er_mul(acc, pow_tiles(P, range_T0(P, r) - range_T0(P, s1)));
+    CFx = warp_er_sum(acc);
+  }
+  // backward: ranges (r, G)
+  {
+    const int nb = P.G - 1 - r;
+    const int q = (nb + 31) / 32;
+    const int s0 = r + 1 + min(nb, lane * q), s1 = r + 1 + min(nb, lane * q + q);
+    ER<double> acc = er_zero<double>();
+    for (int k = s1 - 1; k >= s0; --k) {
+      const int len = (int)(range_T0(P, k + 1) - range_T0(P, k));
+      acc = er_fma(acc, pw(c, len), ER<double>{__ldcg(gt + 4 * k + 1), __ldcg(ge + 4 * k + 1)});
+    }
+    if (s1 > s0) acc = er_mul(acc, pow_tiles(P, range_T0(P, s0) - range_T0(P, r + 1)));
+    CBx = warp_er_sum(acc);
+  }
+}
+
+// [A]: full per-tile carries of the consumed vector x (tables F/B, exponents Xx).
+__device__ void tile_carries(Ctx& c, const StreamParams& P, int par, const double* Fm, const int* Fe,
+                             const double* Bm, const int* Be, const int* Xx) {
+  if (c.warp == 0) {
+    ER<double> CFx, CBx;
+    ext_carries(c, P, par, CFx, CBx);
+    if (c.lane == 0) {
+      c.redm[0] = CFx.m; c.rede[0] = CFx.e;
+      c.redm[1] = CBx.m; c.rede[1] = CBx.e;
+    }
+  }
+  __syncthreads();
+  const ER<double> CFx{c.redm[0], c.rede[0]}, CBx{c.redm[1], c.rede[1]};
+  for (int i = c.tid; i < c.nt; i += c.NT) {
+    const ER<double> CF = er_fma(pw(c, i), CFx, ER<double>{Fm[i], Fe[i]});
+    const ER<double> CB = er_fma(pw(c, c.nt - 1 - i), CBx, ER<double>{Bm[i], Be[i]});
+    const int X = Xx[i];
+    int R = X;
+    if (X == ZE || CF.e - X > LIM || CB.e - X > LIM) R = max(CF.e, CB.e);
+    if (R == ZE) R = 0;
+    c.cfr[i] = er_rel(CF, R);
+    c.cbr[i] = er_rel(CB, R);
+    c.Rr[i] = R;
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------- streamed half-step
+struct HalfArgs {
+  const double* xg;  // consumed mantissas
+  const int* Xx;     // consumed tile exponents
+  const double* tg;  // target mantissas (a or b)
+  const int* Xt;
+  const double* og;  // psi^(l) for the check (CHECK)
+  const int* Xo;
+  double* yg;        // produced mantissas (WRITE)
+  int* Xy;
+  double *yFm, *yBm;
+  int *yFe, *yBe;
+};
+
+// DIV: y = tgt / Kx (solve) else y = Kx (apply); CHECK: accumulate the marginal
+// error sum |psi_old (Kx) - tgt| per tile; WRITE: produce y.
+template <int NW, int S, bool DIV, bool CHECK, bool WRITE>
+__device__ void stream_half(Ctx& c, const StreamParams& P, const HalfArgs& A, int& nonfinite) {
+  const int lane = c.lane, w = c.warp;
+  const long long gbase = (long long)c.T0 * TILE;
+  double* stg = c.stage + (size_t)w * S * 2 * TILE;
+  uint64_t* mb = c.mbar + w * S;
+  constexpr bool LOADT = DIV || CHECK;
+  const double lam = P.lam;
+  const double lp = P.lanepow[lane], rp = P.lanepow[31 - lane];
+
+  auto issue = [&](int k) {
+    const int i = w + k * NW;
+    if (i >= c.nt) return;
+    const int s = k % S;
+    mbar_expect_tx(&mb[s], LOADT ? 2 * TBYTES : TBYTES);
+    bulk_g2s(stg + (s * 2) * TILE, A.xg + gbase + (long long)i * TILE, TBYTES, &mb[s]);
+    if (LOADT) bulk_g2s(stg + (s * 2 + 1) * TILE, A.tg + gbase + (long long)i * TILE, TBYTES, &mb[s]);
+  };
+  if (lane == 0) {
+    fence_async();
+#pragma unroll
+    for (int k = 0; k < S; ++k) issue(k);
+  }
+  int bad = 0;
+  int k = 0;
+  for (int i = w; i < c.nt; i += NW, ++k) {
+    const int s = k % S;
+    mbar_wait(&mb[s], (c.phase >> s) & 1u);
+    c.phase ^= (1u << s);
+    double xv[E], tv[E], ov[E];
+    lds_tile(stg + (s * 2) * TILE, lane, xv);
+    if (LOADT) lds_tile(stg + (s * 2 + 1) * TILE, lane, tv);
+    __syncwarp();
+    if (lane == 0) issue(k + S);
+    if (CHECK) ldg_tile(A.og + gbase + (long long)i * TILE, lane, ov);
+
+    const int X = A.Xx[i];
+    const int R = c.Rr[i];
+    if (X != R) {  // carries far above the tile: compute relative to 2^R (warp-uniform)
+      const double sc = pow2d(max(X - R, -1100));
+#pragma unroll
+      for (int e = 0; e < E; ++e) xv[e] *= sc;
+    }
+    // carries into this lane's chunk
+    double Fi, Gi;
+    tile_scan_lanes(P, lane, xv, Fi, Gi);
+    double cf = __shfl_up_sync(FULL, Fi, 1);
+    double cb = __shfl_down_sync(FULL, Gi, 1);
+    if (lane == 0) cf = 0.0;
+    if (lane == 31) cb = 0.0;
+    cf = fma(lp, c.cfr[i], cf);
+    cb = fma(rp, c.cbr[i], cb);
+    // forward recursion p_k = lam p_{k-1} + x_k (Alg. 1 line 5 / 10)
+    double pf[E];
+    double p = cf;
+#pragma unroll
+    for (int e = 0; e < E; ++e) { p = fma(lam, p, xv[e]); pf[e] = p; }
+    // backward recursion t_k = lam t_{k+1} + x_k, K x = p + lam t_{k+1} (line 6 / 11)
+    // fused with the update y = tgt / (K x) (line 7 / 12)
+    double tn = cb;
+    double errp = 0.0;
+    double sce = 0.0;
+    if (CHECK) sce = pow2d(min(max(A.Xo[i] + R - A.Xt[i], -1100), 1000));
+    double yv[E];
+#pragma unroll
+    for (int e = E - 1; e >= 0; --e) {
+      const double kx = fma(lam, tn, pf[e]);
+      tn = fma(lam, tn, xv[e]);
+      if (CHECK) errp += fabs(fma(ov[e] * sce, kx, -tv[e]));
+      if (WRITE) {
+        if (DIV) yv[e] = (tv[e] > 0.0) ? tv[e] * __drcp_rn(kx) : 0.0;
+        else yv[e] = kx;
+      }
+    }
+    if (CHECK) {
+      const double es = warp_sum(errp);
+      if (lane == 0) c.errt[i] = ldexp(es, A.Xt[i]);
+    }
+    if (WRITE) {
+      // exact power-of-two renormalisation of the output tile
+      double ym = 0.0;
+#pragma unroll
+      for (int e = 0; e < E; ++e) ym = fmax(ym, yv[e]);
+      const int M = warp_max(ym > 0.0 ? expo_d(ym) : ZE);
+      const int base = DIV ? (A.Xt[i] == ZE ? ZE : A.Xt[i] - R) : R;
+      int Y = ZE;
+      if (M != ZE && base != ZE) {
+        const double s1 = pow2d(-(M / 2)), s2 = pow2d(-(M - M / 2));
+#pragma unroll
+        for (int e = 0; e < E; ++e) yv[e] = (yv[e] * s1) * s2;
+        Y = base + M;
+      } else {
+#pragma unroll
+        for (int e = 0; e < E; ++e) yv[e] = 0.0;
+      }
+      double FiY, GiY;
+      tile_scan_lanes(P, lane, yv, FiY, GiY);
+      if (!isfinite(FiY + GiY)) bad = 1;
+      put_totals(lane, FiY, GiY, Y, A.yFm, A.yFe, A.yBm, A.yBe, i);
+      if (lane == 0) A.Xy[i] = Y;
+      // stage through the out ring and bulk-store the tile
+      double* ob = c.outb + (size_t)(w * 2 + (k & 1)) * TILE;
+      if (lane == 0) bulk_wait_read1();
+      __syncwarp();
+      sts_tile(ob, lane, yv);
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        bulk_s2g(A.yg + gbase + (long long)i * TILE, ob, TBYTES);
+        bulk_commit();
+      }
+    }
+  }
+  if (WRITE && lane == 0) bulk_wait_all();
+  if (__any_sync(FULL, bad)) nonfinite = 1;
+}
+
+// ---------------------------------------------------------------- prologue/epilogue
+// Convert a user vector (linear, log, or the constant init) of tile i into
+// mantissas + tile exponent, write the mantissas, return them in registers.
+__device__ void to_tile(const Ctx& c, const StreamParams& P, const double* src, int kind, double init,
+                        double* dst, int i, double (&m)[E], int& X) {
+  // kind: 0 linear, 1 log, 2 constant init
+  const int lane = c.lane;
+  const long long g0 = ((long long)c.T0 + i) * TILE + lane * E;
+  double v[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const bool ok = g0 + e < P.n;
+    if (kind == 2) v[e] = ok ? init : 0.0;
+    else v[e] = ok ? __ldcg(src + g0 + e) : (kind == 1 ? -INFINITY : 0.0);
+  }
+  if (kind == 1) {
+    double M = -INFINITY;
+#pragma unroll
+    for (int e = 0; e < E; ++e) M = fmax(M, v[e]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) M = fmax(M, __shfl_xor_sync(FULL, M, o));
+    if (M == -INFINITY) {
+      X = ZE;
+#pragma unroll
+      for (int e = 0; e < E; ++e) m[e] = 0.0;
+    } else if (!isfinite(M)) {
+      X = 0;
+#pragma unroll
+      for (int e = 0; e < E; ++e) m[e] = NAN;
+    } else {
+      X = (int)floor(M * INV_LN2);
+      const double xh = (double)X * LN2_HI, xl = (double)X * LN2_LO;
+#pragma unroll
+      for (int e = 0; e < E; ++e) m[e] = (v[e] == -INFINITY) ? 0.0 : exp((v[e] - xh) - xl);
+    }
+  } else {
+    double M = 0.0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) M = fmax(M, v[e]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) M = fmax(M, __shfl_xor_sync(FULL, M, o));
+    if (!(M > 0.0)) {
+      X = ZE;
+#pragma unroll
+      for (int e = 0; e < E; ++e) m[e] = 0.0;
+    } else {
+      X = expo_d(M);
+      const double s1 = pow2d(-(X / 2)), s2 = pow2d(-(X - X / 2));
+#pragma unroll
+      for (int e = 0; e < E; ++e) m[e] = (v[e] * s1) * s2;
+    }
+  }
+  stg_tile(dst + ((long long)c.T0 + i) * TILE, lane, m);
+}
+
+__device__ void from_tile(const Ctx& c, const StreamParams& P, const double* srcm, int X, bool logd,
+                          double* dst, int i) {
+  const int lane = c.lane;
+  double m[E];
+  ldg_tile(srcm + ((long long)c.T0 + i) * TILE, lane, m);
+  const long long g0 = ((long long)c.T0 + i) * TILE + lane * E;
+  const double xh = (double)X * LN2_HI, xl = (double)X * LN2_LO;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    if (g0 + e < P.n) {
+      double o;
+      if (logd) o = (m[e] > 0.0 && X != ZE) ? (log(m[e]) + xl) + xh : (m[e] == 0.0 ? -INFINITY : NAN);
+      else o = (X == ZE) ? 0.0 : ldexp(m[e], X);
+      dst[g0 + e] = o;
+    }
+  }
+}
+
+// Convert a user vector into a state buffer with its tile exponents and scan totals.
+__device__ void load_vector(Ctx& c, const StreamParams& P, const double* src, int kind, double init,
+                            double* dst, int* Xt, double* Fm, int* Fe, double* Bm, int* Be) {
+  for (int i = c.warp; i < c.nt; i += c.NW) {
+    double m[E];
+    int X;
+    to_tile(c, P, src, kind, init, dst, i, m, X);
+    if (c.lane == 0) Xt[i] = X;
+    if (Fm) {
+      double Fi, Gi;
+      tile_scan_lanes(P, c.lane, m, Fi, Gi);
+      put_totals(c.lane, Fi, Gi, X, Fm, Fe, Bm, Be, i);
+    }
+  }
+}
+
+// ---------------------------------------------------------------- cost phase
+// Return line: h sum_k phi_k (P'_k + Q'_k) with the Jordan-block
+// recursions P'_k = lam (P'_{k-1} + p_{k-1}), Q'_k = lam (Q'_{k+1} + t_{k+1}) over psi
+// (R7), as a grid-wide scan of the pairs (p, P') and (t, Q').
+struct Pair {
+  ER<double> a, b;  // (p, P') or (t, Q')
+};
+// combine(A left/near, B right/far) over span L (points) of the far part: forward
+// (p, P'): p = l^L pA + pB, P' = l^L (P'A + L pA) + P'B; backward is the mirror image.
+__device__ __forceinline__ Pair pcomb(Pair A, Pair B, ER<double> lL, double L) {
+  Pair r;
+  r.a = er_fma(A.a, lL, B.a);
+  r.b = er_fma(er_add(A.b, er_scale(A.a, L)), lL, B.b);
+  return r;
+}
+__device__ __forceinline__ Pair pzero() { return Pair{er_zero<double>(), er_zero<double>()}; }
+__device__ __forceinline__ Pair shfl_up_pair(Pair x, int d) { return Pair{shfl_up_er(x.a, d), shfl_up_er(x.b, d)}; }
+__device__ __forceinline__ Pair shfl_down_pair(Pair x, int d) {
+  return Pair{shfl_down_er(x.a, d), shfl_down_er(x.b, d)};
+}
+
+// lane-level Jordan aggregates and warp scans in plain fp64 relative to the tile exponent
+__device__ __forceinline__ void jordan_lanes(const StreamParams& P, int lane, const double (&v)[E],
+                                             double& fp, double& fP, double& bt, double& bQ) {
+  const double lam = P.lam;
+  double p = 0, Pp = 0, t = 0, Q = 0;
+#pragma unroll
+  for (int e = 0; e < E; ++e) { Pp = lam * (Pp + p); p = fma(lam, p, v[e]); }
+#pragma unroll
+  for (int e = E - 1; e >= 0; --e) { Q = lam * (Q + t); t = fma(lam, t, v[e]); }
+  fp = p; fP = Pp; bt = t; bQ = Q;
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    const int d = 1 << k;
+    const double L = (double)(E << k), l = P.lvd[k];
+    const double up = __shfl_up_sync(FULL, fp, d), uP = __shfl_up_sync(FULL, fP, d);
+    const double dt = __shfl_down_sync(FULL, bt, d), dQ = __shfl_down_sync(FULL, bQ, d);
+    if (lane >= d) { fP = fma(l, fma(L, up, uP), fP); fp = fma(l, up, fp); }
+    if (lane + d < 32) { bQ = fma(l, fma(L, dt, dQ), bQ); bt = fma(l, dt, bt); }
+  }
+}
+
+__device__ void block_pair_scan(Ctx& c, double* Am, int* Ae, double* A2m, int* A2e, double* Bm, int* Be,
+                                double* B2m, int* B2e, Pair& totF, Pair& totB) {
+  const int nt = c.nt, NT = c.NT, lane = c.lane, warp = c.warp;
+  const int q = (nt + NT - 1) / NT;
+  const int i0 = min(nt, c.tid * q), i1 = min(nt, i0 + q);
+  const ER<double> L1 = pw(c, 1);
+  Pair f = pzero(), g = pzero();
+  for (int i = i0; i < i1; ++i)
+    f = pcomb(f, Pair{ER<double>{Am[i], Ae[i]}, ER<double>{A2m[i], A2e[i]}}, L1, (double)TILE);
+  for (int i = i1 - 1; i >= i0; --i)
+    g = pcomb(g, Pair{ER<double>{Bm[i], Be[i]}, ER<double>{B2m[i], B2e[i]}}, L1, (double)TILE);
+  int sF = i1 - i0, sG = i1 - i0;
+  Pair F = f, G = g;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const Pair uf = shfl_up_pair(F, d);
+    const int us = __shfl_up_sync(FULL, sF, d);
+    const Pair dg = shfl_down_pair(G, d);
+    const int ds = __shfl_down_sync(FULL, sG, d);
+    if (lane >= d) { F = pcomb(uf, F, pw(c, sF), (double)TILE * sF); sF += us; }
+    if (lane + d < 32) { G = pcomb(dg, G, pw(c, sG), (double)TILE * sG); sG += ds; }
+  }
+  Pair eF = shfl_up_pair(F, 1), eG = shfl_down_pair(G, 1);
+  int esF = __shfl_up_sync(FULL, sF, 1), esG = __shfl_down_sync(FULL, sG, 1);
+  if (lane == 0) { eF = pzero(); esF = 0; }
+  if (lane == 31) { eG = pzero(); esG = 0; }
+  double* wm = c.redm;  // [4][64]
+  int* we = c.rede;     // [4][64] + spans [2][64] at 256
+  __syncthreads();
+  if (lane == 31) {
+    wm[warp] = F.a.m; we[warp] = F.a.e; wm[64 + warp] = F.b.m; we[64 + warp] = F.b.e;
+    we[256 + warp] = sF;
+  }
+  if (lane == 0) {
+    wm[128 + warp] = G.a.m; we[128 + warp] = G.a.e; wm[192 + warp] = G.b.m; we[192 + warp] = G.b.e;
+    we[320 + warp] = sG;
+  }
+  __syncthreads();
+  Pair cw = pzero(), cg = pzero();
+  for (int w = 0; w < warp; ++w)
+    cw = pcomb(cw, Pair{ER<double>{wm[w], we[w]}, ER<double>{wm[64 + w], we[64 + w]}}, pw(c, we[256 + w]),
+               (double)TILE * we[256 + w]);
+  for (int w = c.NW - 1; w > warp; --w)
+    cg = pcomb(cg, Pair{ER<double>{wm[128 + w], we[128 + w]}, ER<double>{wm[192 + w], we[192 + w]}},
+               pw(c, we[320 + w]), (double)TILE * we[320 + w]);
+  Pair cf = pcomb(cw, eF, pw(c, esF), (double)TILE * esF);
+  Pair cb = pcomb(cg, eG, pw(c, esG), (double)TILE * esG);
+  for (int i = i0; i < i1; ++i) {
+    const Pair t{ER<double>{Am[i], Ae[i]}, ER<double>{A2m[i], A2e[i]}};
+    Am[i] = cf.a.m; Ae[i] = cf.a.e; A2m[i] = cf.b.m; A2e[i] = cf.b.e;
+    cf = pcomb(cf, t, L1, (double)TILE);
+  }
+  for (int i = i1 - 1; i >= i0; --i) {
+    const Pair t{ER<double>{Bm[i], Be[i]}, ER<double>{B2m[i], B2e[i]}};
+    Bm[i] = cb.a.m; Be[i] = cb.a.e; B2m[i] = cb.b.m; B2e[i] = cb.b.e;
+    cb = pcomb(cb, t, L1, (double)TILE);
+  }
+  __syncthreads();
+  if (c.tid == NT - 1) { wm[0] = cf.a.m; we[0] = cf.a.e; wm[1] = cf.b.m; we[1] = cf.b.e; }
+  if (c.tid == 0) { wm[2] = cb.a.m; we[2] = cb.a.e; wm[3] = cb.b.m; we[3] = cb.b.e; }
+  __syncthreads();
+  totF = Pair{ER<double>{wm[0], we[0]}, ER<double>{wm[1], we[1]}};
+  totB = Pair{ER<double>{wm[2], we[2]}, ER<double>{wm[3], we[3]}};
+  __syncthreads();
+}
+
+// cost of the state (Pm, Xp) = phi, (Qm, Xq) = psi; returns the value on every CTA.
+template <int NW>
+__device__ double cost_phase(Ctx& c, const StreamParams& P, const double* Pm, const int* Xp,
+                             const double* Qm, const int* Xq) {
+  const int lane = c.lane;
+  // tables: forward (p, P') in PF/PB, backward (t, Q') in QF/QB
+  double *Am = c.PFm, *A2m = c.PBm, *Bm = c.QFm, *B2m = c.QBm;
+  int *Ae = c.PFe, *A2e = c.PBe, *Be = c.QFe, *B2e = c.QBe;
+  for (int i = c.warp; i < c.nt; i += NW) {
+    double v[E];
+    ldg_tile(Qm + ((long long)c.T0 + i) * TILE, lane, v);
+    double fp, fP, bt, bQ;
+    jordan_lanes(P, lane, v, fp, fP, bt, bQ);
+    const int X = Xq[i];
+    if (lane == 31) {
+      ER<double> t = er_norm<double>(fp, X); Am[i] = t.m; Ae[i] = t.e;
+      t = er_norm<double>(fP, X); A2m[i] = t.m; A2e[i] = t.e;
+    }
+    if (lane == 0) {
+      ER<double> t = er_norm<double>(bt, X); Bm[i] = t.m; Be[i] = t.e;
+      t = er_norm<double>(bQ, X); B2m[i] = t.m; B2e[i] = t.e;
+    }
+  }
+  __syncthreads();
+  Pair tF, tB;
+  block_pair_scan(c, Am, Ae, A2m, A2e, Bm, Be, B2m, B2e, tF, tB);
+  if (c.tid == 0) {
+    double* g = P.gtot2 + (size_t)c.r * 8;
+    int* ge = P.gtot2e + (size_t)c.r * 8;
+    g[0] = tF.a.m; ge[0] = tF.a.e; g[1] = tF.b.m; ge[1] = tF.b.e;
+    g[2] = tB.a.m; ge[2] = tB.a.e; g[3] = tB.b.m; ge[3] = tB.b.e;
+  }
+  grid_barrier(P.bar, P.G, c.gen);
+  // external pair carries (warp 0)
+  if (c.warp == 0) {
+    const int r = c.r;
+    Pair ef, eb;
+    {
+      const int q = (r + 31) / 32;
+      const int s0 = min(r, lane * q), s1 = min(r, s0 + q);
+      Pair acc = pzero();
+      for (int k = s0; k < s1; ++k) {
+        const int len = (int)(range_T0(P, k + 1) - range_T0(P, k));
+        const double* g = P.gtot2 + (size_t)k * 8;
+        const int* ge = P.gtot2e + (size_t)k * 8;
+        acc = pcomb(acc, Pair{ER<double>{__ldcg(g), __ldcg(ge)}, ER<double>{__ldcg(g + 1), __ldcg(ge + 1)}},
+                    pw(c, len), (double)TILE * len);
+      }
+      if (s1 > s0) {
+        const long long d = range_T0(P, r) - range_T0(P, s1);
+        acc = pcomb(acc, pzero(), pow_tiles(P, d), (double)TILE * d);
+      }
+      // sum of independent contributions: (p, P') add component-wise
+      ef.a = warp_er_sum(acc.a);
+      ef.b = warp_er_sum(acc.b);
+    }
+    {
+      const int nb = P.G - 1 - r;
+      const int q = (nb + 31) / 32;
+      const int s0 = r + 1 + min(nb, lane * q), s1 = r + 1 + min(nb, lane * q + q);
+      Pair acc = pzero();
+      for (int k = s1 - 1; k >= s0; --k) {
+        const int len = (int)(range_T0(P, k + 1) - range_T0(P, k));
+        const double* g = P.gtot2 + (size_t)k * 8;
+        const int* ge = P.gtot2e + (size_t)k * 8;
+        acc = pcomb(acc, Pair{ER<double>{__ldcg(g + 2), __ldcg(ge + 2)}, ER<double>{__ldcg(g + 3), __ldcg(ge + 3)}},
+                    pw(c, len), (double)TILE * len);
+      }
+      if (s1 > s0) {
+        const long long d = range_T0(P, s0) - range_T0(P, r + 1);
+        acc = pcomb(acc, pzero(), pow_tiles(P, d), (double)TILE * d);
+      }
+      eb.a = warp_er_sum(acc.a);
+      eb.b = warp_er_sum(acc.b);
+    }
+    if (lane == 0) {
+      c.redm[500] = ef.a.m; c.rede[500] = ef.a.e; c.redm[501] = ef.b.m; c.rede[501] = ef.b.e;
+      c.redm[502] = eb.a.m; c.rede[502] = eb.a.e; c.redm[503] = eb.b.m; c.rede[503] = eb.b.e;
+    }
+  }
+  __syncthreads();
+  const Pair EF{ER<double>{c.redm[500], c.rede[500]}, ER<double>{c.redm[501], c.rede[501]}};
+  const Pair EB{ER<double>{c.redm[502], c.rede[502]}, ER<double>{c.redm[503], c.rede[503]}};
+  // full per-tile carries relative to R (in place: A/A2 <- forward, B/B2 <- backward)
+  for (int i = c.tid; i < c.nt; i += c.NT) {
+    const Pair cf = pcomb(EF, Pair{ER<double>{Am[i], Ae[i]}, ER<double>{A2m[i], A2e[i]}}, pw(c, i),
+                          (double)TILE * i);
+    const int sb = c.nt - 1 - i;
+    const Pair cb = pcomb(EB, Pair{ER<double>{Bm[i], Be[i]}, ER<double>{B2m[i], B2e[i]}}, pw(c, sb),
+                          (double)TILE * sb);
+    const int X = Xq[i];
+    const int mx = max(max(cf.a.e, cf.b.e), max(cb.a.e, cb.b.e));
+    int R = X;
+    if (X == ZE || mx - X > LIM) R = mx;
+    if (R == ZE) R = 0;
+    Am[i] = er_rel(cf.a, R); A2m[i] = er_rel(cf.b, R);
+    Bm[i] = er_rel(cb.a, R); B2m[i] = er_rel(cb.b, R);
+    c.Rr[i] = R;
+  }
+  __syncthreads();
+  // per-tile weighted dot sum_k phi_k (P'_k + Q'_k)
+  const double lam = P.lam;
+  for (int i = c.warp; i < c.nt; i += NW) {
+    double v[E], ph[E];
+    ldg_tile(Qm + ((long long)c.T0 + i) * TILE, lane, v);
+    ldg_tile(Pm + ((long long)c.T0 + i) * TILE, lane, ph);
+    const int X = Xq[i], R = c.Rr[i];
+    if (X != R) {
+      const double sc = pow2d(max(X - R, -1100));
+#pragma unroll
+      for (int e = 0; e < E; ++e) v[e] *= sc;
+    }
+    double fp, fP, bt, bQ;
+    jordan_lanes(P, lane, v, fp, fP, bt, bQ);
+    // lane-exclusive values
+    double xp = __shfl_up_sync(FULL, fp, 1), xP = __shfl_up_sync(FULL, fP, 1);
+    double xt = __shfl_down_sync(FULL, bt, 1), xQ = __shfl_down_sync(FULL, bQ, 1);
+    if (lane == 0) { xp = 0; xP = 0; }
+    if (lane == 31) { xt = 0; xQ = 0; }
+    // combine with the tile carries over span 8 lane (forward) / 8 (31 - lane) (backward)
+    const double Lf = (double)(E * lane), Lb = (double)(E * (31 - lane));
+    const double lf = P.lanepow[lane], lb = P.lanepow[31 - lane];
+    const double cp = Am[i], cP = A2m[i], ct = Bm[i], cQ = B2m[i];
+    double p = fma(lf, cp, xp), Pp = fma(lf, fma(Lf, cp, cP), xP);
+    double t = fma(lb, ct, xt), Q = fma(lb, fma(Lb, ct, cQ), xQ);
+    double acc = 0.0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) { Pp = lam * (Pp + p); p = fma(lam, p, v[e]); acc = fma(ph[e], Pp, acc); }
+#pragma unroll
+    for (int e = E - 1; e >= 0; --e) { Q = lam * (Q + t); t = fma(lam, t, v[e]); acc = fma(ph[e], Q, acc); }
+    const double s = warp_sum(acc);
+    if (lane == 0) {
+      const ER<double> t2 = (Xp[i] == ZE) ? er_zero<double>() : er_norm<double>(s, R + Xp[i]);
+      c.errt[i] = t2.m;
+      c.Rr[i] = t2.e;
+    }
+  }
+  __syncthreads();
+  const ER<double> tot = block_er_sum(c, c.errt, c.Rr);
+  if (c.tid == 0) {
+    P.gtot2[(size_t)c.r * 8 + 4] = tot.m;
+    P.gtot2e[(size_t)c.r * 8 + 4] = tot.e;
+  }
+  grid_barrier(P.bar, P.G, c.gen);
+  // every CTA folds the G partials in the same fixed order
+  ER<double> s = er_zero<double>();
+  for (int k = lane; k < P.G; k += 32)
+    s = er_add(s, ER<double>{__ldcg(P.gtot2 + (size_t)k * 8 + 4), __ldcg(P.gtot2e + (size_t)k * 8 + 4)});
+  s = warp_er_sum(s);
+  return (s.m == 0.0) ? 0.0 : ldexp(s.m, s.e) * P.h;
+}
+
+// ---------------------------------------------------------------- publish / read
+__device__ void publish(Ctx& c, const StreamParams& P, int slot, ER<double> F, ER<double> B, double errs,
+                        int flag) {
+  if (c.tid == 0) {
+    double* g = P.gtot + ((size_t)slot * P.G + c.r) * 4;
+    int* ge = P.gtote + ((size_t)slot * P.G + c.r) * 4;
+    g[0] = F.m; ge[0] = F.e;
+    g[1] = B.m; ge[1] = B.e;
+    g[2] = errs; ge[2] = flag;
+  }
+}
+// totals over ranges of slot: error sum (fixed order) and OR of flags (warp 0 result
+// broadcast through shared memory)
+__device__ void read_slot(Ctx& c, const StreamParams& P, int slot, double& err, int& flag) {
+  if (c.warp == 0) {
+    double s = 0.0;
+    int f = 0;
+    for (int k = c.lane; k < P.G; k += 32) {
+      s += __ldcg(P.gtot + ((size_t)slot * P.G + k) * 4 + 2);
+      f |= __ldcg(P.gtote + ((size_t)slot * P.G + k) * 4 + 2);
+    }
+    s = warp_sum(s);
+    f = __reduce_or_sync(FULL, (unsigned)f);
+    if (c.lane == 0) { c.redm[510] = s; c.rede[510] = f; }
+  }
+  __syncthreads();
+  err = c.redm[510];
+  flag = c.rede[510];
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------- the kernel
+template <int NW, int S>
+__global__ void __launch_bounds__(32 * NW, 1) fs1_stream_kernel(const StreamParams P) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  Ctx c;
+  c.NW = NW;
+  c.NT = 32 * NW;
+  c.tid = threadIdx.x;
+  c.lane = c.tid & 31;
+  c.warp = c.tid >> 5;
+  c.r = blockIdx.x;
+  c.T0 = (int)range_T0(P, c.r);
+  c.nt = (int)(range_T0(P, c.r + 1) - c.T0);
+  const Layout L = layout(NW, S, P.ntmax);
+  c.stage = reinterpret_cast<double*>(smem + L.stage);
+  c.outb = reinterpret_cast<double*>(smem + L.outb);
+  c.mbar = reinterpret_cast<uint64_t*>(smem + L.mbar);
+  c.pwm = reinterpret_cast<double*>(smem + L.pwm);
+  c.pwe = reinterpret_cast<int*>(smem + L.pwe);
+  c.AX = reinterpret_cast<int*>(smem + L.ax);
+  c.BX = reinterpret_cast<int*>(smem + L.bx);
+  c.PX = reinterpret_cast<int*>(smem + L.px);
+  c.QX[0] = reinterpret_cast<int*>(smem + L.qx0);
+  c.QX[1] = reinterpret_cast<int*>(smem + L.qx1);
+  c.PFm = reinterpret_cast<double*>(smem + L.pfm);
+  c.PBm = reinterpret_cast<double*>(smem + L.pbm);
+  c.QFm = reinterpret_cast<double*>(smem + L.qfm);
+  c.QBm = reinterpret_cast<double*>(smem + L.qbm);
+  c.PFe = reinterpret_cast<int*>(smem + L.pfe);
+  c.PBe = reinterpret_cast<int*>(smem + L.pbe);
+  c.QFe = reinterpret_cast<int*>(smem + L.qfe);
+  c.QBe = reinterpret_cast<int*>(smem + L.qbe);
+  c.cfr = reinterpret_cast<double*>(smem + L.cfr);
+  c.cbr = reinterpret_cast<double*>(smem + L.cbr);
+  c.Rr = reinterpret_cast<int*>(smem + L.rr);
+  c.errt = reinterpret_cast<double*>(smem + L.errt);
+  c.redm = reinterpret_cast<double*>(smem + L.redm);
+  c.rede = reinterpret_cast<int*>(smem + L.rede);
+  c.phase = 0;
+  c.gen = 0;
+
+  if (c.lane == 0) {
+    for (int s = 0; s < S; ++s) mbar_init(&c.mbar[c.warp * S + s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int k = c.tid; k <= P.ntmax; k += c.NT) {
+    const ER<double> t = pow_tiles(P, k);
+    c.pwm[k] = t.m;
+    c.pwe[k] = t.e;
+  }
+  for (int i = c.tid; i < c.nt; i += c.NT) c.errt[i] = 0.0;
+  __syncthreads();
+
+  const double* dA = reinterpret_cast<const double*>(P.a);
+  const double* dB = reinterpret_cast<const double*>(P.b);
+  double* dU = reinterpret_cast<double*>(P.u);
+  double* dV = reinterpret_cast<double*>(P.v);
+  double* Qm[2] = {P.Qm0, P.Qm1};
+  int nonfinite = 0;
+
+  if (P.mode == MODE_APPLY) {
+    load_vector(c, P, reinterpret_cast<const double*>(P.x), P.logd ? 1 : 0, 0.0, P.Pm, c.PX, c.PFm, c.PFe,
+                c.PBm, c.PBe);
+    __syncthreads();
+    ER<double> tF, tB;
+    block_tile_scan(c, c.PFm, c.PFe, c.PBm, c.PBe, tF, tB);
+    publish(c, P, 0, tF, tB, 0.0, 0);
+    grid_barrier(P.bar, P.G, c.gen);
+    tile_carries(c, P, 0, c.PFm, c.PFe, c.PBm, c.PBe, c.PX);
+    HalfArgs A{P.Pm, c.PX, nullptr, nullptr, nullptr, nullptr, P.Qm0, c.QX[0],
+               c.QFm, c.QBm, c.QFe, c.QBe};
+    stream_half<NW, S, false, false, true>(c, P, A, nonfinite);
+    __syncthreads();
+    fence_async();
+    __syncthreads();
+    for (int i = c.warp; i < c.nt; i += NW)
+      from_tile(c, P, P.Qm0, c.QX[0][i], P.logd, reinterpret_cast<double*>(P.y), i);
+    return;
+  }
+  if (P.mode == MODE_COST) {
+    load_vector(c, P, dU, P.logd ? 1 : 0, 0.0, P.Pm, c.PX, nullptr, nullptr, nullptr, nullptr);
+    load_vector(c, P, dV, P.logd ? 1 : 0, 0.0, P.Qm0, c.QX[0], nullptr, nullptr, nullptr, nullptr);
+    __syncthreads();
+    grid_barrier(P.bar, P.G, c.gen);
+    const double cost = cost_phase<NW>(c, P, P.Pm, c.PX, P.Qm0, c.QX[0]);
+    if (c.r == 0 && c.tid == 0 && P.cost) P.cost[0] = cost;
+    return;
+  }
+
+  // ---------------- solve (Algorithm 1)
+  const int kin = P.input_is_log ? 1 : 0;
+  load_vector(c, P, dA, kin, 0.0, P.Am, c.AX, nullptr, nullptr, nullptr, nullptr);
+  load_vector(c, P, dB, kin, 0.0, P.Bm, c.BX, nullptr, nullptr, nullptr, nullptr);
+  const double init = 1.0 / (double)P.n;  // phi0 = psi0 = 1/N
+  load_vector(c, P, dU, P.warm ? 1 : 2, init, P.Pm, c.PX, c.PFm, c.PFe, c.PBm, c.PBe);
+  load_vector(c, P, dV, P.warm ? 1 : 2, init, Qm[0], c.QX[0], nullptr, nullptr, nullptr, nullptr);
+  __syncthreads();
+  int par = 0;
+  {
+    ER<double> tF, tB;
+    block_tile_scan(c, c.PFm, c.PFe, c.PBm, c.PBe, tF, tB);
+    publish(c, P, par, tF, tB, 0.0, 0);
+    grid_barrier(P.bar, P.G, c.gen);
+  }
+  const bool use_tol = P.tol > 0.0;
+  int l = 0, qi = 0, flag = 0;
+  double errv = NAN;
+  while (true) {
+    const bool check = (l >= P.itr_max) || (use_tol && (l % P.check_interval) == 0);
+    const bool last = l >= P.itr_max;
+    // ---- lines 2-7: psi = b ./ (K^T phi), with the marginal error on check iterations
+    tile_carries(c, P, par, c.PFm, c.PFe, c.PBm, c.PBe, c.PX);
+    const int qo = check ? (qi ^ 1) : qi;  // a checking step keeps psi^(l) in Qm[qi]
+    HalfArgs A{P.Pm, c.PX, P.Bm, c.BX, Qm[qi], c.QX[qi], Qm[qo], c.QX[qo], c.QFm, c.QBm, c.QFe, c.QBe};
+    nonfinite = 0;
+    if (!check) stream_half<NW, S, true, false, true>(c, P, A, nonfinite);
+    else if (!last) stream_half<NW, S, true, true, true>(c, P, A, nonfinite);
+    else stream_half<NW, S, true, true, false>(c, P, A, nonfinite);
+    __syncthreads();
+    {
+      ER<double> tF = er_zero<double>(), tB = er_zero<double>();
+      if (!last) block_tile_scan(c, c.QFm, c.QFe, c.QBm, c.QBe, tF, tB);
+      double es = 0.0;
+      if (check) {
+        // deterministic per-range error sum
+        double* em = c.errt;
+        const int q = (c.nt + c.NT - 1) / c.NT;
+        const int i0 = min(c.nt, c.tid * q), i1 = min(c.nt, i0 + q);
+        double s = 0.0;
+        for (int i = i0; i < i1; ++i) s += em[i];
+        s = warp_sum(s);
+        __syncthreads();
+        if (c.lane == 0) c.redm[c.warp] = s;
+        __syncthreads();
+        for (int w = 0; w < NW; ++w) es += c.redm[w];
+        __syncthreads();
+      }
+      const int nf = __syncthreads_or(nonfinite);
+      publish(c, P, par ^ 1, tF, tB, es, nf);
+      grid_barrier(P.bar, P.G, c.gen);
+      par ^= 1;
+    }
+    {
+      double e;
+      int f;
+      read_slot(c, P, par, e, f);
+      if (check) {
+        errv = e;
+        if (last || errv <= P.tol) {
+          flag = (use_tol && errv <= P.tol) ? 1 : 4;
+          break;
+        }
+        qi ^= 1;
+      }
+      if (f) { ++l; flag = 2; break; }
+    }
+    // ---- lines 8-12: phi = a ./ (K psi)
+    tile_carries(c, P, par, c.QFm, c.QFe, c.QBm, c.QBe, c.QX[qi]);
+    HalfArgs B{Qm[qi], c.QX[qi], P.Am, c.AX, nullptr, nullptr, P.Pm, c.PX, c.PFm, c.PBm, c.PFe, c.PBe};
+    nonfinite = 0;
+    stream_half<NW, S, true, false, true>(c, P, B, nonfinite);
+    __syncthreads();
+    {
+      ER<double> tF, tB;
+      block_tile_scan(c, c.PFm, c.PFe, c.PBm, c.PBe, tF, tB);
+      const int nf = __syncthreads_or(nonfinite);
+      publish(c, P, par ^ 1, tF, tB, 0.0, nf);
+      grid_barrier(P.bar, P.G, c.gen);
+      par ^= 1;
+      double e;
+      int f;
+      read_slot(c, P, par, e, f);
+      ++l;  // line 13
+      if (f) { flag = 2; break; }
+    }
+  }
+  double cost = NAN;
+  if (flag != 2) cost = cost_phase<NW>(c, P, P.Pm, c.PX, Qm[qi], c.QX[qi]);
+  else errv = NAN;
+  // outputs: F = log phi, G = log psi
+  for (int i = c.warp; i < c.nt; i += NW) {
+    from_tile(c, P, P.Pm, c.PX[i], true, dU, i);
+    from_tile(c, P, Qm[qi], c.QX[qi][i], true, dV, i);
+  }
+  if (c.r == 0 && c.tid == 0) {
+    if (P.iters) P.iters[0] = l;
+    if (P.err) P.err[0] = errv;
+    if (P.flags) P.flags[0] = flag;
+    if (P.cost) P.cost[0] = cost;
+  }
+}
+
+}  // namespace stm
+}  // namespace fs1

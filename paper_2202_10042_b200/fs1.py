@@ -40,6 +40,7 @@ class Spec:
     tol: float = 0.0
     check_interval: int = 1
     warm_start: bool = False
+    kernel: int = 0          # 0 auto; test-only overrides: 1 persistent, 2 streaming
 
     def desc(self) -> L.Desc:
         return L.Desc(ndim=self.ndim, n=self.n, m=self.m, h1=self.h1, h2=self.h2, eps=self.eps,
@@ -58,7 +59,11 @@ class Plan:
         self._h = ctypes.c_void_p()
         ws = ctypes.c_size_t()
         d = spec.desc()
-        s = L.lib().fs1_plan(ctypes.byref(d), device, ctypes.byref(self._h), ctypes.byref(ws))
+        if spec.kernel:
+            s = L.lib().fs1__plan_kind(ctypes.byref(d), device, spec.kernel, ctypes.byref(self._h),
+                                       ctypes.byref(ws))
+        else:
+            s = L.lib().fs1_plan(ctypes.byref(d), device, ctypes.byref(self._h), ctypes.byref(ws))
         if s != L.FS1_OK:
             raise L.FS1Error(s, "fs1_plan")
         self.workspace_bytes = ws.value
@@ -128,7 +133,7 @@ def _check(t, name, dtype, device, size):
 
 
 def solve(a, b, *, h, eps, itr_max, tol=0.0, domain="scaling", input_is_log=False,
-          check_interval=1, u0=None, v0=None, shape=None, h2=None, want_cost=True):
+          check_interval=1, u0=None, v0=None, shape=None, h2=None, want_cost=True, kernel=0):
     """Batched FS-1 solve.  a, b: CUDA tensors [batch, n] (1D) or [batch, n*m] with
     shape=(n, m) (2D, column-major).  Returns dict u, v, iters, err, flags, cost."""
     dev = a.device.index
@@ -143,7 +148,7 @@ def solve(a, b, *, h, eps, itr_max, tol=0.0, domain="scaling", input_is_log=Fals
     spec = Spec(ndim=ndim, n=n, m=m, h1=float(h), h2=float(h2 if h2 is not None else (h if ndim == 2 else 0.0)),
                 eps=float(eps), batch=batch, dtype=a.dtype, domain=domain,
                 input_is_log=bool(input_is_log), itr_max=int(itr_max), tol=float(tol),
-                check_interval=int(check_interval), warm_start=u0 is not None)
+                check_interval=int(check_interval), warm_start=u0 is not None, kernel=int(kernel))
     p = plan(spec, dev)
     if u0 is not None:
         u, v = u0.clone(), v0.clone()
@@ -157,7 +162,7 @@ def solve(a, b, *, h, eps, itr_max, tol=0.0, domain="scaling", input_is_log=Fals
     return {"u": u, "v": v, "iters": iters, "err": err, "flags": flags, "cost": cost}
 
 
-def cost(u, v, *, h, eps, domain="scaling", shape=None, h2=None):
+def cost(u, v, *, h, eps, domain="scaling", shape=None, h2=None, kernel=0):
     dev = u.device.index
     ndim, n, m = (1, u.shape[-1], 1) if shape is None else (2, *shape)
     size = n * m
@@ -165,13 +170,13 @@ def cost(u, v, *, h, eps, domain="scaling", shape=None, h2=None):
     _check(v, "v", u.dtype, dev, size)
     batch = u.numel() // size
     spec = Spec(ndim=ndim, n=n, m=m, h1=float(h), h2=float(h2 if h2 is not None else (h if ndim == 2 else 0.0)),
-                eps=float(eps), batch=batch, dtype=u.dtype, domain=domain, itr_max=0)
+                eps=float(eps), batch=batch, dtype=u.dtype, domain=domain, itr_max=0, kernel=int(kernel))
     out = torch.empty(batch, dtype=torch.float64, device=u.device)
     plan(spec, dev).cost_into(u, v, out)
     return out
 
 
-def apply(x, *, h, eps, domain="scaling", shape=None, h2=None):
+def apply(x, *, h, eps, domain="scaling", shape=None, h2=None, kernel=0):
     """y = K x (scaling) or log K e^x (log) for every vector of x."""
     dev = x.device.index
     ndim, n, m = (1, x.shape[-1], 1) if shape is None else (2, *shape)
@@ -179,7 +184,7 @@ def apply(x, *, h, eps, domain="scaling", shape=None, h2=None):
     _check(x, "x", x.dtype, dev, size)
     batch = x.numel() // size
     spec = Spec(ndim=ndim, n=n, m=m, h1=float(h), h2=float(h2 if h2 is not None else (h if ndim == 2 else 0.0)),
-                eps=float(eps), batch=batch, dtype=x.dtype, domain=domain, itr_max=0)
+                eps=float(eps), batch=batch, dtype=x.dtype, domain=domain, itr_max=0, kernel=int(kernel))
     y = torch.empty_like(x)
     plan(spec, dev).apply_into(x, y)
     return y

@@ -194,3 +194,16 @@ def test_2d_cost_separable_equals_quadruple_sum():
         assert got == pytest.approx(ref, rel=1e-13)
     # h1 = h2 = 0 -> 0
     assert dense.cost_2d_bruteforce(P, S, 1.0, 1.0, 0.0, 0.0) == 0.0
+
+
+def test_log_recursion_accumulator_precision():
+    """The LSE recursion oracle at config-3-like magnitudes (|X| ~ 5e3, c ~ 6e-4, memory
+    1/(1 - lambda) ~ 1700) stays within a few ulp of |y| of the dense definition: its
+    extended-precision accumulator removes the fp64 drift (R24)."""
+    n = 6000
+    x = np.linspace(0.0, 1.0, n)
+    X = 5000.0 * np.sin(3.0 * x) - 2000.0 * x
+    c = 6e-4
+    y = recur.sweep_log(X, c)
+    ref = dense.apply_log(X, c)
+    assert np.max(np.abs(y - ref)) / np.max(np.abs(ref)) <= 2e-15
