@@ -69,7 +69,7 @@ void fill_stream_tables(StreamParams& P, double c) {
 
 // Plan the K2 streaming kernel: G = SMs (one CTA per SM), the deepest TMA ring that
 // fits next to the per-tile tables.
-fs1_status plan_stream(fs1_plan_s* p, int device) {
+fs1_status plan_stream(fs1_plan_s* p, int device, int variant) {
   const fs1_desc& d = p->d;
   if (d.ndim != 1 || d.dtype != FS1_F64) return FS1_ERR_UNSUPPORTED;
   int sms = 0, optin = 0;
@@ -85,7 +85,8 @@ fs1_status plan_stream(fs1_plan_s* p, int device) {
   const StreamEntry* best = nullptr;
   size_t smem = 0;
   for (int i = 0; i < cnt; ++i) {
-    const size_t need = stream_smem(tab[i].NW, tab[i].S, ntmax);
+    if (variant >= 0 && i != variant) continue;
+    const size_t need = stream_smem(tab[i].NW, tab[i].S, ntmax, G);
     if (need <= (size_t)optin) { best = &tab[i]; smem = need; break; }
   }
   if (!best) return FS1_ERR_UNSUPPORTED;
@@ -265,12 +266,12 @@ static fs1_status plan_impl(const fs1_desc* desc, int device, int force, fs1_pla
   const bool logd = d.domain == FS1_LOG;
   const double c = d.h1 / d.eps;
 
-  if (d.ndim == 1 && force == 2) {
+  if (d.ndim == 1 && (force == 2 || force >= 10)) {
     std::lock_guard<std::mutex> lk(g_attr_mu);
     int cur = 0;
     if (cudaGetDevice(&cur) != cudaSuccess) { delete p; return FS1_ERR_CUDA; }
     if (cur != device && cudaSetDevice(device) != cudaSuccess) { delete p; return FS1_ERR_CUDA; }
-    const fs1_status st = plan_stream(p, device);
+    const fs1_status st = plan_stream(p, device, force >= 10 ? force - 10 : -1);
     if (cur != device) cudaSetDevice(cur);
     if (st != FS1_OK) { delete p; return st; }
   } else if (d.ndim == 1) {
@@ -308,7 +309,7 @@ static fs1_status plan_impl(const fs1_desc* desc, int device, int force, fs1_pla
       int cur = 0;
       if (cudaGetDevice(&cur) != cudaSuccess) { delete p; return FS1_ERR_CUDA; }
       if (cur != device && cudaSetDevice(device) != cudaSuccess) { delete p; return FS1_ERR_CUDA; }
-      const fs1_status st = plan_stream(p, device);
+      const fs1_status st = plan_stream(p, device, -1);
       if (cur != device) cudaSetDevice(cur);
       if (st != FS1_OK) { delete p; return st; }
       if (workspace_bytes) *workspace_bytes = p->ws;
@@ -367,7 +368,8 @@ fs1_status fs1_plan(const fs1_desc* desc, int device, fs1_plan_t** out, size_t* 
 }
 
 // test-only (not in include/fs1.h): plan with a forced kernel family
-// (kind 1 persistent, 2 streaming) so the parity tests reach K2 at small n.
+// (kind 1 persistent, 2 streaming, 10 + i streaming instantiation i) so the parity
+// tests reach K2 at small n and the benchmarks can compare instantiations.
 fs1_status fs1__plan_kind(const fs1_desc* desc, int device, int kind, fs1_plan_t** out,
                           size_t* workspace_bytes) {
   return plan_impl(desc, device, kind, out, workspace_bytes);

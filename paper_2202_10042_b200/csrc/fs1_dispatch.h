@@ -32,6 +32,6 @@ struct StreamEntry {
   cudaError_t (*launch)(const StreamParams&, int grid, size_t smem, cudaStream_t);
 };
 const StreamEntry* stream_table(int* count);
-size_t stream_smem(int NW, int S, int ntmax);
+size_t stream_smem(int NW, int S, int ntmax, int G);
 
 }  // namespace fs1

@@ -49,19 +49,22 @@ constexpr double INV_LN2 = 1.44269504088896338700e+00;
 
 // ------------------------------------------------------------------ shared layout
 struct Layout {
-  size_t stage, outb, mbar, pwm, pwe, ax, bx, px, qx0, qx1, pfm, pbm, pfe, pbe, qfm, qbm, qfe,
-      qbe, cfr, cbr, rr, errt, redm, rede, total;
+  size_t stage, mbar, pwm, pwe, ax, bx, px, qx0, qx1, pfm, pbm, pfe, pbe, qfm, qbm, qfe, qbe, cfr,
+      cbr, rr, errt, redm, rede, dpm, dpe, tza, tzb, total;
 };
 
 __host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~(size_t)15; }
 
-__host__ __device__ inline Layout layout(int NW, int S, int ntmax) {
+__host__ __device__ inline Layout layout(int NW, int S, int ntmax, int G) {
   Layout L;
   size_t o = 0;
   const size_t nt = (size_t)ntmax + 1;
   L.stage = o; o = al16(o + (size_t)NW * S * 2 * TBYTES);
-  L.outb = o;  o = al16(o + (size_t)NW * 2 * TBYTES);
   L.mbar = o;  o = al16(o + (size_t)NW * S * 8);
+  L.dpm = o;   o = al16(o + (size_t)G * 8);
+  L.dpe = o;   o = al16(o + (size_t)G * 4);
+  L.tza = o;   o = al16(o + nt);
+  L.tzb = o;   o = al16(o + nt);
   L.pwm = o;   o = al16(o + nt * 8);
   L.pfm = o;   o = al16(o + nt * 8);
   L.pbm = o;   o = al16(o + nt * 8);
@@ -128,6 +131,72 @@ __device__ __forceinline__ void fence_async() { asm volatile("fence.proxy.async;
 __device__ __forceinline__ void fence_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
+// Warp scan step without selects: the shuffle's in-range predicate guards the FMA.
+// up:   v + m * v[lane - d]  (lane >= d), else v
+// down: v + m * v[lane + d]  (lane + d < 32), else v
+__device__ __forceinline__ double scan_up(double v, unsigned d, double m) {
+  double r = v;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t.reg .b32 lo, hi, a, b;\n\t.reg .f64 s;\n\t"
+      "mov.b64 {lo, hi}, %1;\n\t"
+      "shfl.sync.up.b32 a|p, lo, %2, 0, -1;\n\t"
+      "shfl.sync.up.b32 b, hi, %2, 0, -1;\n\t"
+      "mov.b64 s, {a, b};\n\t"
+      "@p fma.rn.f64 %0, %3, s, %1;\n\t}"
+      : "+d"(r)
+      : "d"(v), "r"(d), "d"(m));
+  return r;
+}
+__device__ __forceinline__ double scan_down(double v, unsigned d, double m) {
+  double r = v;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t.reg .b32 lo, hi, a, b;\n\t.reg .f64 s;\n\t"
+      "mov.b64 {lo, hi}, %1;\n\t"
+      "shfl.sync.down.b32 a|p, lo, %2, 31, -1;\n\t"
+      "shfl.sync.down.b32 b, hi, %2, 31, -1;\n\t"
+      "mov.b64 s, {a, b};\n\t"
+      "@p fma.rn.f64 %0, %3, s, %1;\n\t}"
+      : "+d"(r)
+      : "d"(v), "r"(d), "d"(m));
+  return r;
+}
+// exclusive neighbours: v[lane-1] (0 at lane 0) and v[lane+1] (0 at lane 31)
+__device__ __forceinline__ double prev_or0(double v) {
+  double r = 0.0;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t.reg .b32 lo, hi, a, b;\n\t"
+      "mov.b64 {lo, hi}, %1;\n\t"
+      "shfl.sync.up.b32 a|p, lo, 1, 0, -1;\n\t"
+      "shfl.sync.up.b32 b, hi, 1, 0, -1;\n\t"
+      "@p mov.b64 %0, {a, b};\n\t}"
+      : "+d"(r)
+      : "d"(v));
+  return r;
+}
+__device__ __forceinline__ double next_or0(double v) {
+  double r = 0.0;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t.reg .b32 lo, hi, a, b;\n\t"
+      "mov.b64 {lo, hi}, %1;\n\t"
+      "shfl.sync.down.b32 a|p, lo, 1, 31, -1;\n\t"
+      "shfl.sync.down.b32 b, hi, 1, 31, -1;\n\t"
+      "@p mov.b64 %0, {a, b};\n\t}"
+      : "+d"(r)
+      : "d"(v));
+  return r;
+}
+// t / x without branches: hardware reciprocal estimate, one Newton step, one
+// residual correction of the quotient (< 1 ulp; x = 0 or non-finite -> non-finite).
+__device__ __forceinline__ double fdiv(double t, double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  const double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  const double q = t * r;
+  const double rem = fma(-x, q, t);
+  return fma(r, rem, q);
+}
+
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -209,14 +278,18 @@ struct Ctx {
   int tid, lane, warp, NT, NW;
   int r, T0, nt;
   double* stage;
-  double* outb;
   uint64_t* mbar;
+  double* dpm;          // lambda^{256 d_k}: distance from range k to this range (ext carries)
+  int* dpe;
+  unsigned char* tzA;   // tile of a / b has a zero (or padding) entry
+  unsigned char* tzB;
   double* pwm;
   int* pwe;
   int* AX;
   int* BX;
   int* PX;
-  int* QX[2];
+  int* QX0;
+  int* QX1;
   double *PFm, *PBm, *QFm, *QBm;
   int *PFe, *PBe, *QFe, *QBe;
   double* cfr;
@@ -260,18 +333,16 @@ __device__ __forceinline__ void tile_scan_lanes(const StreamParams& P, int lane,
   const double lam = P.lam;
   double f = 0.0, g = 0.0;
 #pragma unroll
-  for (int e = 0; e < E; ++e) f = fma(lam, f, v[e]);
-#pragma unroll
-  for (int e = E - 1; e >= 0; --e) g = fma(lam, g, v[e]);
+  for (int e = 0; e < E; ++e) {
+    f = fma(lam, f, v[e]);
+    g = fma(lam, g, v[E - 1 - e]);
+  }
   Fi = f;
   Gi = g;
 #pragma unroll
   for (int k = 0; k < 5; ++k) {
-    const int d = 1 << k;
-    const double up = __shfl_up_sync(FULL, Fi, d);
-    const double dn = __shfl_down_sync(FULL, Gi, d);
-    if (lane >= d) Fi = fma(P.lvd[k], up, Fi);
-    if (lane + d < 32) Gi = fma(P.lvd[k], dn, Gi);
+    Fi = scan_up(Fi, 1u << k, P.lvd[k]);
+    Gi = scan_down(Gi, 1u << k, P.lvd[k]);
   }
 }
 
@@ -294,7 +365,7 @@ __device__ __forceinline__ void put_totals(int lane, double Fi, double Gi, int Y
 // In: F/B hold per-tile totals (forward at the tile end, backward at the tile start).
 // Out (in place): exclusive local carries CFloc_i = sum_{i'<i} lambda^{256(i-1-i')} FT_i',
 // CBloc_i = sum_{i'>i} lambda^{256(i'-i-1)} GT_i'; returns the range totals.
-__device__ void block_tile_scan(Ctx& c, double* Fm, int* Fe, double* Bm, int* Be, ER<double>& totF,
+__device__ __forceinline__ void block_tile_scan(Ctx& c, double* Fm, int* Fe, double* Bm, int* Be, ER<double>& totF,
                                 ER<double>& totB) {
   const int nt = c.nt, NT = c.NT, lane = c.lane, warp = c.warp;
   const int q = (nt + NT - 1) / NT;
@@ -355,7 +426,7 @@ __device__ void block_tile_scan(Ctx& c, double* Fm, int* Fe, double* Bm, int* Be
 }
 
 // Deterministic block sum (fixed tree) of per-tile ER values vm/ve[0..nt).
-__device__ ER<double> block_er_sum(Ctx& c, const double* vm, const int* ve) {
+__device__ __forceinline__ ER<double> block_er_sum(Ctx& c, const double* vm, const int* ve) {
   const int nt = c.nt, NT = c.NT;
   const int q = (nt + NT - 1) / NT;
   const int i0 = min(nt, c.tid * q), i1 = min(nt, i0 + q);
@@ -372,40 +443,28 @@ __device__ ER<double> block_er_sum(Ctx& c, const double* vm, const int* ve) {
 }
 
 // ---------------------------------------------------------------- external carries
-// Warp 0: fold the other ranges' totals (slot par) into this range's carries.
-__device__ void ext_carries(Ctx& c, const StreamParams& P, int par, ER<double>& CFx, ER<double>& CBx) {
+// Warp 0: the other ranges' totals (slot par), each decayed by the precomputed
+// lambda^{256 d_k} to this range's boundary, summed in a fixed order.
+__device__ __forceinline__ void ext_carries(Ctx& c, const StreamParams& P, int par, ER<double>& CFx, ER<double>& CBx) {
   const double* gt = P.gtot + (size_t)par * P.G * 4;
   const int* ge = P.gtote + (size_t)par * P.G * 4;
-  const int r = c.r, lane = c.lane;
-  // forward: ranges [0, r)
-  {
-    const int q = (r + 31) / 32;
-    const int s0 = min(r, lane * q), s1 = min(r, s0 + q);
-    ER<double> acc = er_zero<double>();
-    for (int k = s0; k < s1; ++k) {
-      const int len = (int)(range_T0(P, k + 1) - range_T0(P, k));
-      acc = er_fma(acc, pw(c, len), ER<double>{__ldcg(gt + 4 * k), __ldcg(ge + 4 * k)});
-    }
-    if (s1 > s0) acc = er_mul(acc, pow_tiles(P, range_T0(P, r) - range_T0(P, s1)));
-    CFx = warp_er_sum(acc);
+  ER<double> f = er_zero<double>(), b = er_zero<double>();
+  for (int k = c.lane; k < P.G; k += 32) {
+    if (k == c.r) continue;
+    const ER<double> dp{c.dpm[k], c.dpe[k]};
+    if (k < c.r) f = er_add(f, er_mul(dp, ER<double>{__ldcg(gt + 4 * k), __ldcg(ge + 4 * k)}));
+    else b = er_add(b, er_mul(dp, ER<double>{__ldcg(gt + 4 * k + 1), __ldcg(ge + 4 * k + 1)}));
   }
-  // backward: ranges (r, G)
-  {
-    const int nb = P.G - 1 - r;
-    const int q = (nb + 31) / 32;
-    const int s0 = r + 1 + min(nb, lane * q), s1 = r + 1 + min(nb, lane * q + q);
-    ER<double> acc = er_zero<double>();
-    for (int k = s1 - 1; k >= s0; --k) {
-      const int len = (int)(range_T0(P, k + 1) - range_T0(P, k));
-      acc = er_fma(acc, pw(c, len), ER<double>{__ldcg(gt + 4 * k + 1), __ldcg(ge + 4 * k + 1)});
-    }
-    if (s1 > s0) acc = er_mul(acc, pow_tiles(P, range_T0(P, s0) - range_T0(P, r + 1)));
-    CBx = warp_er_sum(acc);
-  }
+  CFx = warp_er_sum(f);
+  CBx = warp_er_sum(b);
+}
+// tiles between range k and this range r (the decay distance of k's total)
+__device__ __forceinline__ long long range_gap(const StreamParams& P, int k, int r) {
+  return k < r ? range_T0(P, r) - range_T0(P, k + 1) : range_T0(P, k) - range_T0(P, r + 1);
 }
 
 // [A]: full per-tile carries of the consumed vector x (tables F/B, exponents Xx).
-__device__ void tile_carries(Ctx& c, const StreamParams& P, int par, const double* Fm, const int* Fe,
+__device__ __forceinline__ void tile_carries(Ctx& c, const StreamParams& P, int par, const double* Fm, const int* Fe,
                              const double* Bm, const int* Be, const int* Xx) {
   if (c.warp == 0) {
     ER<double> CFx, CBx;
@@ -443,12 +502,16 @@ struct HalfArgs {
   int* Xy;
   double *yFm, *yBm;
   int *yFe, *yBe;
+  const unsigned char* tz;  // per-tile "target has a zero entry" flags
 };
 
 // DIV: y = tgt / Kx (solve) else y = Kx (apply); CHECK: accumulate the marginal
 // error sum |psi_old (Kx) - tgt| per tile; WRITE: produce y.
+// Each warp streams the tiles i = warp, warp + NW, ... of this range through its
+// S-stage ring; y overwrites x in the stage and leaves by TMA bulk store; a stage
+// is refilled (S - 1 tiles ahead) once the store of its previous tile has read it.
 template <int NW, int S, bool DIV, bool CHECK, bool WRITE>
-__device__ void stream_half(Ctx& c, const StreamParams& P, const HalfArgs& A, int& nonfinite) {
+__device__ __forceinline__ void stream_half(Ctx& c, const StreamParams& P, const HalfArgs& A, int& nonfinite) {
   const int lane = c.lane, w = c.warp;
   const long long gbase = (long long)c.T0 * TILE;
   double* stg = c.stage + (size_t)w * S * 2 * TILE;
@@ -457,7 +520,7 @@ __device__ void stream_half(Ctx& c, const StreamParams& P, const HalfArgs& A, in
   const double lam = P.lam;
   const double lp = P.lanepow[lane], rp = P.lanepow[31 - lane];
 
-  auto issue = [&](int k) {
+  auto issue = [&](int k) {  // lane 0
     const int i = w + k * NW;
     if (i >= c.nt) return;
     const int s = k % S;
@@ -468,19 +531,19 @@ __device__ void stream_half(Ctx& c, const StreamParams& P, const HalfArgs& A, in
   if (lane == 0) {
     fence_async();
 #pragma unroll
-    for (int k = 0; k < S; ++k) issue(k);
+    for (int k = 0; k < S - 1; ++k) issue(k);
   }
   int bad = 0;
   int k = 0;
   for (int i = w; i < c.nt; i += NW, ++k) {
     const int s = k % S;
+    double* xs = stg + (s * 2) * TILE;
     mbar_wait(&mb[s], (c.phase >> s) & 1u);
     c.phase ^= (1u << s);
-    double xv[E], tv[E], ov[E];
-    lds_tile(stg + (s * 2) * TILE, lane, xv);
-    if (LOADT) lds_tile(stg + (s * 2 + 1) * TILE, lane, tv);
-    __syncwarp();
-    if (lane == 0) issue(k + S);
+    double xv[E], tv[E];
+    lds_tile(xs, lane, xv);
+    if (LOADT) lds_tile(xs + TILE, lane, tv);
+    double ov[E];
     if (CHECK) ldg_tile(A.og + gbase + (long long)i * TILE, lane, ov);
 
     const int X = A.Xx[i];
@@ -490,35 +553,31 @@ __device__ void stream_half(Ctx& c, const StreamParams& P, const HalfArgs& A, in
 #pragma unroll
       for (int e = 0; e < E; ++e) xv[e] *= sc;
     }
-    // carries into this lane's chunk
+    // carries into this lane's chunk: intra-tile exclusive scan + decayed tile carries
     double Fi, Gi;
     tile_scan_lanes(P, lane, xv, Fi, Gi);
-    double cf = __shfl_up_sync(FULL, Fi, 1);
-    double cb = __shfl_down_sync(FULL, Gi, 1);
-    if (lane == 0) cf = 0.0;
-    if (lane == 31) cb = 0.0;
-    cf = fma(lp, c.cfr[i], cf);
-    cb = fma(rp, c.cbr[i], cb);
+    const double cf = fma(lp, c.cfr[i], prev_or0(Fi));
+    const double cb = fma(rp, c.cbr[i], next_or0(Gi));
     // forward recursion p_k = lam p_{k-1} + x_k (Alg. 1 line 5 / 10)
     double pf[E];
     double p = cf;
 #pragma unroll
     for (int e = 0; e < E; ++e) { p = fma(lam, p, xv[e]); pf[e] = p; }
-    // backward recursion t_k = lam t_{k+1} + x_k, K x = p + lam t_{k+1} (line 6 / 11)
-    // fused with the update y = tgt / (K x) (line 7 / 12)
+    // backward recursion t_k = lam t_{k+1} + x_k, K x = p + lam t_{k+1} (line 6 / 11),
+    // fused with the update y = tgt / (K x) (line 7 / 12); y overwrites tv
     double tn = cb;
     double errp = 0.0;
     double sce = 0.0;
     if (CHECK) sce = pow2d(min(max(A.Xo[i] + R - A.Xt[i], -1100), 1000));
-    double yv[E];
+    const bool guard = DIV && A.tz[i];  // zero targets: y = 0 exactly (warp-uniform)
 #pragma unroll
     for (int e = E - 1; e >= 0; --e) {
       const double kx = fma(lam, tn, pf[e]);
       tn = fma(lam, tn, xv[e]);
       if (CHECK) errp += fabs(fma(ov[e] * sce, kx, -tv[e]));
       if (WRITE) {
-        if (DIV) yv[e] = (tv[e] > 0.0) ? tv[e] * __drcp_rn(kx) : 0.0;
-        else yv[e] = kx;
+        if (DIV) tv[e] = guard ? (tv[e] > 0.0 ? fdiv(tv[e], kx) : 0.0) : fdiv(tv[e], kx);
+        else tv[e] = kx;
       }
     }
     if (CHECK) {
@@ -526,38 +585,44 @@ __device__ void stream_half(Ctx& c, const StreamParams& P, const HalfArgs& A, in
       if (lane == 0) c.errt[i] = ldexp(es, A.Xt[i]);
     }
     if (WRITE) {
-      // exact power-of-two renormalisation of the output tile
-      double ym = 0.0;
+      // exact power-of-two renormalisation of the output tile: the largest high word
+      // of the (non-negative) doubles gives the tile's top binary exponent
+      int hm = 0;
 #pragma unroll
-      for (int e = 0; e < E; ++e) ym = fmax(ym, yv[e]);
-      const int M = warp_max(ym > 0.0 ? expo_d(ym) : ZE);
+      for (int e = 0; e < E; ++e) hm = max(hm, __double2hiint(tv[e]));
+      hm = warp_max(hm);
       const int base = DIV ? (A.Xt[i] == ZE ? ZE : A.Xt[i] - R) : R;
       int Y = ZE;
-      if (M != ZE && base != ZE) {
-        const double s1 = pow2d(-(M / 2)), s2 = pow2d(-(M - M / 2));
+      if (hm >= 0x00100000 && base != ZE) {
+        const int M = min(max((hm >> 20) - 1023, -1020), 1020);
+        const double sc = pow2d(-M);
 #pragma unroll
-        for (int e = 0; e < E; ++e) yv[e] = (yv[e] * s1) * s2;
+        for (int e = 0; e < E; ++e) tv[e] *= sc;
         Y = base + M;
       } else {
 #pragma unroll
-        for (int e = 0; e < E; ++e) yv[e] = 0.0;
+        for (int e = 0; e < E; ++e) tv[e] = 0.0;
       }
       double FiY, GiY;
-      tile_scan_lanes(P, lane, yv, FiY, GiY);
+      tile_scan_lanes(P, lane, tv, FiY, GiY);
       if (!isfinite(FiY + GiY)) bad = 1;
       put_totals(lane, FiY, GiY, Y, A.yFm, A.yFe, A.yBm, A.yBe, i);
       if (lane == 0) A.Xy[i] = Y;
-      // stage through the out ring and bulk-store the tile
-      double* ob = c.outb + (size_t)(w * 2 + (k & 1)) * TILE;
-      if (lane == 0) bulk_wait_read1();
-      __syncwarp();
-      sts_tile(ob, lane, yv);
+      // y overwrites x in this stage (each lane rewrites only the chunks it read)
+      sts_tile(xs, lane, tv);
       fence_async_smem();
       __syncwarp();
       if (lane == 0) {
-        bulk_s2g(A.yg + gbase + (long long)i * TILE, ob, TBYTES);
+        bulk_s2g(A.yg + gbase + (long long)i * TILE, xs, TBYTES);
         bulk_commit();
       }
+    } else {
+      __syncwarp();
+    }
+    if (lane == 0) {
+      // refill the previous tile's stage once its store has read it
+      if (WRITE) bulk_wait_read1();
+      issue(k + S - 1);
     }
   }
   if (WRITE && lane == 0) bulk_wait_all();
@@ -567,7 +632,7 @@ __device__ void stream_half(Ctx& c, const StreamParams& P, const HalfArgs& A, in
 // ---------------------------------------------------------------- prologue/epilogue
 // Convert a user vector (linear, log, or the constant init) of tile i into
 // mantissas + tile exponent, write the mantissas, return them in registers.
-__device__ void to_tile(const Ctx& c, const StreamParams& P, const double* src, int kind, double init,
+__device__ __forceinline__ void to_tile(const Ctx& c, const StreamParams& P, const double* src, int kind, double init,
                         double* dst, int i, double (&m)[E], int& X) {
   // kind: 0 linear, 1 log, 2 constant init
   const int lane = c.lane;
@@ -619,7 +684,7 @@ __device__ void to_tile(const Ctx& c, const StreamParams& P, const double* src, 
   stg_tile(dst + ((long long)c.T0 + i) * TILE, lane, m);
 }
 
-__device__ void from_tile(const Ctx& c, const StreamParams& P, const double* srcm, int X, bool logd,
+__device__ __forceinline__ void from_tile(const Ctx& c, const StreamParams& P, const double* srcm, int X, bool logd,
                           double* dst, int i) {
   const int lane = c.lane;
   double m[E];
@@ -638,13 +703,21 @@ __device__ void from_tile(const Ctx& c, const StreamParams& P, const double* src
 }
 
 // Convert a user vector into a state buffer with its tile exponents and scan totals.
-__device__ void load_vector(Ctx& c, const StreamParams& P, const double* src, int kind, double init,
-                            double* dst, int* Xt, double* Fm, int* Fe, double* Bm, int* Be) {
+__device__ __forceinline__ void load_vector(Ctx& c, const StreamParams& P, const double* src, int kind, double init,
+                            double* dst, int* Xt, double* Fm, int* Fe, double* Bm, int* Be,
+                            unsigned char* tz = nullptr) {
   for (int i = c.warp; i < c.nt; i += c.NW) {
     double m[E];
     int X;
     to_tile(c, P, src, kind, init, dst, i, m, X);
     if (c.lane == 0) Xt[i] = X;
+    if (tz) {
+      bool z = false;
+#pragma unroll
+      for (int e = 0; e < E; ++e) z |= !(m[e] > 0.0);
+      z = __any_sync(FULL, z);
+      if (c.lane == 0) tz[i] = z ? 1 : 0;
+    }
     if (Fm) {
       double Fi, Gi;
       tile_scan_lanes(P, c.lane, m, Fi, Gi);
@@ -695,7 +768,7 @@ __device__ __forceinline__ void jordan_lanes(const StreamParams& P, int lane, co
   }
 }
 
-__device__ void block_pair_scan(Ctx& c, double* Am, int* Ae, double* A2m, int* A2e, double* Bm, int* Be,
+__device__ __forceinline__ void block_pair_scan(Ctx& c, double* Am, int* Ae, double* A2m, int* A2e, double* Bm, int* Be,
                                 double* B2m, int* B2e, Pair& totF, Pair& totB) {
   const int nt = c.nt, NT = c.NT, lane = c.lane, warp = c.warp;
   const int q = (nt + NT - 1) / NT;
@@ -763,7 +836,7 @@ __device__ void block_pair_scan(Ctx& c, double* Am, int* Ae, double* A2m, int* A
 
 // cost of the state (Pm, Xp) = phi, (Qm, Xq) = psi; returns the value on every CTA.
 template <int NW>
-__device__ double cost_phase(Ctx& c, const StreamParams& P, const double* Pm, const int* Xp,
+__device__ __forceinline__ double cost_phase(Ctx& c, const StreamParams& P, const double* Pm, const int* Xp,
                              const double* Qm, const int* Xq) {
   const int lane = c.lane;
   // tables: forward (p, P') in PF/PB, backward (t, Q') in QF/QB
@@ -794,48 +867,32 @@ __device__ double cost_phase(Ctx& c, const StreamParams& P, const double* Pm, co
     g[2] = tB.a.m; ge[2] = tB.a.e; g[3] = tB.b.m; ge[3] = tB.b.e;
   }
   grid_barrier(P.bar, P.G, c.gen);
-  // external pair carries (warp 0)
+  // external pair carries (warp 0): every other range's totals advanced over the gap
+  // to this range (precomputed lambda^{256 d}), summed component-wise
   if (c.warp == 0) {
-    const int r = c.r;
-    Pair ef, eb;
-    {
-      const int q = (r + 31) / 32;
-      const int s0 = min(r, lane * q), s1 = min(r, s0 + q);
-      Pair acc = pzero();
-      for (int k = s0; k < s1; ++k) {
-        const int len = (int)(range_T0(P, k + 1) - range_T0(P, k));
-        const double* g = P.gtot2 + (size_t)k * 8;
-        const int* ge = P.gtot2e + (size_t)k * 8;
-        acc = pcomb(acc, Pair{ER<double>{__ldcg(g), __ldcg(ge)}, ER<double>{__ldcg(g + 1), __ldcg(ge + 1)}},
-                    pw(c, len), (double)TILE * len);
+    Pair ef = pzero(), eb = pzero();
+    for (int k = lane; k < P.G; k += 32) {
+      if (k == c.r) continue;
+      const double* g = P.gtot2 + (size_t)k * 8;
+      const int* ge = P.gtot2e + (size_t)k * 8;
+      const ER<double> dp{c.dpm[k], c.dpe[k]};
+      const double L = (double)TILE * (double)range_gap(P, k, c.r);
+      if (k < c.r) {
+        const Pair t = pcomb(Pair{ER<double>{__ldcg(g), __ldcg(ge)}, ER<double>{__ldcg(g + 1), __ldcg(ge + 1)}},
+                             pzero(), dp, L);
+        ef.a = er_add(ef.a, t.a);
+        ef.b = er_add(ef.b, t.b);
+      } else {
+        const Pair t = pcomb(Pair{ER<double>{__ldcg(g + 2), __ldcg(ge + 2)}, ER<double>{__ldcg(g + 3), __ldcg(ge + 3)}},
+                             pzero(), dp, L);
+        eb.a = er_add(eb.a, t.a);
+        eb.b = er_add(eb.b, t.b);
       }
-      if (s1 > s0) {
-        const long long d = range_T0(P, r) - range_T0(P, s1);
-        acc = pcomb(acc, pzero(), pow_tiles(P, d), (double)TILE * d);
-      }
-      // sum of independent contributions: (p, P') add component-wise
-      ef.a = warp_er_sum(acc.a);
-      ef.b = warp_er_sum(acc.b);
     }
-    {
-      const int nb = P.G - 1 - r;
-      const int q = (nb + 31) / 32;
-      const int s0 = r + 1 + min(nb, lane * q), s1 = r + 1 + min(nb, lane * q + q);
-      Pair acc = pzero();
-      for (int k = s1 - 1; k >= s0; --k) {
-        const int len = (int)(range_T0(P, k + 1) - range_T0(P, k));
-        const double* g = P.gtot2 + (size_t)k * 8;
-        const int* ge = P.gtot2e + (size_t)k * 8;
-        acc = pcomb(acc, Pair{ER<double>{__ldcg(g + 2), __ldcg(ge + 2)}, ER<double>{__ldcg(g + 3), __ldcg(ge + 3)}},
-                    pw(c, len), (double)TILE * len);
-      }
-      if (s1 > s0) {
-        const long long d = range_T0(P, s0) - range_T0(P, r + 1);
-        acc = pcomb(acc, pzero(), pow_tiles(P, d), (double)TILE * d);
-      }
-      eb.a = warp_er_sum(acc.a);
-      eb.b = warp_er_sum(acc.b);
-    }
+    ef.a = warp_er_sum(ef.a);
+    ef.b = warp_er_sum(ef.b);
+    eb.a = warp_er_sum(eb.a);
+    eb.b = warp_er_sum(eb.b);
     if (lane == 0) {
       c.redm[500] = ef.a.m; c.rede[500] = ef.a.e; c.redm[501] = ef.b.m; c.rede[501] = ef.b.e;
       c.redm[502] = eb.a.m; c.rede[502] = eb.a.e; c.redm[503] = eb.b.m; c.rede[503] = eb.b.e;
@@ -914,7 +971,7 @@ __device__ double cost_phase(Ctx& c, const StreamParams& P, const double* Pm, co
 }
 
 // ---------------------------------------------------------------- publish / read
-__device__ void publish(Ctx& c, const StreamParams& P, int slot, ER<double> F, ER<double> B, double errs,
+__device__ __forceinline__ void publish(Ctx& c, const StreamParams& P, int slot, ER<double> F, ER<double> B, double errs,
                         int flag) {
   if (c.tid == 0) {
     double* g = P.gtot + ((size_t)slot * P.G + c.r) * 4;
@@ -926,7 +983,7 @@ __device__ void publish(Ctx& c, const StreamParams& P, int slot, ER<double> F, E
 }
 // totals over ranges of slot: error sum (fixed order) and OR of flags (warp 0 result
 // broadcast through shared memory)
-__device__ void read_slot(Ctx& c, const StreamParams& P, int slot, double& err, int& flag) {
+__device__ __forceinline__ void read_slot(Ctx& c, const StreamParams& P, int slot, double& err, int& flag) {
   if (c.warp == 0) {
     double s = 0.0;
     int f = 0;
@@ -946,7 +1003,7 @@ __device__ void read_slot(Ctx& c, const StreamParams& P, int slot, double& err, 
 
 // ---------------------------------------------------------------- the kernel
 template <int NW, int S>
-__global__ void __launch_bounds__(32 * NW, 1) fs1_stream_kernel(const StreamParams P) {
+__global__ void __launch_bounds__(32 * NW, 1) fs1_stream_kernel(const __grid_constant__ StreamParams P) {
   extern __shared__ __align__(128) unsigned char smem[];
   Ctx c;
   c.NW = NW;
@@ -957,17 +1014,20 @@ __global__ void __launch_bounds__(32 * NW, 1) fs1_stream_kernel(const StreamPara
   c.r = blockIdx.x;
   c.T0 = (int)range_T0(P, c.r);
   c.nt = (int)(range_T0(P, c.r + 1) - c.T0);
-  const Layout L = layout(NW, S, P.ntmax);
+  const Layout L = layout(NW, S, P.ntmax, P.G);
   c.stage = reinterpret_cast<double*>(smem + L.stage);
-  c.outb = reinterpret_cast<double*>(smem + L.outb);
   c.mbar = reinterpret_cast<uint64_t*>(smem + L.mbar);
+  c.dpm = reinterpret_cast<double*>(smem + L.dpm);
+  c.dpe = reinterpret_cast<int*>(smem + L.dpe);
+  c.tzA = smem + L.tza;
+  c.tzB = smem + L.tzb;
   c.pwm = reinterpret_cast<double*>(smem + L.pwm);
   c.pwe = reinterpret_cast<int*>(smem + L.pwe);
   c.AX = reinterpret_cast<int*>(smem + L.ax);
   c.BX = reinterpret_cast<int*>(smem + L.bx);
   c.PX = reinterpret_cast<int*>(smem + L.px);
-  c.QX[0] = reinterpret_cast<int*>(smem + L.qx0);
-  c.QX[1] = reinterpret_cast<int*>(smem + L.qx1);
+  c.QX0 = reinterpret_cast<int*>(smem + L.qx0);
+  c.QX1 = reinterpret_cast<int*>(smem + L.qx1);
   c.PFm = reinterpret_cast<double*>(smem + L.pfm);
   c.PBm = reinterpret_cast<double*>(smem + L.pbm);
   c.QFm = reinterpret_cast<double*>(smem + L.qfm);
@@ -994,6 +1054,11 @@ __global__ void __launch_bounds__(32 * NW, 1) fs1_stream_kernel(const StreamPara
     c.pwm[k] = t.m;
     c.pwe[k] = t.e;
   }
+  for (int k = c.tid; k < P.G; k += c.NT) {  // decay from range k to this range
+    const ER<double> t = (k == c.r) ? er_zero<double>() : pow_tiles(P, range_gap(P, k, c.r));
+    c.dpm[k] = t.m;
+    c.dpe[k] = t.e;
+  }
   for (int i = c.tid; i < c.nt; i += c.NT) c.errt[i] = 0.0;
   __syncthreads();
 
@@ -1001,7 +1066,6 @@ __global__ void __launch_bounds__(32 * NW, 1) fs1_stream_kernel(const StreamPara
   const double* dB = reinterpret_cast<const double*>(P.b);
   double* dU = reinterpret_cast<double*>(P.u);
   double* dV = reinterpret_cast<double*>(P.v);
-  double* Qm[2] = {P.Qm0, P.Qm1};
   int nonfinite = 0;
 
   if (P.mode == MODE_APPLY) {
@@ -1013,33 +1077,32 @@ __global__ void __launch_bounds__(32 * NW, 1) fs1_stream_kernel(const StreamPara
     publish(c, P, 0, tF, tB, 0.0, 0);
     grid_barrier(P.bar, P.G, c.gen);
     tile_carries(c, P, 0, c.PFm, c.PFe, c.PBm, c.PBe, c.PX);
-    HalfArgs A{P.Pm, c.PX, nullptr, nullptr, nullptr, nullptr, P.Qm0, c.QX[0],
-               c.QFm, c.QBm, c.QFe, c.QBe};
+    HalfArgs A{P.Pm, c.PX, nullptr, nullptr, nullptr, nullptr, P.Qm0, c.QX0,
+               c.QFm, c.QBm, c.QFe, c.QBe, nullptr};
     stream_half<NW, S, false, false, true>(c, P, A, nonfinite);
     __syncthreads();
     fence_async();
     __syncthreads();
     for (int i = c.warp; i < c.nt; i += NW)
-      from_tile(c, P, P.Qm0, c.QX[0][i], P.logd, reinterpret_cast<double*>(P.y), i);
+      from_tile(c, P, P.Qm0, c.QX0[i], P.logd, reinterpret_cast<double*>(P.y), i);
     return;
   }
   if (P.mode == MODE_COST) {
     load_vector(c, P, dU, P.logd ? 1 : 0, 0.0, P.Pm, c.PX, nullptr, nullptr, nullptr, nullptr);
-    load_vector(c, P, dV, P.logd ? 1 : 0, 0.0, P.Qm0, c.QX[0], nullptr, nullptr, nullptr, nullptr);
+    load_vector(c, P, dV, P.logd ? 1 : 0, 0.0, P.Qm0, c.QX0, nullptr, nullptr, nullptr, nullptr);
     __syncthreads();
-    grid_barrier(P.bar, P.G, c.gen);
-    const double cost = cost_phase<NW>(c, P, P.Pm, c.PX, P.Qm0, c.QX[0]);
+    const double cost = cost_phase<NW>(c, P, P.Pm, c.PX, P.Qm0, c.QX0);
     if (c.r == 0 && c.tid == 0 && P.cost) P.cost[0] = cost;
     return;
   }
 
   // ---------------- solve (Algorithm 1)
   const int kin = P.input_is_log ? 1 : 0;
-  load_vector(c, P, dA, kin, 0.0, P.Am, c.AX, nullptr, nullptr, nullptr, nullptr);
-  load_vector(c, P, dB, kin, 0.0, P.Bm, c.BX, nullptr, nullptr, nullptr, nullptr);
+  load_vector(c, P, dA, kin, 0.0, P.Am, c.AX, nullptr, nullptr, nullptr, nullptr, c.tzA);
+  load_vector(c, P, dB, kin, 0.0, P.Bm, c.BX, nullptr, nullptr, nullptr, nullptr, c.tzB);
   const double init = 1.0 / (double)P.n;  // phi0 = psi0 = 1/N
   load_vector(c, P, dU, P.warm ? 1 : 2, init, P.Pm, c.PX, c.PFm, c.PFe, c.PBm, c.PBe);
-  load_vector(c, P, dV, P.warm ? 1 : 2, init, Qm[0], c.QX[0], nullptr, nullptr, nullptr, nullptr);
+  load_vector(c, P, dV, P.warm ? 1 : 2, init, P.Qm0, c.QX0, nullptr, nullptr, nullptr, nullptr);
   __syncthreads();
   int par = 0;
   {
@@ -1057,7 +1120,11 @@ __global__ void __launch_bounds__(32 * NW, 1) fs1_stream_kernel(const StreamPara
     // ---- lines 2-7: psi = b ./ (K^T phi), with the marginal error on check iterations
     tile_carries(c, P, par, c.PFm, c.PFe, c.PBm, c.PBe, c.PX);
     const int qo = check ? (qi ^ 1) : qi;  // a checking step keeps psi^(l) in Qm[qi]
-    HalfArgs A{P.Pm, c.PX, P.Bm, c.BX, Qm[qi], c.QX[qi], Qm[qo], c.QX[qo], c.QFm, c.QBm, c.QFe, c.QBe};
+    double* Qi = qi ? P.Qm1 : P.Qm0;
+    int* QXi = qi ? c.QX1 : c.QX0;
+    double* Qo = qo ? P.Qm1 : P.Qm0;
+    int* QXo = qo ? c.QX1 : c.QX0;
+    HalfArgs A{P.Pm, c.PX, P.Bm, c.BX, Qi, QXi, Qo, QXo, c.QFm, c.QBm, c.QFe, c.QBe, c.tzB};
     nonfinite = 0;
     if (!check) stream_half<NW, S, true, false, true>(c, P, A, nonfinite);
     else if (!last) stream_half<NW, S, true, true, true>(c, P, A, nonfinite);
@@ -1069,14 +1136,13 @@ __global__ void __launch_bounds__(32 * NW, 1) fs1_stream_kernel(const StreamPara
       double es = 0.0;
       if (check) {
         // deterministic per-range error sum
-        double* em = c.errt;
         const int q = (c.nt + c.NT - 1) / c.NT;
         const int i0 = min(c.nt, c.tid * q), i1 = min(c.nt, i0 + q);
-        double s = 0.0;
-        for (int i = i0; i < i1; ++i) s += em[i];
-        s = warp_sum(s);
+        double sm = 0.0;
+        for (int i = i0; i < i1; ++i) sm += c.errt[i];
+        sm = warp_sum(sm);
         __syncthreads();
-        if (c.lane == 0) c.redm[c.warp] = s;
+        if (c.lane == 0) c.redm[c.warp] = sm;
         __syncthreads();
         for (int w = 0; w < NW; ++w) es += c.redm[w];
         __syncthreads();
@@ -1101,8 +1167,10 @@ __global__ void __launch_bounds__(32 * NW, 1) fs1_stream_kernel(const StreamPara
       if (f) { ++l; flag = 2; break; }
     }
     // ---- lines 8-12: phi = a ./ (K psi)
-    tile_carries(c, P, par, c.QFm, c.QFe, c.QBm, c.QBe, c.QX[qi]);
-    HalfArgs B{Qm[qi], c.QX[qi], P.Am, c.AX, nullptr, nullptr, P.Pm, c.PX, c.PFm, c.PBm, c.PFe, c.PBe};
+    double* Qc = qi ? P.Qm1 : P.Qm0;
+    int* QXc = qi ? c.QX1 : c.QX0;
+    tile_carries(c, P, par, c.QFm, c.QFe, c.QBm, c.QBe, QXc);
+    HalfArgs B{Qc, QXc, P.Am, c.AX, nullptr, nullptr, P.Pm, c.PX, c.PFm, c.PBm, c.PFe, c.PBe, c.tzA};
     nonfinite = 0;
     stream_half<NW, S, true, false, true>(c, P, B, nonfinite);
     __syncthreads();
@@ -1120,13 +1188,15 @@ __global__ void __launch_bounds__(32 * NW, 1) fs1_stream_kernel(const StreamPara
       if (f) { flag = 2; break; }
     }
   }
+  double* Qf = qi ? P.Qm1 : P.Qm0;
+  int* QXf = qi ? c.QX1 : c.QX0;
   double cost = NAN;
-  if (flag != 2) cost = cost_phase<NW>(c, P, P.Pm, c.PX, Qm[qi], c.QX[qi]);
+  if (flag != 2) cost = cost_phase<NW>(c, P, P.Pm, c.PX, Qf, QXf);
   else errv = NAN;
   // outputs: F = log phi, G = log psi
   for (int i = c.warp; i < c.nt; i += NW) {
     from_tile(c, P, P.Pm, c.PX[i], true, dU, i);
-    from_tile(c, P, Qm[qi], c.QX[qi][i], true, dV, i);
+    from_tile(c, P, Qf, QXf[i], true, dV, i);
   }
   if (c.r == 0 && c.tid == 0) {
     if (P.iters) P.iters[0] = l;
