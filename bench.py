@@ -338,7 +338,7 @@ def run_fs1(args, cfg):
                                 "kernel_ms": kern_avg_s * 1e3,
                                 "peak_source": f"derived: {props.multi_processor_count} SMs x "
                                                f"{clk_mhz:.0f} MHz x 16 MUFU/clk / 2 rcp per update"}
-        if info["kernel"].startswith("stream"):
+        if info["kernel"].startswith(("stream", "sep2d")):
             # HBM roofline: SURVEY.md §8(d)'s 6 words per update (read x,
             # tgt and write y in both half-steps) x N x iterations; the once-per-solve
             # prologue, exit check, cost and epilogue passes (16 words per point) are

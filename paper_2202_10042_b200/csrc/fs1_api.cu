@@ -23,7 +23,8 @@ struct fs1_plan_s {
   PersistParams base;  // multipliers + scalars; pointers filled per call
   const StreamEntry* se;
   StreamParams sbase;  // K2: scalars + multiplier tables; pointers filled per call
-  int grid;            // K2: co-resident CTAs
+  Sep2dParams tbase;   // K3
+  int grid;            // K2 / K3: co-resident CTAs
   size_t smem;         // dynamic shared memory per CTA (>= the kernel's need; sized for occupancy)
   size_t ws;
   fs1_plan_info_t info;
@@ -33,7 +34,9 @@ namespace {
 
 constexpr int KIND_PERSIST = 0;
 constexpr int KIND_STREAM = 1;
+constexpr int KIND_SEP2D = 2;
 void er_pow(long double c, long double L, double* m, int* e);
+void fill_persist_tables(PersistParams& P, double c, int E);
 constexpr int TILE = 256;
 
 size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -143,6 +146,91 @@ StreamParams stream_params(const fs1_plan_s* p, void* ws) {
   P.gtot2e = (int*)(b + w.gtot2e);
   P.bar = (unsigned*)(b + w.bar);
   return P;
+}
+
+// K3 workspace: log a, (log b)^T, G ping-pong, pass scratch (fp32 [n m] each) + partials
+struct SepWs {
+  size_t LA, LBt, Gt0, Gt1, Z, part, flagp, bar, total;
+};
+SepWs sep_ws(size_t nm, int G) {
+  SepWs w;
+  size_t o = 0;
+  const size_t v = al256(nm * 4);
+  w.LA = o; o += v;
+  w.LBt = o; o += v;
+  w.Gt0 = o; o += v;
+  w.Gt1 = o; o += v;
+  w.Z = o; o += v;
+  w.part = o; o += al256((size_t)3 * G * 8);
+  w.flagp = o; o += al256((size_t)3 * G * 4);
+  w.bar = o; o += 256;
+  w.total = o;
+  return w;
+}
+
+fs1_status plan_sep2d(fs1_plan_s* p, int device) {
+  const fs1_desc& d = p->d;
+  if (d.dtype != FS1_F32 || d.domain != FS1_LOG) return FS1_ERR_UNSUPPORTED;
+  if (d.n > sep2d_lmax() || d.m > sep2d_lmax() || d.n * d.m > (1LL << 31)) return FS1_ERR_UNSUPPORTED;
+  const double c1 = d.h1 / d.eps, c2 = d.h2 / d.eps;
+  if (c1 * 8 > 40.0 || c2 * 8 > 40.0) return FS1_ERR_UNSUPPORTED;  // chunk span
+  int sms = 0;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return FS1_ERR_CUDA;
+  if (cudaFuncSetAttribute(sep2d_fn(), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sep2d_smem()) !=
+      cudaSuccess)
+    return FS1_ERR_CUDA;
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sep2d_fn(), 256, sep2d_smem()) != cudaSuccess)
+    return FS1_ERR_CUDA;
+  if (occ < 1) return FS1_ERR_UNSUPPORTED;
+  const long long lines = std::max(d.n, d.m);
+  const int G = (int)std::min<long long>((long long)sms * occ, std::max<long long>(1, lines));
+  p->kind = KIND_SEP2D;
+  p->grid = G;
+  p->smem = sep2d_smem();
+  Sep2dParams& P = p->tbase;
+  memset(&P, 0, sizeof(P));
+  fill_persist_tables(P.ax1, c1, 8);
+  fill_persist_tables(P.ax2, c2, 8);
+  P.ax1.lam = exp(-c1); P.ax1.h = d.h1;
+  P.ax2.lam = exp(-c2); P.ax2.h = d.h2;
+  P.n = (int)d.n;
+  P.m = (int)d.m;
+  P.G = G;
+  P.tol = d.tol;
+  P.itr_max = d.itr_max;
+  P.check_interval = d.check_interval;
+  P.warm = d.warm_start;
+  P.input_is_log = d.input_is_log;
+  p->ws = sep_ws((size_t)d.n * d.m, G).total;
+  snprintf(p->info.kernel, sizeof(p->info.kernel), "sep2d_f32_log_E8_W8");
+  p->info.chunk = 8;
+  p->info.threads = 256;
+  p->info.ctas_per_problem = G;
+  p->info.grid = G;
+  p->info.smem_bytes = p->smem;
+  p->info.workspace_bytes = p->ws;
+  return FS1_OK;
+}
+
+Sep2dParams sep_params(const fs1_plan_s* p, void* ws) {
+  Sep2dParams P = p->tbase;
+  const SepWs w = sep_ws((size_t)P.n * P.m, P.G);
+  char* b = (char*)ws;
+  P.LA = (float*)(b + w.LA);
+  P.LBt = (float*)(b + w.LBt);
+  P.Gt0 = (float*)(b + w.Gt0);
+  P.Gt1 = (float*)(b + w.Gt1);
+  P.Z = (float*)(b + w.Z);
+  P.part = (double*)(b + w.part);
+  P.flagp = (int*)(b + w.flagp);
+  P.bar = (unsigned*)(b + w.bar);
+  return P;
+}
+
+fs1_status launch_sep(const fs1_plan_s* p, Sep2dParams& P, cudaStream_t st) {
+  if (cudaMemsetAsync(P.bar, 0, 2 * sizeof(unsigned), st) != cudaSuccess) return FS1_ERR_CUDA;
+  return launch_sep2d(P, p->grid, st) == cudaSuccess ? FS1_OK : FS1_ERR_CUDA;
 }
 
 fs1_status launch_stream(const fs1_plan_s* p, StreamParams& P, cudaStream_t st) {
@@ -355,8 +443,13 @@ static fs1_status plan_impl(const fs1_desc* desc, int device, int force, fs1_pla
     p->info.smem_bytes = p->smem;
     p->info.workspace_bytes = 0;
   } else {
-    delete p;
-    return FS1_ERR_UNSUPPORTED;
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    int cur = 0;
+    if (cudaGetDevice(&cur) != cudaSuccess) { delete p; return FS1_ERR_CUDA; }
+    if (cur != device && cudaSetDevice(device) != cudaSuccess) { delete p; return FS1_ERR_CUDA; }
+    const fs1_status st = plan_sep2d(p, device);
+    if (cur != device) cudaSetDevice(cur);
+    if (st != FS1_OK) { delete p; return st; }
   }
   if (workspace_bytes) *workspace_bytes = p->ws;
   *out = p;
@@ -383,6 +476,15 @@ fs1_status fs1__set_debug(fs1_plan_t* plan, double* buf) {
   return FS1_OK;
 }
 
+// test-only (not in include/fs1.h): phase timestamps of the streaming kernel,
+// buf = [grid][64][4] u64 (globaltimer ns at: barrier exit, carries ready, stream
+// done, totals published) for the first 64 psi half-steps.
+fs1_status fs1__set_stream_timers(fs1_plan_t* plan, unsigned long long* buf) {
+  if (!plan) return FS1_ERR_ARG;
+  plan->sbase.tdbg = buf;
+  return FS1_OK;
+}
+
 fs1_status fs1_plan_info(const fs1_plan_t* plan, fs1_plan_info_t* info) {
   if (!plan || !info) return FS1_ERR_ARG;
   *info = plan->info;
@@ -402,6 +504,20 @@ fs1_status fs1_solve(const fs1_plan_t* plan, const void* a, const void* b, void*
     P.iters = iters; P.err = err; P.flags = flags; P.cost = cost;
     cudaError_t e = plan->pe->launch_solve(P, plan->d.batch, plan->smem, (cudaStream_t)stream);
     return e == cudaSuccess ? FS1_OK : FS1_ERR_CUDA;
+  }
+  if (plan->kind == KIND_SEP2D) {
+    const long long nm = plan->d.n * plan->d.m;
+    for (long long k = 0; k < plan->d.batch; ++k) {
+      Sep2dParams P = sep_params(plan, workspace);
+      P.a = (const float*)a + k * nm; P.b = (const float*)b + k * nm;
+      P.u = (float*)u + k * nm; P.v = (float*)v + k * nm;
+      P.iters = iters ? iters + k : nullptr; P.err = err ? err + k : nullptr;
+      P.flags = flags ? flags + k : nullptr; P.cost = cost ? cost + k : nullptr;
+      P.mode = 0;
+      const fs1_status st = launch_sep(plan, P, (cudaStream_t)stream);
+      if (st != FS1_OK) return st;
+    }
+    return FS1_OK;
   }
   if (plan->kind == KIND_STREAM) {
     if (plan->d.domain != FS1_LOG) return FS1_ERR_UNSUPPORTED;
@@ -440,6 +556,18 @@ fs1_status fs1_cost(const fs1_plan_t* plan, const void* u, const void* v, double
     cudaError_t e = plan->pe->launch_solve(P, plan->d.batch, plan->smem, (cudaStream_t)stream);
     return e == cudaSuccess ? FS1_OK : FS1_ERR_CUDA;
   }
+  if (plan->kind == KIND_SEP2D) {
+    const long long nm = plan->d.n * plan->d.m;
+    for (long long k = 0; k < plan->d.batch; ++k) {
+      Sep2dParams P = sep_params(plan, workspace);
+      P.u = (float*)const_cast<void*>(u) + k * nm; P.v = (float*)const_cast<void*>(v) + k * nm;
+      P.cost = cost + k;
+      P.mode = 2;
+      const fs1_status st = launch_sep(plan, P, (cudaStream_t)stream);
+      if (st != FS1_OK) return st;
+    }
+    return FS1_OK;
+  }
   if (plan->kind == KIND_STREAM) {
     for (long long k = 0; k < plan->d.batch; ++k) {
       StreamParams P = stream_params(plan, workspace);
@@ -461,6 +589,17 @@ fs1_status fs1_apply(const fs1_plan_t* plan, const void* x, void* y, void* works
   if (plan->kind == KIND_PERSIST) {
     cudaError_t e = plan->pe->launch_apply(plan->base, x, y, plan->d.batch, (cudaStream_t)stream);
     return e == cudaSuccess ? FS1_OK : FS1_ERR_CUDA;
+  }
+  if (plan->kind == KIND_SEP2D) {
+    const long long nm = plan->d.n * plan->d.m;
+    for (long long k = 0; k < plan->d.batch; ++k) {
+      Sep2dParams P = sep_params(plan, workspace);
+      P.x = (const float*)x + k * nm; P.y = (float*)y + k * nm;
+      P.mode = 1;
+      const fs1_status st = launch_sep(plan, P, (cudaStream_t)stream);
+      if (st != FS1_OK) return st;
+    }
+    return FS1_OK;
   }
   if (plan->kind == KIND_STREAM) {
     for (long long k = 0; k < plan->d.batch; ++k) {

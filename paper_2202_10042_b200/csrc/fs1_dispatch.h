@@ -34,4 +34,10 @@ struct StreamEntry {
 const StreamEntry* stream_table(int* count);
 size_t stream_smem(int NW, int S, int ntmax, int G);
 
+// K3 separable 2D kernel (fs1_sep2d.cu)
+cudaError_t launch_sep2d(const Sep2dParams& P, int grid, cudaStream_t st);
+const void* sep2d_fn();
+size_t sep2d_smem();
+int sep2d_lmax();
+
 }  // namespace fs1

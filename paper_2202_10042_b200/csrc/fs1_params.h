@@ -68,6 +68,7 @@ struct StreamParams {
   double* gtot2;     // [G][8] cost-phase range totals (p, P', t, Q') m
   int* gtot2e;       // [G][8]
   unsigned* bar;     // grid barrier {count, generation}
+  unsigned long long* tdbg;  // optional phase timestamps (test-only), [G][64 half-steps][4]
   long long n;
   long long npad;    // ntiles * 256
   int ntiles;
@@ -86,6 +87,33 @@ struct StreamParams {
   double lanepow[32];  // lambda^{8 l}
   double t2m[20];    // lambda^{256 * 2^j} as mantissa in [1,2) ...
   int t2e[20];       // ... and binary exponent (Remark 3.3: never formed alone in fp64)
+};
+
+// Separable 2D kernel (K3 in SURVEY.md §2.2), fp32 log domain, one problem per launch.
+struct Sep2dParams {
+  PersistParams ax1;  // scan tables of axis 1 (lambda1 = e^{-h1/eps}, h1), E = 8
+  PersistParams ax2;  // axis 2 (lambda2, h2)
+  const void* a;      // [n*m] column-major (log-weights when input_is_log)
+  const void* b;
+  void* u;            // [n*m] F = log phi, column-major (state, in place)
+  void* v;            // [n*m] G = log psi, column-major (written at exit)
+  int32_t* iters;
+  double* err;
+  int32_t* flags;
+  double* cost;
+  const void* x;      // apply input / output (column-major logs)
+  void* y;
+  float* LA;          // [n*m] log a, column-major
+  float* LBt;         // [m*n] log b, row-major (transposed)
+  float* Gt0;         // [m*n] G, row-major, ping-pong pair
+  float* Gt1;
+  float* Z;           // [n*m] pass scratch
+  double* part;       // [3][G] per-CTA partial sums
+  int* flagp;         // [3][G]
+  unsigned* bar;
+  int n, m, G;
+  double tol;
+  int itr_max, check_interval, warm, input_is_log, mode;
 };
 
 }  // namespace fs1

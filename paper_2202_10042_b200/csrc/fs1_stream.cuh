@@ -49,7 +49,7 @@ constexpr double INV_LN2 = 1.44269504088896338700e+00;
 
 // ------------------------------------------------------------------ shared layout
 struct Layout {
-  size_t stage, mbar, pwm, pwe, ax, bx, px, qx0, qx1, pfm, pbm, pfe, pbe, qfm, qbm, qfe, qbe, cfr,
+  size_t stage, mbar, pwm, pwd, pwe, ax, bx, px, qx0, qx1, pfm, pbm, pfe, pbe, qfm, qbm, qfe, qbe, cfr,
       cbr, rr, errt, redm, rede, dpm, dpe, tza, tzb, total;
 };
 
@@ -66,6 +66,7 @@ __host__ __device__ inline Layout layout(int NW, int S, int ntmax, int G) {
   L.tza = o;   o = al16(o + nt);
   L.tzb = o;   o = al16(o + nt);
   L.pwm = o;   o = al16(o + nt * 8);
+  L.pwd = o;   o = al16(o + nt * 8);
   L.pfm = o;   o = al16(o + nt * 8);
   L.pbm = o;   o = al16(o + nt * 8);
   L.qfm = o;   o = al16(o + nt * 8);
@@ -197,6 +198,12 @@ __device__ __forceinline__ double fdiv(double t, double x) {
   return fma(r, rem, q);
 }
 
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -206,23 +213,18 @@ __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// Grid-wide barrier of the co-resident CTAs (cooperative launch guarantees
-// residency).  bar[0] counts arrivals, bar[1] is the generation.
+// Grid-wide barrier of the co-resident CTAs (the cooperative launch guarantees
+// residency): one release-add per CTA on a monotonic counter, then an acquire
+// spin until it reaches G x (barriers so far).  bar[0] must be 0 at launch.
 __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned G, unsigned& gen) {
   __syncthreads();
   if (threadIdx.x == 0) {
     fence_async();
     __threadfence();
-    const unsigned g = gen;
-    const unsigned prev = atomicAdd(bar, 1u);
-    if (prev == G - 1) {
-      atomicExch(bar, 0u);
-      __threadfence();
-      st_release(bar + 1, g + 1);
-    } else {
-      while (ld_acquire(bar + 1) == g) __nanosleep(20);
+    const unsigned target = (gen + 1) * G;
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+    while (ld_acquire(bar) < target) {
     }
-    __threadfence();
     fence_async();
   }
   ++gen;
@@ -230,47 +232,45 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned G, unsigned
 }
 
 // ------------------------------------------------------------------ swizzled tiles
-// Lane l owns points [8l, 8l+8) of a tile = 4 double2 chunks at 16-byte slots
-// 4l..4l+3.  Instruction j touches chunk j ^ sw(l), sw = (l>>1)&3: the 8 lanes of
-// a 128-bit phase then hit 8 distinct 16-byte bank groups (no conflicts); two
-// conditional swaps restore the natural order in registers.
-__device__ __forceinline__ void csw(double2& a, double2& b, bool c) {
-  const double2 x = a, y = b;
-  a.x = c ? y.x : x.x; a.y = c ? y.y : x.y;
-  b.x = c ? x.x : y.x; b.y = c ? x.y : y.y;
-}
+// Lane l owns points [8l, 8l+8) of a tile = 4 double2 chunks.  Every internal
+// vector (workspace mantissas of a, b, phi, psi) stores chunk j of lane l at
+// 16-byte slot 4l + (j ^ sw(l)), sw = (l>>1)&3, in global AND shared memory (the
+// TMA copies are verbatim).  Instruction j of a warp then touches slots
+// 4l + (j ^ sw): the 8 lanes of a 128-bit phase hit 8 distinct bank groups
+// (conflict-free) and registers come out in natural order with no selects.
+__device__ __forceinline__ int swz(int lane) { return (lane >> 1) & 3; }
 __device__ __forceinline__ void lds_tile(const double* base, int lane, double (&v)[E]) {
-  const int sw = (lane >> 1) & 3;
+  const int sw = swz(lane);
   const double2* p = reinterpret_cast<const double2*>(base) + lane * 4;
-  double2 r0 = p[0 ^ sw], r1 = p[1 ^ sw], r2 = p[2 ^ sw], r3 = p[3 ^ sw];
-  csw(r0, r1, sw & 1); csw(r2, r3, sw & 1);
-  csw(r0, r2, sw & 2); csw(r1, r3, sw & 2);
-  v[0] = r0.x; v[1] = r0.y; v[2] = r1.x; v[3] = r1.y;
-  v[4] = r2.x; v[5] = r2.y; v[6] = r3.x; v[7] = r3.y;
-}
-__device__ __forceinline__ void sts_tile(double* base, int lane, const double (&v)[E]) {
-  const int sw = (lane >> 1) & 3;
-  double2 r0 = make_double2(v[0], v[1]), r1 = make_double2(v[2], v[3]);
-  double2 r2 = make_double2(v[4], v[5]), r3 = make_double2(v[6], v[7]);
-  csw(r0, r2, sw & 2); csw(r1, r3, sw & 2);
-  csw(r0, r1, sw & 1); csw(r2, r3, sw & 1);
-  double2* p = reinterpret_cast<double2*>(base) + lane * 4;
-  p[0 ^ sw] = r0; p[1 ^ sw] = r1; p[2 ^ sw] = r2; p[3 ^ sw] = r3;
-}
-// plain blocked global access (prologue / epilogue / cost phase)
-__device__ __forceinline__ void ldg_tile(const double* g, int lane, double (&v)[E]) {
-  const double2* p = reinterpret_cast<const double2*>(g + lane * E);
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    const double2 t = __ldcg(p + j);
+    const double2 t = p[j ^ sw];
+    v[2 * j] = t.x;
+    v[2 * j + 1] = t.y;
+  }
+}
+__device__ __forceinline__ void sts_tile(double* base, int lane, const double (&v)[E]) {
+  const int sw = swz(lane);
+  double2* p = reinterpret_cast<double2*>(base) + lane * 4;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) p[j ^ sw] = make_double2(v[2 * j], v[2 * j + 1]);
+}
+// the same permuted layout from / to global memory (prologue, epilogue, cost, check)
+__device__ __forceinline__ void ldg_tile(const double* g, int lane, double (&v)[E]) {
+  const int sw = swz(lane);
+  const double2* p = reinterpret_cast<const double2*>(g) + lane * 4;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const double2 t = __ldcg(p + (j ^ sw));
     v[2 * j] = t.x;
     v[2 * j + 1] = t.y;
   }
 }
 __device__ __forceinline__ void stg_tile(double* g, int lane, const double (&v)[E]) {
-  double2* p = reinterpret_cast<double2*>(g + lane * E);
+  const int sw = swz(lane);
+  double2* p = reinterpret_cast<double2*>(g) + lane * 4;
 #pragma unroll
-  for (int j = 0; j < 4; ++j) p[j] = make_double2(v[2 * j], v[2 * j + 1]);
+  for (int j = 0; j < 4; ++j) p[j ^ sw] = make_double2(v[2 * j], v[2 * j + 1]);
 }
 
 // ------------------------------------------------------------------ context
@@ -284,6 +284,7 @@ struct Ctx {
   unsigned char* tzA;   // tile of a / b has a zero (or padding) entry
   unsigned char* tzB;
   double* pwm;
+  double* pwd;  // lambda^{256 k} as a plain double (0 once it underflows)
   int* pwe;
   int* AX;
   int* BX;
@@ -365,8 +366,8 @@ __device__ __forceinline__ void put_totals(int lane, double Fi, double Gi, int Y
 // In: F/B hold per-tile totals (forward at the tile end, backward at the tile start).
 // Out (in place): exclusive local carries CFloc_i = sum_{i'<i} lambda^{256(i-1-i')} FT_i',
 // CBloc_i = sum_{i'>i} lambda^{256(i'-i-1)} GT_i'; returns the range totals.
-__device__ __forceinline__ void block_tile_scan(Ctx& c, double* Fm, int* Fe, double* Bm, int* Be, ER<double>& totF,
-                                ER<double>& totB) {
+__device__ __forceinline__ void block_tile_scan_er(Ctx& c, double* Fm, int* Fe, double* Bm, int* Be,
+                                                   ER<double>& totF, ER<double>& totB) {
   const int nt = c.nt, NT = c.NT, lane = c.lane, warp = c.warp;
   const int q = (nt + NT - 1) / NT;
   const int i0 = min(nt, c.tid * q), i1 = min(nt, i0 + q);
@@ -422,6 +423,89 @@ __device__ __forceinline__ void block_tile_scan(Ctx& c, double* Fm, int* Fe, dou
   __syncthreads();
   totF = ER<double>{wFm[0], wFe[0]};
   totB = ER<double>{wGm[0], wGe[0]};
+  __syncthreads();
+}
+
+// The same scan in plain fp64 relative to 2^M (M = the largest tile exponent of the
+// range) when every nonzero total lies within 2^900 of it — always so at C3 — and in
+// extended range otherwise.  Contributions that underflow relative to 2^M are below
+// 2^-122 of every tile they reach.
+__device__ __forceinline__ void block_tile_scan(Ctx& c, double* Fm, int* Fe, double* Bm, int* Be, ER<double>& totF,
+                                                ER<double>& totB) {
+  const int nt = c.nt, NT = c.NT, lane = c.lane, warp = c.warp;
+  int mx = ZE, mn = 0x7fffffff;
+  for (int i = c.tid; i < nt; i += NT) {
+    if (Fm[i] > 0.0) { mx = max(mx, Fe[i]); mn = min(mn, Fe[i]); }
+    if (Bm[i] > 0.0) { mx = max(mx, Be[i]); mn = min(mn, Be[i]); }
+  }
+  mx = warp_max(mx);
+  mn = warp_min(mn);
+  int* wi = c.rede + 384;
+  __syncthreads();
+  if (lane == 0) { wi[warp] = mx; wi[32 + warp] = mn; }
+  __syncthreads();
+  mx = ZE;
+  mn = 0x7fffffff;
+  for (int w = 0; w < c.NW; ++w) { mx = max(mx, wi[w]); mn = min(mn, wi[32 + w]); }
+  if (mx != ZE && mn < mx - 900) {
+    block_tile_scan_er(c, Fm, Fe, Bm, Be, totF, totB);
+    return;
+  }
+  const int M = (mx == ZE) ? 0 : mx;
+  const int q = (nt + NT - 1) / NT;
+  const int i0 = min(nt, c.tid * q), i1 = min(nt, i0 + q);
+  const double L1 = c.pwd[1];
+  double f = 0.0, g = 0.0;
+  for (int i = i0; i < i1; ++i) f = fma(f, L1, Fm[i] * pow2d(max(Fe[i] - M, -1100)));
+  for (int i = i1 - 1; i >= i0; --i) g = fma(g, L1, Bm[i] * pow2d(max(Be[i] - M, -1100)));
+  int sF = i1 - i0, sG = i1 - i0;
+  double F = f, G = g;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const double uf = __shfl_up_sync(FULL, F, d);
+    const int us = __shfl_up_sync(FULL, sF, d);
+    const double dg = __shfl_down_sync(FULL, G, d);
+    const int ds = __shfl_down_sync(FULL, sG, d);
+    if (lane >= d) { F = fma(uf, c.pwd[sF], F); sF += us; }
+    if (lane + d < 32) { G = fma(dg, c.pwd[sG], G); sG += ds; }
+  }
+  double eF = __shfl_up_sync(FULL, F, 1);
+  int esF = __shfl_up_sync(FULL, sF, 1);
+  double eG = __shfl_down_sync(FULL, G, 1);
+  int esG = __shfl_down_sync(FULL, sG, 1);
+  if (lane == 0) { eF = 0.0; esF = 0; }
+  if (lane == 31) { eG = 0.0; esG = 0; }
+  double* wF = c.redm;
+  double* wG = c.redm + 64;
+  int* wFs = c.rede + 128;
+  int* wGs = c.rede + 192;
+  __syncthreads();
+  if (lane == 31) { wF[warp] = F; wFs[warp] = sF; }
+  if (lane == 0) { wG[warp] = G; wGs[warp] = sG; }
+  __syncthreads();
+  double cw = 0.0, cg = 0.0;
+  for (int w = 0; w < warp; ++w) cw = fma(cw, c.pwd[wFs[w]], wF[w]);
+  for (int w = c.NW - 1; w > warp; --w) cg = fma(cg, c.pwd[wGs[w]], wG[w]);
+  double cf = fma(cw, c.pwd[esF], eF);
+  double cb = fma(cg, c.pwd[esG], eG);
+  for (int i = i0; i < i1; ++i) {
+    const double t = Fm[i] * pow2d(max(Fe[i] - M, -1100));
+    const ER<double> o = er_norm<double>(cf, M);
+    Fm[i] = o.m; Fe[i] = o.e;
+    cf = fma(cf, L1, t);
+  }
+  for (int i = i1 - 1; i >= i0; --i) {
+    const double t = Bm[i] * pow2d(max(Be[i] - M, -1100));
+    const ER<double> o = er_norm<double>(cb, M);
+    Bm[i] = o.m; Be[i] = o.e;
+    cb = fma(cb, L1, t);
+  }
+  __syncthreads();
+  if (c.tid == NT - 1) { wF[0] = cf; }
+  if (c.tid == 0) { wG[0] = cb; }
+  __syncthreads();
+  totF = er_norm<double>(wF[0], M);
+  totB = er_norm<double>(wG[0], M);
   __syncthreads();
 }
 
@@ -510,8 +594,13 @@ struct HalfArgs {
 // Each warp streams the tiles i = warp, warp + NW, ... of this range through its
 // S-stage ring; y overwrites x in the stage and leaves by TMA bulk store; a stage
 // is refilled (S - 1 tiles ahead) once the store of its previous tile has read it.
+// Prefetch: `pre` = the first S-1 tiles of this half-step were already issued by the
+// previous call; (nx, nt_) != null = issue the next half-step's first S-1 tiles
+// (x = the y this warp just produced, target nt_) before the grid barrier.
 template <int NW, int S, bool DIV, bool CHECK, bool WRITE>
-__device__ __forceinline__ void stream_half(Ctx& c, const StreamParams& P, const HalfArgs& A, int& nonfinite) {
+__device__ __forceinline__ void stream_half(Ctx& c, const StreamParams& P, const HalfArgs& A, int& nonfinite,
+                                            bool pre = false, const double* nx = nullptr,
+                                            const double* ntg = nullptr) {
   const int lane = c.lane, w = c.warp;
   const long long gbase = (long long)c.T0 * TILE;
   double* stg = c.stage + (size_t)w * S * 2 * TILE;
@@ -528,7 +617,7 @@ __device__ __forceinline__ void stream_half(Ctx& c, const StreamParams& P, const
     bulk_g2s(stg + (s * 2) * TILE, A.xg + gbase + (long long)i * TILE, TBYTES, &mb[s]);
     if (LOADT) bulk_g2s(stg + (s * 2 + 1) * TILE, A.tg + gbase + (long long)i * TILE, TBYTES, &mb[s]);
   };
-  if (lane == 0) {
+  if (lane == 0 && !pre) {
     fence_async();
 #pragma unroll
     for (int k = 0; k < S - 1; ++k) issue(k);
@@ -626,7 +715,29 @@ __device__ __forceinline__ void stream_half(Ctx& c, const StreamParams& P, const
     }
   }
   if (WRITE && lane == 0) bulk_wait_all();
+  if (nx && lane == 0) {  // next half-step: same tiles of this warp, stages 0..S-2
+    fence_async();
+#pragma unroll
+    for (int k2 = 0; k2 < S - 1; ++k2) {
+      const int i = w + k2 * NW;
+      if (i >= c.nt) break;
+      mbar_expect_tx(&mb[k2], 2 * TBYTES);
+      bulk_g2s(stg + (k2 * 2) * TILE, nx + gbase + (long long)i * TILE, TBYTES, &mb[k2]);
+      bulk_g2s(stg + (k2 * 2 + 1) * TILE, ntg + gbase + (long long)i * TILE, TBYTES, &mb[k2]);
+    }
+  }
   if (__any_sync(FULL, bad)) nonfinite = 1;
+}
+
+// Wait out prefetched loads that will not be consumed (the solve stops).
+template <int NW, int S>
+__device__ __forceinline__ void drain_prefetch(Ctx& c) {
+  uint64_t* mb = c.mbar + c.warp * S;
+  for (int k = 0; k < S - 1; ++k) {
+    if (c.warp + k * NW >= c.nt) break;
+    mbar_wait(&mb[k], (c.phase >> k) & 1u);
+    c.phase ^= (1u << k);
+  }
 }
 
 // ---------------------------------------------------------------- prologue/epilogue
@@ -1022,6 +1133,7 @@ __global__ void __launch_bounds__(32 * NW, 1) fs1_stream_kernel(const __grid_con
   c.tzA = smem + L.tza;
   c.tzB = smem + L.tzb;
   c.pwm = reinterpret_cast<double*>(smem + L.pwm);
+  c.pwd = reinterpret_cast<double*>(smem + L.pwd);
   c.pwe = reinterpret_cast<int*>(smem + L.pwe);
   c.AX = reinterpret_cast<int*>(smem + L.ax);
   c.BX = reinterpret_cast<int*>(smem + L.bx);
@@ -1053,6 +1165,7 @@ __global__ void __launch_bounds__(32 * NW, 1) fs1_stream_kernel(const __grid_con
     const ER<double> t = pow_tiles(P, k);
     c.pwm[k] = t.m;
     c.pwe[k] = t.e;
+    c.pwd[k] = er_rel(t, 0);
   }
   for (int k = c.tid; k < P.G; k += c.NT) {  // decay from range k to this range
     const ER<double> t = (k == c.r) ? er_zero<double>() : pow_tiles(P, range_gap(P, k, c.r));
@@ -1113,12 +1226,16 @@ __global__ void __launch_bounds__(32 * NW, 1) fs1_stream_kernel(const __grid_con
   }
   const bool use_tol = P.tol > 0.0;
   int l = 0, qi = 0, flag = 0;
+  bool pre = false;
   double errv = NAN;
   while (true) {
     const bool check = (l >= P.itr_max) || (use_tol && (l % P.check_interval) == 0);
     const bool last = l >= P.itr_max;
     // ---- lines 2-7: psi = b ./ (K^T phi), with the marginal error on check iterations
+    unsigned long long* td = (P.tdbg && c.tid == 0 && l < 64) ? P.tdbg + ((size_t)c.r * 64 + l) * 4 : nullptr;
+    if (td) td[0] = gtimer();
     tile_carries(c, P, par, c.PFm, c.PFe, c.PBm, c.PBe, c.PX);
+    if (td) td[1] = gtimer();
     const int qo = check ? (qi ^ 1) : qi;  // a checking step keeps psi^(l) in Qm[qi]
     double* Qi = qi ? P.Qm1 : P.Qm0;
     int* QXi = qi ? c.QX1 : c.QX0;
@@ -1126,10 +1243,13 @@ __global__ void __launch_bounds__(32 * NW, 1) fs1_stream_kernel(const __grid_con
     int* QXo = qo ? c.QX1 : c.QX0;
     HalfArgs A{P.Pm, c.PX, P.Bm, c.BX, Qi, QXi, Qo, QXo, c.QFm, c.QBm, c.QFe, c.QBe, c.tzB};
     nonfinite = 0;
-    if (!check) stream_half<NW, S, true, false, true>(c, P, A, nonfinite);
-    else if (!last) stream_half<NW, S, true, true, true>(c, P, A, nonfinite);
-    else stream_half<NW, S, true, true, false>(c, P, A, nonfinite);
+    // a non-checking psi step is always followed by the phi step: prefetch its tiles
+    if (!check) stream_half<NW, S, true, false, true>(c, P, A, nonfinite, pre, Qo, P.Am);
+    else if (!last) stream_half<NW, S, true, true, true>(c, P, A, nonfinite, pre);
+    else stream_half<NW, S, true, true, false>(c, P, A, nonfinite, pre);
+    pre = !check;
     __syncthreads();
+    if (td) td[2] = gtimer();
     {
       ER<double> tF = er_zero<double>(), tB = er_zero<double>();
       if (!last) block_tile_scan(c, c.QFm, c.QFe, c.QBm, c.QBe, tF, tB);
@@ -1149,6 +1269,7 @@ __global__ void __launch_bounds__(32 * NW, 1) fs1_stream_kernel(const __grid_con
       }
       const int nf = __syncthreads_or(nonfinite);
       publish(c, P, par ^ 1, tF, tB, es, nf);
+      if (td) td[3] = gtimer();
       grid_barrier(P.bar, P.G, c.gen);
       par ^= 1;
     }
@@ -1164,7 +1285,10 @@ __global__ void __launch_bounds__(32 * NW, 1) fs1_stream_kernel(const __grid_con
         }
         qi ^= 1;
       }
-      if (f) { ++l; flag = 2; break; }
+      if (f) {
+        if (pre) drain_prefetch<NW, S>(c);
+        ++l; flag = 2; break;
+      }
     }
     // ---- lines 8-12: phi = a ./ (K psi)
     double* Qc = qi ? P.Qm1 : P.Qm0;
@@ -1172,7 +1296,8 @@ __global__ void __launch_bounds__(32 * NW, 1) fs1_stream_kernel(const __grid_con
     tile_carries(c, P, par, c.QFm, c.QFe, c.QBm, c.QBe, QXc);
     HalfArgs B{Qc, QXc, P.Am, c.AX, nullptr, nullptr, P.Pm, c.PX, c.PFm, c.PBm, c.PFe, c.PBe, c.tzA};
     nonfinite = 0;
-    stream_half<NW, S, true, false, true>(c, P, B, nonfinite);
+    stream_half<NW, S, true, false, true>(c, P, B, nonfinite, pre, P.Pm, P.Bm);
+    pre = true;  // the next psi step reads phi (just written) and b
     __syncthreads();
     {
       ER<double> tF, tB;
@@ -1185,7 +1310,10 @@ __global__ void __launch_bounds__(32 * NW, 1) fs1_stream_kernel(const __grid_con
       int f;
       read_slot(c, P, par, e, f);
       ++l;  // line 13
-      if (f) { flag = 2; break; }
+      if (f) {
+        drain_prefetch<NW, S>(c);
+        flag = 2; break;
+      }
     }
   }
   double* Qf = qi ? P.Qm1 : P.Qm0;

@@ -72,7 +72,10 @@ class Plan:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h is not None and h.value:
-            L.lib().fs1_plan_destroy(h)
+            try:
+                L.lib().fs1_plan_destroy(h)
+            except Exception:  # interpreter shutdown: module globals already torn down
+                pass
             self._h = None
 
     def info(self) -> dict:
