@@ -210,6 +210,7 @@ def run_fs1(args, cfg):
     import torch
     import torch.distributed as dist
 
+    from paper_2202_10042_b200 import dist as fdist
     from paper_2202_10042_b200 import fs1
 
     ws, rank, local = dist_env()
@@ -218,7 +219,8 @@ def run_fs1(args, cfg):
     torch.cuda.set_device(local)
     dev = torch.device(f"cuda:{local}")
     B = per_gpu_batch(cfg, args)
-    pair_ids = range(rank * B, (rank + 1) * B)
+    total = B * ws                      # weak scaling: B pairs per GPU
+    pair_ids = fdist.shard(total, rank, ws)
     A, Bm = gi.batch(cfg, pair_ids)
     tdt = torch.float32 if cfg.dtype == "f32" else torch.float64
     a = torch.from_numpy(A).to(dev)
@@ -233,16 +235,13 @@ def run_fs1(args, cfg):
     err = torch.empty(B, dtype=torch.float64, device=dev)
     flags = torch.empty(B, dtype=torch.int32, device=dev)
     cost = torch.empty(B, dtype=torch.float64, device=dev)
-    res = torch.empty((B, 4), dtype=torch.float64, device=dev)
-    gathered = torch.empty((ws * B, 4), dtype=torch.float64, device=dev) if ws > 1 else None
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > L2 (126 MB)
     stream = torch.cuda.current_stream(dev)
 
     def step():
         plan.solve_into(a, b, u, v, iters, err, flags, cost)
         if ws > 1:   # the one collective of the path: gather per-pair results (NCCL)
-            torch.stack([cost, err, iters.double(), flags.double()], 1, out=res)
-            dist.all_gather_into_tensor(gathered, res)
+            fdist.gather_results(fdist.pack_results(cost, err, iters, flags), total)
 
     for _ in range(args.warmup):
         step()
@@ -264,8 +263,7 @@ def run_fs1(args, cfg):
             plan.solve_into(a, b, u, v, iters, err, flags, cost)
             kev[i][1].record(stream)
             if ws > 1:
-                torch.stack([cost, err, iters.double(), flags.double()], 1, out=res)
-                dist.all_gather_into_tensor(gathered, res)
+                fdist.gather_results(fdist.pack_results(cost, err, iters, flags), total)
             ev[i][1].record(stream)
         torch.cuda.synchronize()
         if ws > 1:
