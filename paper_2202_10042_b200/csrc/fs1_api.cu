@@ -25,6 +25,8 @@ struct fs1_plan_s {
   StreamParams sbase;  // K2: scalars + multiplier tables; pointers filled per call
   Sep2dParams tbase;   // K3
   int grid;            // K2 / K3: co-resident CTAs
+  const Sep2dwEntry* sw = nullptr;  // K3w solve kernel (nullptr: K3)
+  int gridw = 0;                    // K3w co-resident CTAs
   size_t smem;         // dynamic shared memory per CTA (>= the kernel's need; sized for occupancy)
   size_t ws;
   fs1_plan_info_t info;
@@ -81,6 +83,7 @@ fs1_status plan_stream(fs1_plan_s* p, int device, int variant) {
     return FS1_ERR_CUDA;
   const long long ntiles = (d.n + TILE - 1) / TILE;
   if (ntiles > (1LL << 30)) return FS1_ERR_UNSUPPORTED;
+
   const int G = (int)std::min<long long>(sms, ntiles);
   const int ntmax = (int)((ntiles + G - 1) / G);
   int cnt = 0;
@@ -148,27 +151,33 @@ StreamParams stream_params(const fs1_plan_s* p, void* ws) {
   return P;
 }
 
-// K3 workspace: log a, (log b)^T, G ping-pong, pass scratch (fp32 [n m] each) + partials
+// K3 / K3w workspace: log a, (log b)^T, G ping-pong, two pass scratches, F (K3w), fp32
+// arrays of max(n m, lines x LP) floats each, + per-CTA partials and the barrier
 struct SepWs {
-  size_t LA, LBt, Gt0, Gt1, Z, part, flagp, bar, total;
+  size_t LA, LBt, Gt0, Gt1, Z, Z2, Fp, part, flagp, bar, total;
 };
-SepWs sep_ws(size_t nm, int G) {
+SepWs sep_ws(size_t nm, size_t nperm, int G) {
   SepWs w;
   size_t o = 0;
-  const size_t v = al256(nm * 4);
+  const size_t v = al256(std::max(nm, nperm) * 4);
   w.LA = o; o += v;
   w.LBt = o; o += v;
   w.Gt0 = o; o += v;
   w.Gt1 = o; o += v;
   w.Z = o; o += v;
+  w.Z2 = o; o += nperm ? v : 0;
+  w.Fp = o; o += nperm ? v : 0;
   w.part = o; o += al256((size_t)3 * G * 8);
   w.flagp = o; o += al256((size_t)3 * G * 4);
   w.bar = o; o += 256;
   w.total = o;
   return w;
 }
+size_t sep_nperm(const Sep2dParams& P) {
+  return P.wE ? (size_t)std::max(P.n, P.m) * 32 * P.wE : 0;
+}
 
-fs1_status plan_sep2d(fs1_plan_s* p, int device) {
+fs1_status plan_sep2d(fs1_plan_s* p, int device, int force) {
   const fs1_desc& d = p->d;
   if (d.dtype != FS1_F32 || d.domain != FS1_LOG) return FS1_ERR_UNSUPPORTED;
   if (d.n > sep2d_lmax() || d.m > sep2d_lmax() || d.n * d.m > (1LL << 31)) return FS1_ERR_UNSUPPORTED;
@@ -202,26 +211,72 @@ fs1_status plan_sep2d(fs1_plan_s* p, int device) {
   P.check_interval = d.check_interval;
   P.warm = d.warm_start;
   P.input_is_log = d.input_is_log;
-  p->ws = sep_ws((size_t)d.n * d.m, G).total;
   snprintf(p->info.kernel, sizeof(p->info.kernel), "sep2d_f32_log_E8_W8");
   p->info.chunk = 8;
   p->info.threads = 256;
   p->info.ctas_per_problem = G;
   p->info.grid = G;
-  p->info.smem_bytes = p->smem;
+  // K3w (warp-per-line solve): the smallest chunk E whose 32 E covers both axes and
+  // whose span c E stays within the fp32 chunk range
+  P.wE = 0;
+  p->sw = nullptr;
+  if (force != 3) {
+    int cnt = 0;
+    const Sep2dwEntry* tab = sep2dw_table(&cnt);
+    for (int i = 0; i < cnt; ++i) {
+      const int E = tab[i].E;
+      if (32LL * E < std::max(d.n, d.m) || c1 * E > 40.0 || c2 * E > 40.0) continue;
+      if (p->sw && p->sw->E <= E) continue;
+      if (cudaFuncSetAttribute(tab[i].fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tab[i].smem) !=
+          cudaSuccess)
+        return FS1_ERR_CUDA;
+      int o2 = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, tab[i].fn, 256, tab[i].smem) != cudaSuccess)
+        return FS1_ERR_CUDA;
+      if (o2 < 1) continue;
+      p->sw = &tab[i];
+      const long long groups = (std::max(d.n, d.m) + 7) / 8;
+      p->gridw = (int)std::min<long long>((long long)sms * o2, groups);
+    }
+    if (p->sw) {
+      const int E = p->sw->E;
+      P.wE = E;
+      const double cs[2] = {c1, c2};
+      for (int ax = 0; ax < 2; ++ax) {
+        const long double C = (long double)cs[ax];
+        P.wax[ax].lam = (float)expl(-C);
+        P.wax[ax].lamH = (float)expl(-C * (long double)(E / 2));
+        for (int k = 0; k < 5; ++k) {
+          double m;
+          er_pow(C, (long double)E * (1 << k), &m, &P.wax[ax].Le[k]);
+          P.wax[ax].Lm[k] = (float)m;
+          if (P.wax[ax].Lm[k] >= 2.0f) { P.wax[ax].Lm[k] *= 0.5f; P.wax[ax].Le[k] += 1; }
+        }
+      }
+      snprintf(p->info.kernel, sizeof(p->info.kernel), "sep2dw_f32_log_E%d_W8", E);
+      p->info.chunk = E;
+      p->info.ctas_per_problem = p->gridw;
+      p->info.grid = p->gridw;
+      p->info.smem_bytes = p->sw->smem;
+    }
+  }
+  p->ws = sep_ws((size_t)d.n * d.m, sep_nperm(P), std::max(G, p->gridw)).total;
+  if (!p->sw) p->info.smem_bytes = p->smem;
   p->info.workspace_bytes = p->ws;
   return FS1_OK;
 }
 
 Sep2dParams sep_params(const fs1_plan_s* p, void* ws) {
   Sep2dParams P = p->tbase;
-  const SepWs w = sep_ws((size_t)P.n * P.m, P.G);
+  const SepWs w = sep_ws((size_t)P.n * P.m, sep_nperm(P), std::max(P.G, p->gridw));
   char* b = (char*)ws;
   P.LA = (float*)(b + w.LA);
   P.LBt = (float*)(b + w.LBt);
   P.Gt0 = (float*)(b + w.Gt0);
   P.Gt1 = (float*)(b + w.Gt1);
   P.Z = (float*)(b + w.Z);
+  P.Z2 = P.wE ? (float*)(b + w.Z2) : nullptr;
+  P.Fp = P.wE ? (float*)(b + w.Fp) : nullptr;
   P.part = (double*)(b + w.part);
   P.flagp = (int*)(b + w.flagp);
   P.bar = (unsigned*)(b + w.bar);
@@ -230,6 +285,10 @@ Sep2dParams sep_params(const fs1_plan_s* p, void* ws) {
 
 fs1_status launch_sep(const fs1_plan_s* p, Sep2dParams& P, cudaStream_t st) {
   if (cudaMemsetAsync(P.bar, 0, 2 * sizeof(unsigned), st) != cudaSuccess) return FS1_ERR_CUDA;
+  if (P.mode == 0 && p->sw) {  // solve: the warp-per-line kernel K3w
+    P.G = p->gridw;
+    return p->sw->launch(P, p->gridw, st) == cudaSuccess ? FS1_OK : FS1_ERR_CUDA;
+  }
   return launch_sep2d(P, p->grid, st) == cudaSuccess ? FS1_OK : FS1_ERR_CUDA;
 }
 
@@ -447,7 +506,7 @@ static fs1_status plan_impl(const fs1_desc* desc, int device, int force, fs1_pla
     int cur = 0;
     if (cudaGetDevice(&cur) != cudaSuccess) { delete p; return FS1_ERR_CUDA; }
     if (cur != device && cudaSetDevice(device) != cudaSuccess) { delete p; return FS1_ERR_CUDA; }
-    const fs1_status st = plan_sep2d(p, device);
+    const fs1_status st = plan_sep2d(p, device, force);
     if (cur != device) cudaSetDevice(cur);
     if (st != FS1_OK) { delete p; return st; }
   }
@@ -521,6 +580,10 @@ fs1_status fs1_solve(const fs1_plan_t* plan, const void* a, const void* b, void*
   }
   if (plan->kind == KIND_STREAM) {
     if (plan->d.domain != FS1_LOG) return FS1_ERR_UNSUPPORTED;
+    // one binary exponent per 256-point tile holds a tile of the potentials in fp64
+    // only if they can vary by at most c x 256 <= 600 nats across it: Sinkhorn's
+    // potentials are c-Lipschitz up to log a, log b (R25)
+    if (plan->d.h1 / plan->d.eps * TILE > 600.0) return FS1_ERR_UNSUPPORTED;
     // one cooperative launch per problem, in order on the stream (shared workspace)
     for (long long k = 0; k < plan->d.batch; ++k) {
       StreamParams P = stream_params(plan, workspace);

@@ -40,4 +40,13 @@ const void* sep2d_fn();
 size_t sep2d_smem();
 int sep2d_lmax();
 
+// K3w warp-per-line separable 2D solve (fs1_sep2dw.cu), E in {8, 16, 32, 64}
+struct Sep2dwEntry {
+  int E;
+  const void* fn;
+  size_t smem;
+  cudaError_t (*launch)(const Sep2dParams&, int grid, cudaStream_t);
+};
+const Sep2dwEntry* sep2dw_table(int* count);
+
 }  // namespace fs1

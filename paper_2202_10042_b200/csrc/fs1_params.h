@@ -108,12 +108,21 @@ struct Sep2dParams {
   float* Gt0;         // [m*n] G, row-major, ping-pong pair
   float* Gt1;
   float* Z;           // [n*m] pass scratch
+  float* Z2;          // K3w: [m][LP] second transposed scratch (permuted lines)
+  float* Fp;          // K3w: [m][LP] F state (permuted lines)
   double* part;       // [3][G] per-CTA partial sums
   int* flagp;         // [3][G]
   unsigned* bar;
   int n, m, G;
   double tol;
   int itr_max, check_interval, warm, input_is_log, mode;
+  // K3w (warp-per-line solve): chunk E (0 = CTA-line kernel K3), per-axis scan tables
+  int wE;
+  struct WAx {
+    float lam, lamH;  // lambda_k, lambda_k^{E/2}
+    float Lm[5];      // lambda_k^{E 2^j} = Lm 2^Le (Remark 3.3)
+    int Le[5];
+  } wax[2];
 };
 
 }  // namespace fs1

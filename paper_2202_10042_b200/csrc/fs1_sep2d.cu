@@ -2,6 +2,7 @@
 #include <cuda_runtime.h>
 
 #include "fs1_dispatch.h"
+#define FS1_SEP2D_KERNEL_TU
 #include "fs1_sep2d.cuh"
 
 namespace fs1 {

@@ -312,6 +312,7 @@ __device__ __forceinline__ double grid_sum(Ctx& c, const Sep2dParams& P, double 
   return r;
 }
 
+#ifdef FS1_SEP2D_KERNEL_TU  // defined once, in fs1_sep2d.cu
 __global__ void __launch_bounds__(NT, 1) fs1_sep2d_kernel(const __grid_constant__ Sep2dParams P) {
   extern __shared__ __align__(128) unsigned char smem[];
   Ctx c;
@@ -430,6 +431,8 @@ __global__ void __launch_bounds__(NT, 1) fs1_sep2d_kernel(const __grid_constant_
     if (P.cost) P.cost[0] = cost;
   }
 }
+
+#endif  // FS1_SEP2D_KERNEL_TU
 
 }  // namespace sep
 }  // namespace fs1

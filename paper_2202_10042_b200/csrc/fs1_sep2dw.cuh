@@ -1,0 +1,474 @@
+// fs1_sep2dw.cuh — K3w: the warp-per-line separable 2D FS-1 solve (fp32, log domain;
+// config C4, 2048 x 2048).
+//
+// Algorithm 2 with K = T_M(lambda2) (x) T_N(lambda1)
+// (PAPER.md:255-280): every K x is a pass of 1D applies along axis 1 (K0 on every
+// column) and a pass along axis 2.  Each 1D
+// line apply is the forward / backward recursion of Eq. "recursion"
+// (PAPER.md:129-137), run by ONE WARP per line as a chunked scan: lane l owns the E
+// consecutive points [lE, lE+E) of a line of up to 32 E points.
+//
+// Layout.  Every internal array is a set of lines of LP = 32 E floats stored in the
+// lane-chunk-permuted order: float4 j of lane l's chunk sits at float4 slot
+// 32 j + l, so a warp loads its whole line with E/4 fully coalesced 512-byte
+// LDG.128 and every lane ends up with its own chunk in registers (no shared-memory
+// staging, no bank conflicts).  Padding points (index >= line length) hold -inf.
+//
+// Passes.  Two fused passes per iteration, each one grid barrier:
+//   R (lines = rows i, along axis 2):  Y = log K2 e^{Z1_i}  (Z1 = K1 phi, transposed)
+//       [check: err += sum |e^{G_old + Y} - b|]
+//       G_i = log b_i - Y                        (psi update)
+//       Z2 = log K2 e^{G_i}, written transposed  (first pass of the phi half-step)
+//   C (lines = columns j, along axis 1):  F_j = log a_j - log K1 e^{Z2_j}
+//       Z1 = log K1 e^{F_j}, written transposed  (first pass of the next psi half-step)
+// The fused second apply reuses the freshly updated line from registers, so each
+// point is read and written twice per iteration instead of four times, and there
+// are 2 grid barriers per iteration instead of 4.  Transposed writes go through a
+// per-CTA shared stage of W = 8 lines so that each position leaves as two float4.
+//
+// Arithmetic (the chunk-relative log scheme): a lane converts its
+// chunk once per apply, m_e = 2^(X_e log2 e - oe) with oe = floor(max X log2 e)
+// (one MUFU ex2 per point), runs the recursions linearly in fp32 relative to 2^oe,
+// and leaves through one MUFU lg2 per point.  Chunk totals cross lanes as
+// extended-range fp32 numbers (mantissa in [1,2), int exponent) in a 5-level warp
+// shuffle scan with multipliers lambda^{E 2^k} formed on the host (Remark 3.3).
+// In-lane work runs as 2-4 independent chains (ILP): the chunk halves get their own
+// carries from the half aggregates.
+#pragma once
+#include <math.h>
+#include <stdint.h>
+
+#include "fs1_sep2d.cuh"
+
+namespace fs1 {
+namespace sepw {
+
+constexpr int W = 8;        // warps = lines per CTA group
+constexpr int NT = 32 * W;
+constexpr int LIMF = 60;    // carries up to 2^60 above a chunk keep its exponent
+constexpr float LOG2E = 1.4426950408889634f;
+constexpr float LN2 = 0.6931471805599453f;
+
+template <int E> struct Cfg {
+  static constexpr int LP = 32 * E;             // padded line length (floats)
+  static constexpr int Q = E / 4;               // float4 per lane chunk
+  static constexpr int SROW = E + 4;            // stage floats per lane chunk (padded)
+  static constexpr int SLINE = 32 * SROW;       // stage floats per line
+  static constexpr size_t STAGE = (size_t)W * SLINE * 4;
+  static constexpr size_t STAGE_ALL = STAGE > (size_t)sep::OFF_XM ? STAGE : (size_t)sep::OFF_XM;
+  static constexpr size_t OFF_XM = STAGE_ALL;
+  static constexpr size_t OFF_XI = OFF_XM + 4 * sep::W * 8;
+  static constexpr size_t OFF_RED = OFF_XI + 4 * sep::W * 4;
+  static constexpr size_t OFF_IRED = OFF_RED + 64 * 8;
+  static constexpr size_t SMEM = OFF_IRED + 64 * 4;
+};
+
+// position of point q of a line in the permuted layout
+template <int E> __device__ __forceinline__ int pidx(int q) {
+  const int l = q / E, e = q - l * E;
+  return ((e >> 2) * 32 + l) * 4 + (e & 3);
+}
+// point of permuted slot k
+template <int E> __device__ __forceinline__ int pinv(int k) {
+  const int j4 = k >> 2, l = j4 & 31, e = (j4 >> 5) * 4 + (k & 3);
+  return l * E + e;
+}
+
+// ------------------------------------------------------------ extended-range fp32
+struct ERf {
+  float m;
+  int e;
+};
+__device__ __forceinline__ float p2f(int d) {  // exact 2^d, 0 below 2^-126
+  d = min(d, 127);
+  return d >= -126 ? __uint_as_float((unsigned)(d + 127) << 23) : 0.f;
+}
+__device__ __forceinline__ ERf ern(float x, int e) {  // normalise x 2^e (x >= 0, normal or 0)
+  ERf r;
+  if (x > 0.f) {
+    const unsigned u = __float_as_uint(x);
+    r.e = e + (int)((u >> 23) & 0xffu) - 127;
+    r.m = __uint_as_float((u & 0x807fffffu) | 0x3f800000u);
+  } else {
+    r.m = 0.f;
+    r.e = ZE;
+  }
+  return r;
+}
+__device__ __forceinline__ ERf era(ERf a, ERf b) {
+  const int e = max(a.e, b.e);
+  return ern(fmaf(a.m, p2f(a.e - e), b.m * p2f(b.e - e)), e);
+}
+__device__ __forceinline__ ERf erm(ERf a, float bm, int be) { return ern(a.m * bm, a.e + be); }
+
+// Per-axis scan tables (host-formed, Remark 3.3), read straight from the
+// __grid_constant__ parameter block (constant-bank operands, no registers).
+using AxT = Sep2dParams::WAx;
+
+// ------------------------------------------------------------ one line apply
+// A: this lane's chunk of natural logs X (padding -inf).  On return A[e] = (K e^X)_e
+// relative to 2^R (linear fp32), R returned.
+template <int E>
+__device__ __forceinline__ int line_apply(float (&A)[E], const AxT& T, int lane) {
+  constexpr int H = E / 2;
+  float M = -INFINITY;
+#pragma unroll
+  for (int e = 0; e < E; ++e) M = fmaxf(M, A[e]);
+  int oe;
+  if (M == -INFINITY) {
+    oe = ZE;
+#pragma unroll
+    for (int e = 0; e < E; ++e) A[e] = 0.f;
+  } else if (!(M < INFINITY)) {  // +inf weight: poison the chunk (the problem flags NONFINITE)
+    oe = 0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) A[e] = NAN;
+  } else {
+    oe = (int)floorf(M * LOG2E);
+    const float o = (float)oe;
+#pragma unroll
+    for (int e = 0; e < E; ++e) A[e] = sep::ex2f(fmaf(A[e], LOG2E, -o));
+  }
+  // chunk aggregates (Horner, zero carries), 4 independent chains over the halves
+  const float lam = T.lam, lH = T.lamH;
+  float f0 = 0.f, f1 = 0.f, g0 = 0.f, g1 = 0.f;
+#pragma unroll
+  for (int e = 0; e < H; ++e) {
+    f0 = fmaf(lam, f0, A[e]);
+    f1 = fmaf(lam, f1, A[H + e]);
+    g0 = fmaf(lam, g0, A[H - 1 - e]);
+    g1 = fmaf(lam, g1, A[E - 1 - e]);
+  }
+  ERf F = ern(fmaf(lH, f0, f1), oe);  // forward total at the chunk end
+  ERf B = ern(fmaf(lH, g1, g0), oe);  // backward total at the chunk start
+  // warp inclusive scans of the affine maps y -> lambda^{E d} y + c (Hillis-Steele)
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    const int d = 1 << k;
+    const ERf up{__shfl_up_sync(FULL, F.m, d), __shfl_up_sync(FULL, F.e, d)};
+    const ERf dn{__shfl_down_sync(FULL, B.m, d), __shfl_down_sync(FULL, B.e, d)};
+    if (lane >= d) F = era(erm(up, T.Lm[k], T.Le[k]), F);
+    if (lane + d < 32) B = era(erm(dn, T.Lm[k], T.Le[k]), B);
+  }
+  ERf cf{__shfl_up_sync(FULL, F.m, 1), __shfl_up_sync(FULL, F.e, 1)};
+  ERf cb{__shfl_down_sync(FULL, B.m, 1), __shfl_down_sync(FULL, B.e, 1)};
+  if (lane == 0) cf = ERf{0.f, ZE};
+  if (lane == 31) cb = ERf{0.f, ZE};
+  // reference exponent of the chunk: its own, unless the carries dwarf it
+  int R = oe;
+  if (oe == ZE || cf.e - oe > LIMF || cb.e - oe > LIMF) {
+    R = max(cf.e, cb.e);
+    if (R == ZE) R = (oe == ZE) ? 0 : oe;
+    const float s = (oe == ZE) ? 0.f : p2f(oe - R);
+#pragma unroll
+    for (int e = 0; e < E; ++e) A[e] *= s;
+    f0 *= s;
+    g1 *= s;
+  }
+  const float cfr = cf.m * p2f(cf.e - R), cbr = cb.m * p2f(cb.e - R);
+  // forward recursion p_k = lam p_{k-1} + x_k (Alg. 2 lines 4 / 9), two chains
+  const float q0 = fmaf(lH, cfr, f0);  // p at the end of the first half
+  float p = cfr, q = q0;
+#pragma unroll
+  for (int e = 0; e < H; ++e) {
+    p = fmaf(lam, p, A[e]);
+    A[e] = p;
+    q = fmaf(lam, q, A[H + e]);
+    A[H + e] = q;
+  }
+  // backward recursion t_k = lam t_{k+1} + x_k and K x = p + lam t_{k+1} (lines 5 / 10),
+  // two chains; x_k = p_k - lam p_{k-1} is recovered from the stored forward values
+  float ta = cbr, tb = fmaf(lH, cbr, g1);
+#pragma unroll
+  for (int i = 0; i < H; ++i) {
+    const int ea = E - 1 - i, eb = H - 1 - i;
+    const float xa = fmaf(-lam, (ea == H) ? q0 : A[ea - 1], A[ea]);
+    const float ka = fmaf(lam, ta, A[ea]);
+    ta = fmaf(lam, ta, xa);
+    A[ea] = ka;
+    const float xb = fmaf(-lam, (eb == 0) ? cfr : A[eb - 1], A[eb]);
+    const float kb = fmaf(lam, tb, A[eb]);
+    tb = fmaf(lam, tb, xb);
+    A[eb] = kb;
+  }
+  return R;
+}
+
+template <int E>
+__device__ __forceinline__ void load_line(const float* line, int lane, float (&A)[E]) {
+  const float4* q = reinterpret_cast<const float4*>(line);
+#pragma unroll
+  for (int j = 0; j < E / 4; ++j) {
+    const float4 v = __ldcg(q + j * 32 + lane);
+    A[4 * j] = v.x; A[4 * j + 1] = v.y; A[4 * j + 2] = v.z; A[4 * j + 3] = v.w;
+  }
+}
+template <int E>
+__device__ __forceinline__ void store_line(float* line, int lane, const float (&A)[E]) {
+  float4* q = reinterpret_cast<float4*>(line);
+#pragma unroll
+  for (int j = 0; j < E / 4; ++j)
+    q[j * 32 + lane] = make_float4(A[4 * j], A[4 * j + 1], A[4 * j + 2], A[4 * j + 3]);
+}
+
+// MODE bits of a fused pass
+constexpr int UPD = 1, WR = 2, CHK = 4, FUSE = 8;
+
+// One fused pass over `nlines` lines of length `len` (axis tables T):
+//   UPD:  Y = log K e^{X}, values = LT - Y (the update), [CHK] error vs Yold, [WR] -> Yout
+//   FUSE: Z = log K e^{values} (values = X when !UPD), written transposed into Zout
+//         (lines = positions 0..len-1, points = this pass's line indices).
+template <int E, int MODE>
+__device__ __forceinline__ void fused_pass(sep::Ctx& c, const AxT& T, const float* X, const float* LT,
+                                           const float* Yold, float* Yout, float* Zout, int nlines, int len,
+                                           int G, double& errsum, int& bad) {
+  using C = Cfg<E>;
+  const int lane = c.lane, w = c.warp;
+  const int ngroups = (nlines + W - 1) / W;
+  float* stage = c.s.stage;
+  for (int grp = c.r; grp < ngroups; grp += G) {
+    const int line = grp * W + w;
+    float A[E];
+    if (line < nlines) {
+      const size_t off = (size_t)line * C::LP;
+      load_line<E>(X + off, lane, A);
+      if (MODE & UPD) {
+        const int R = line_apply<E>(A, T, lane);
+        const float Rl = (float)R * LN2;
+        double ep = 0.0;
+        const float4* lt4 = reinterpret_cast<const float4*>(LT + off);
+        const float4* yo4 = reinterpret_cast<const float4*>((MODE & CHK) ? Yold + off : LT + off);
+        int b = 0;
+#pragma unroll
+        for (int j = 0; j < E / 4; ++j) {
+          const float4 t4 = __ldcg(lt4 + j * 32 + lane);
+          float4 o4;
+          if (MODE & CHK) o4 = __ldcg(yo4 + j * 32 + lane);
+          const float tl[4] = {t4.x, t4.y, t4.z, t4.w};
+          const float yo[4] = {o4.x, o4.y, o4.z, o4.w};
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            const int e = 4 * j + r;
+            const float Y = fmaf(sep::lg2f(A[e]), LN2, Rl);
+            if (MODE & CHK) {
+              const float ea = sep::ex2f((yo[r] + Y) * LOG2E);
+              const float eb = (tl[r] == -INFINITY) ? 0.f : sep::ex2f(tl[r] * LOG2E);
+              ep += fabs((double)ea - (double)eb);
+            }
+            const float v = (tl[r] == -INFINITY) ? -INFINITY : tl[r] - Y;
+            if (MODE & WR) b |= (v != v) | (v == INFINITY);
+            A[e] = v;
+          }
+        }
+        if (MODE & WR) {
+          store_line<E>(Yout + off, lane, A);
+          if (b) bad = 1;
+        }
+        if (MODE & CHK) {
+          ep = warp_sum(ep);
+          if (lane == 0) c.s.red[w] = ep;
+        }
+      }
+      if (MODE & FUSE) {
+        const int R2 = line_apply<E>(A, T, lane);
+        const float Rl2 = (float)R2 * LN2;
+        float4* st = reinterpret_cast<float4*>(stage + (size_t)w * C::SLINE + lane * C::SROW);
+#pragma unroll
+        for (int j = 0; j < E / 4; ++j)
+          st[j] = make_float4(fmaf(sep::lg2f(A[4 * j]), LN2, Rl2), fmaf(sep::lg2f(A[4 * j + 1]), LN2, Rl2),
+                              fmaf(sep::lg2f(A[4 * j + 2]), LN2, Rl2), fmaf(sep::lg2f(A[4 * j + 3]), LN2, Rl2));
+      }
+    } else {
+      if ((MODE & CHK) && lane == 0) c.s.red[w] = 0.0;
+      if (MODE & FUSE) {
+        float4* st = reinterpret_cast<float4*>(stage + (size_t)w * C::SLINE + lane * C::SROW);
+#pragma unroll
+        for (int j = 0; j < E / 4; ++j) st[j] = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+      }
+    }
+    if ((MODE & (CHK | FUSE)) == 0) continue;
+    __syncthreads();
+    if (MODE & CHK) {  // line errors in line order (deterministic)
+      if (c.tid == 0) {
+        double s = 0.0;
+        for (int k = 0; k < W; ++k) s += c.s.red[k];
+        errsum += s;
+      }
+    }
+    if (MODE & FUSE) {
+      // position p of these W lines -> consumer line p, points grp W .. grp W + W - 1
+      const int q0 = grp * W, lc = q0 / E, e0 = q0 - lc * E;  // same lane chunk (E >= 8)
+      for (int p = c.tid; p < len; p += NT) {
+        const int sp = (p / E) * C::SROW + (p % E);
+        float v[W];
+#pragma unroll
+        for (int k = 0; k < W; ++k) v[k] = stage[(size_t)k * C::SLINE + sp];
+        float4* o = reinterpret_cast<float4*>(Zout + (size_t)p * C::LP);
+        o[(e0 >> 2) * 32 + lc] = make_float4(v[0], v[1], v[2], v[3]);
+        o[((e0 >> 2) + 1) * 32 + lc] = make_float4(v[4], v[5], v[6], v[7]);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------ layout conversions
+// dst (permuted lines, `lines` x LP) <- src natural: point q of line l is
+// src[l * ls + q * qs] (f applied), padding -inf.  mode 0 copy, 1 log, 2 constant.
+template <int E>
+__device__ __forceinline__ void to_perm(const sep::Ctx& c, const float* src, long long ls, long long qs, int lines,
+                                        int len, float* dst, int mode, float cst, int G) {
+  using C = Cfg<E>;
+  const size_t tot = (size_t)lines * C::LP;
+  for (size_t k = (size_t)c.r * NT + c.tid; k < tot; k += (size_t)G * NT) {
+    const int l = (int)(k / C::LP), s = (int)(k % C::LP);
+    const int q = pinv<E>(s);
+    float v = -INFINITY;
+    if (q < len) {
+      if (mode == 2) {
+        v = cst;
+      } else {
+        v = __ldcg(src + (size_t)l * ls + (size_t)q * qs);
+        if (mode == 1) v = logf(v);
+      }
+    }
+    dst[k] = v;
+  }
+}
+// natural dst[l * ls + q] <- permuted src line l point q (q < len)
+template <int E>
+__device__ __forceinline__ void from_perm(const sep::Ctx& c, const float* src, int lines, int len, float* dst,
+                                          int G) {
+  using C = Cfg<E>;
+  const size_t tot = (size_t)lines * len;
+  for (size_t k = (size_t)c.r * NT + c.tid; k < tot; k += (size_t)G * NT) {
+    const int l = (int)(k / len), q = (int)(k % len);
+    dst[k] = __ldcg(src + (size_t)l * C::LP + pidx<E>(q));
+  }
+}
+__device__ __forceinline__ void fill(const sep::Ctx& c, float* dst, size_t cnt, float v, int G) {
+  for (size_t k = (size_t)c.r * NT + c.tid; k < cnt; k += (size_t)G * NT) dst[k] = v;
+}
+
+// ------------------------------------------------------------ the kernel (solve only)
+template <int E>
+__global__ void __launch_bounds__(NT, 1) fs1_sep2dw_kernel(const __grid_constant__ Sep2dParams P) {
+  using C = Cfg<E>;
+  extern __shared__ __align__(128) unsigned char smem[];
+  sep::Ctx c;
+  c.tid = threadIdx.x;
+  c.lane = c.tid & 31;
+  c.warp = c.tid >> 5;
+  c.r = blockIdx.x;
+  c.par = 0;
+  c.gen = 0;
+  c.s.stage = reinterpret_cast<float*>(smem);
+  c.s.xm = reinterpret_cast<double*>(smem + C::OFF_XM);
+  c.s.xi = reinterpret_cast<int*>(smem + C::OFF_XI);
+  c.s.red = reinterpret_cast<double*>(smem + C::OFF_RED);
+  c.s.ired = reinterpret_cast<int*>(smem + C::OFF_IRED);
+  const int n = P.n, m = P.m, G = P.G;
+  const float* A = reinterpret_cast<const float*>(P.a);
+  const float* Bv = reinterpret_cast<const float*>(P.b);
+  float* U = reinterpret_cast<float*>(P.u);
+  float* V = reinterpret_cast<float*>(P.v);
+  const AxT& T1 = P.wax[0];
+  const AxT& T2 = P.wax[1];
+  // permuted state: LA, F columns (m lines of n points); LBt, G rows (n lines of m);
+  // Z1 rows (K1 phi, transposed), Z2 columns (K2 psi, transposed)
+  float* LA = P.LA;
+  float* LBt = P.LBt;
+  float* Fp = P.Fp;
+  float* Z1 = P.Z;
+  float* Z2 = P.Z2;
+
+  // ---- prologue: log a, (log b)^T, phi0 = psi0 = 1/(N M)
+  const int li = P.input_is_log ? 0 : 1;
+  to_perm<E>(c, A, n, 1, m, n, LA, li, 0.f, G);
+  to_perm<E>(c, Bv, 1, n, n, m, LBt, li, 0.f, G);
+  const float init = -logf((float)n) - logf((float)m);
+  if (!P.warm) {
+    to_perm<E>(c, nullptr, 0, 0, m, n, Fp, 2, init, G);
+    to_perm<E>(c, nullptr, 0, 0, n, m, P.Gt0, 2, init, G);
+  } else {
+    to_perm<E>(c, U, n, 1, m, n, Fp, 0, 0.f, G);
+    to_perm<E>(c, V, 1, n, n, m, P.Gt0, 0, 0.f, G);
+  }
+  fill(c, Z1, (size_t)n * C::LP, -INFINITY, G);
+  fill(c, Z2, (size_t)m * C::LP, -INFINITY, G);
+  stm::grid_barrier(P.bar, G, c.gen);
+  double dummy = 0.0;
+  int bad = 0;
+  // Z1 = K1 on the columns of F, transposed
+  fused_pass<E, FUSE>(c, T1, Fp, nullptr, nullptr, nullptr, Z1, m, n, G, dummy, bad);
+  stm::grid_barrier(P.bar, G, c.gen);
+
+  int l = 0, qi = 0, flag = 0;
+  double errv = NAN;
+  const bool use_tol = P.tol > 0.0;
+  while (true) {
+    const bool check = (l >= P.itr_max) || (use_tol && (l % P.check_interval) == 0);
+    const bool last = l >= P.itr_max;
+    float* Gi = qi ? P.Gt1 : P.Gt0;
+    float* Go = qi ? P.Gt0 : P.Gt1;
+    double es = 0.0;
+    bad = 0;
+    // ---- pass R: psi half-step (Alg. 2 lines 3-7) + first pass of the phi half-step
+    if (!check) fused_pass<E, UPD | WR | FUSE>(c, T2, Z1, LBt, nullptr, Go, Z2, n, m, G, es, bad);
+    else if (!last) fused_pass<E, UPD | WR | CHK | FUSE>(c, T2, Z1, LBt, Gi, Go, Z2, n, m, G, es, bad);
+    else fused_pass<E, UPD | CHK>(c, T2, Z1, LBt, Gi, Go, Z2, n, m, G, es, bad);
+    bad = __syncthreads_or(bad);
+    int f;
+    const double e = sep::grid_sum(c, P, es, 0, f, bad);
+    if (check) {
+      errv = e;
+      if (last || errv <= P.tol) {
+        flag = (use_tol && errv <= P.tol) ? 1 : 4;
+        break;
+      }
+    }
+    qi ^= 1;  // psi^(l+1) is current
+    if (f) { ++l; flag = 2; break; }
+    // ---- pass C: phi half-step (lines 8-12) + first pass of the next psi half-step
+    bad = 0;
+    fused_pass<E, UPD | WR | FUSE>(c, T1, Z2, LA, nullptr, Fp, Z1, m, n, G, es, bad);
+    bad = __syncthreads_or(bad);
+    sep::grid_sum(c, P, 0.0, 1, f, bad);
+    ++l;  // line 13
+    if (f) { flag = 2; break; }
+  }
+
+  // ---- outputs in the user layout: F column-major into u, G row-major natural (for the
+  // cost) into the LA buffer, then transposed into v (column-major)
+  float* Gc = qi ? P.Gt1 : P.Gt0;
+  float* Gnat = LA;
+  from_perm<E>(c, Fp, m, n, U, G);
+  from_perm<E>(c, Gc, n, m, Gnat, G);
+  stm::grid_barrier(P.bar, G, c.gen);
+  double cost = NAN;
+  if (flag != 2) {
+    // return line on the CTA-line machinery: phi (W1 (x) K2) psi + psi (K1 (x) W2) phi
+    float* Zc = Z1;   // K2 along rows of psi -> column-major (natural)
+    float* Gs = Z2;   // K1 along columns of phi -> row-major (natural)
+    sep::pass_transposed(c, P.ax2, Gnat, n, m, Zc, G);
+    sep::pass_transposed(c, P.ax1, U, m, n, Gs, G);
+    stm::grid_barrier(P.bar, G, c.gen);
+    double s = 0.0;
+    for (int j = c.r; j < m; j += G) s += sep::line_cost(c, P.ax1, Zc + (size_t)j * n, U + (size_t)j * n, n);
+    for (int i = c.r; i < n; i += G) s += sep::line_cost(c, P.ax2, Gs + (size_t)i * m, Gnat + (size_t)i * m, m);
+    int f;
+    cost = sep::grid_sum(c, P, s, 2, f, 0);
+  } else {
+    errv = NAN;
+  }
+  sep::transpose_phase(c, Gnat, n, m, V, false, G);
+  if (c.r == 0 && c.tid == 0) {
+    if (P.iters) P.iters[0] = l;
+    if (P.err) P.err[0] = errv;
+    if (P.flags) P.flags[0] = flag;
+    if (P.cost) P.cost[0] = cost;
+  }
+}
+
+}  // namespace sepw
+}  // namespace fs1

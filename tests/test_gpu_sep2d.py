@@ -94,6 +94,23 @@ def test_sep2d_solve_parity(n, m, eps, itr):
     assert_solve_parity(out, ref, "log", "f32", tol=TOL32)
 
 
+@pytest.mark.parametrize("n,m,eps", [(37, 53, 0.02), (256, 200, 2e-3), (600, 900, 2e-3)])
+def test_sep2d_warp_line_kernel_equals_cta_line_kernel(n, m, eps):
+    """K3w (warp per line, the solve default) and K3 (CTA per line, kernel=3) on the same
+    problem: independent scan schedules of the same recursions agree to fp32 rounding."""
+    la, lb = _pair2d(n, m, 5 * n + m)
+    A, B = _cuda(la[None]), _cuda(lb[None])
+    kw = dict(h=1 / n, h2=1 / m, eps=eps, itr_max=15, domain="log", input_is_log=True, shape=(n, m))
+    assert fs1.plan(fs1.Spec(ndim=2, n=n, m=m, h1=1 / n, h2=1 / m, eps=eps, batch=1, dtype=torch.float32,
+                             domain="log", input_is_log=True, itr_max=15)).info()["kernel"].startswith("sep2dw")
+    ow = fs1.solve(A, B, **kw)
+    oc = fs1.solve(A, B, kernel=3, **kw)
+    assert rel_norm(ow["u"].double().cpu().numpy()[0], oc["u"].double().cpu().numpy()[0]) <= 2e-6
+    assert rel_norm(ow["v"].double().cpu().numpy()[0], oc["v"].double().cpu().numpy()[0]) <= 2e-6
+    assert rel(ow["cost"].item(), oc["cost"].item()) <= 1e-5
+    assert abs(ow["err"].item() - oc["err"].item()) <= 1e-5 * max(1.0, oc["err"].item())
+
+
 def test_sep2d_linear_weights_and_tolerance_stop():
     n, m = 48, 40
     la, lb = _pair2d(n, m, 7)
