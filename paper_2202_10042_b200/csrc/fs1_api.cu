@@ -544,6 +544,14 @@ fs1_status fs1__set_stream_timers(fs1_plan_t* plan, unsigned long long* buf) {
   return FS1_OK;
 }
 
+// test-only: phase timestamps of the 2D warp-line kernel at iteration 5, pass R:
+// buf = [grid][8 warps][2 groups][8] u64 + [grid] barrier exits.
+fs1_status fs1__set_sep_timers(fs1_plan_t* plan, unsigned long long* buf) {
+  if (!plan) return FS1_ERR_ARG;
+  plan->tbase.tdbg = buf;
+  return FS1_OK;
+}
+
 fs1_status fs1_plan_info(const fs1_plan_t* plan, fs1_plan_info_t* info) {
   if (!plan || !info) return FS1_ERR_ARG;
   *info = plan->info;

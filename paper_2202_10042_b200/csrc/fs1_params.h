@@ -118,6 +118,7 @@ struct Sep2dParams {
   int itr_max, check_interval, warm, input_is_log, mode;
   // K3w (warp-per-line solve): chunk E (0 = CTA-line kernel K3), per-axis scan tables
   int wE;
+  unsigned long long* tdbg;  // optional phase timestamps (test-only): [G][W][2 groups][8]
   struct WAx {
     float lam, lamH;  // lambda_k, lambda_k^{E/2}
     float Lm[5];      // lambda_k^{E 2^j} = Lm 2^Le (Remark 3.3)

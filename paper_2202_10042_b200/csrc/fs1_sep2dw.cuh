@@ -9,10 +9,12 @@
 // consecutive points [lE, lE+E) of a line of up to 32 E points.
 //
 // Layout.  Every internal array is a set of lines of LP = 32 E floats stored in the
-// lane-chunk-permuted order: float4 j of lane l's chunk sits at float4 slot
-// 32 j + l, so a warp loads its whole line with E/4 fully coalesced 512-byte
-// LDG.128 and every lane ends up with its own chunk in registers (no shared-memory
-// staging, no bank conflicts).  Padding points (index >= line length) hold -inf.
+// lane-chunk-permuted order: the 8-float run j of lane l's chunk sits at run slot
+// 32 j + l, so a warp loads its whole line with E/8 fully coalesced 1 KiB
+// 256-bit loads and every lane ends up with its own chunk in registers (no
+// shared-memory staging), and the 8 lines of a group land as one 32-byte sector
+// per position in the transposed write.  Padding points (index >= line length)
+// hold -inf.
 //
 // Passes.  Two fused passes per iteration, each one grid barrier:
 //   R (lines = rows i, along axis 2):  Y = log K2 e^{Z1_i}  (Z1 = K1 phi, transposed)
@@ -24,7 +26,7 @@
 // The fused second apply reuses the freshly updated line from registers, so each
 // point is read and written twice per iteration instead of four times, and there
 // are 2 grid barriers per iteration instead of 4.  Transposed writes go through a
-// per-CTA shared stage of W = 8 lines so that each position leaves as two float4.
+// per-CTA shared stage of W = 8 lines so that each position leaves as one sector.
 //
 // Arithmetic (the chunk-relative log scheme): a lane converts its
 // chunk once per apply, m_e = 2^(X_e log2 e - oe) with oe = floor(max X log2 e)
@@ -53,25 +55,40 @@ template <int E> struct Cfg {
   static constexpr int LP = 32 * E;             // padded line length (floats)
   static constexpr int Q = E / 4;               // float4 per lane chunk
   static constexpr int SROW = E + 4;            // stage floats per lane chunk (padded)
-  static constexpr int SLINE = 32 * SROW;       // stage floats per line
+  static constexpr int SLINE = 32 * SROW;       // stage floats per line (>= LP)
   static constexpr size_t STAGE = (size_t)W * SLINE * 4;
   static constexpr size_t STAGE_ALL = STAGE > (size_t)sep::OFF_XM ? STAGE : (size_t)sep::OFF_XM;
-  static constexpr size_t OFF_XM = STAGE_ALL;
+  static constexpr size_t LINEB = (size_t)LP * 4;
+  static constexpr size_t OFF_MBAR = STAGE_ALL;                // [W][2] mbarriers
+  static constexpr size_t OFF_XM = OFF_MBAR + W * 2 * 8;
   static constexpr size_t OFF_XI = OFF_XM + 4 * sep::W * 8;
   static constexpr size_t OFF_RED = OFF_XI + 4 * sep::W * 4;
   static constexpr size_t OFF_IRED = OFF_RED + 64 * 8;
   static constexpr size_t SMEM = OFF_IRED + 64 * 4;
 };
 
-// position of point q of a line in the permuted layout
+// position of point q of a line in the permuted layout: 8-float run j of lane l's chunk
+// sits at run slot 32 j + l (one 32-byte sector)
 template <int E> __device__ __forceinline__ int pidx(int q) {
   const int l = q / E, e = q - l * E;
-  return ((e >> 2) * 32 + l) * 4 + (e & 3);
+  return ((e >> 3) * 32 + l) * 8 + (e & 7);
 }
 // point of permuted slot k
 template <int E> __device__ __forceinline__ int pinv(int k) {
-  const int j4 = k >> 2, l = j4 & 31, e = (j4 >> 5) * 4 + (k & 3);
+  const int j8 = k >> 3, l = j8 & 31, e = (j8 >> 5) * 8 + (k & 7);
   return l * E + e;
+}
+
+// 256-bit global accesses (LDG/STG.E.ENL2.256): one full sector per lane
+__device__ __forceinline__ void ldg8(const float* p, float* v) {
+  asm volatile("ld.global.cg.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+               : "l"(p));
+}
+__device__ __forceinline__ void stg8(float* p, const float* v) {
+  asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(v[0]), "f"(v[1]), "f"(v[2]),
+               "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
+               : "memory");
 }
 
 // ------------------------------------------------------------ extended-range fp32
@@ -196,59 +213,76 @@ __device__ __forceinline__ int line_apply(float (&A)[E], const AxT& T, int lane)
 
 template <int E>
 __device__ __forceinline__ void load_line(const float* line, int lane, float (&A)[E]) {
-  const float4* q = reinterpret_cast<const float4*>(line);
 #pragma unroll
-  for (int j = 0; j < E / 4; ++j) {
-    const float4 v = __ldcg(q + j * 32 + lane);
-    A[4 * j] = v.x; A[4 * j + 1] = v.y; A[4 * j + 2] = v.z; A[4 * j + 3] = v.w;
-  }
+  for (int j = 0; j < E / 8; ++j) ldg8(line + (j * 32 + lane) * 8, &A[8 * j]);
 }
 template <int E>
 __device__ __forceinline__ void store_line(float* line, int lane, const float (&A)[E]) {
-  float4* q = reinterpret_cast<float4*>(line);
 #pragma unroll
-  for (int j = 0; j < E / 4; ++j)
-    q[j * 32 + lane] = make_float4(A[4 * j], A[4 * j + 1], A[4 * j + 2], A[4 * j + 3]);
+  for (int j = 0; j < E / 8; ++j) stg8(line + (j * 32 + lane) * 8, &A[8 * j]);
 }
 
 // MODE bits of a fused pass
 constexpr int UPD = 1, WR = 2, CHK = 4, FUSE = 8;
 
+// Per-warp TMA state: X line and target (+ G_old) line buffers with one mbarrier each.
+struct WarpIO {
+  float* ts;       // target line: aliases this warp's stage region (free until the FUSE output)
+  uint64_t* mb;    // [2]: (unused), target
+  unsigned ph0, ph1;  // parity of the next wait on mb[0] / mb[1]
+};
+
 // One fused pass over `nlines` lines of length `len` (axis tables T):
 //   UPD:  Y = log K e^{X}, values = LT - Y (the update), [CHK] error vs Yold, [WR] -> Yout
 //   FUSE: Z = log K e^{values} (values = X when !UPD), written transposed into Zout
 //         (lines = positions 0..len-1, points = this pass's line indices).
+// Inputs arrive by 1D TMA bulk copies (cp.async.bulk, mbarrier complete_tx) issued by
+// lane 0 when the warp takes the line: the target line lands while the first apply
+// runs, so the update reads it from shared memory without a global-latency stall.
 template <int E, int MODE>
-__device__ __forceinline__ void fused_pass(sep::Ctx& c, const AxT& T, const float* X, const float* LT,
-                                           const float* Yold, float* Yout, float* Zout, int nlines, int len,
-                                           int G, double& errsum, int& bad) {
+__device__ __forceinline__ void fused_pass(sep::Ctx& c, WarpIO& io, const AxT& T, const float* X,
+                                           const float* LT, const float* Yold, float* Yout, float* Zout,
+                                           int nlines, int len, int G, double& errsum, int& bad,
+                                           unsigned long long* td = nullptr) {
   using C = Cfg<E>;
   const int lane = c.lane, w = c.warp;
   const int ngroups = (nlines + W - 1) / W;
   float* stage = c.s.stage;
-  for (int grp = c.r; grp < ngroups; grp += G) {
+  int gi = 0;
+  for (int grp = c.r; grp < ngroups; grp += G, ++gi) {
+    unsigned long long* t = (td && lane == 0 && gi < 2) ? td + (((size_t)c.r * W + w) * 2 + gi) * 8 : nullptr;
+    if (t) t[0] = stm::gtimer();
     const int line = grp * W + w;
     float A[E];
     if (line < nlines) {
       const size_t off = (size_t)line * C::LP;
-      load_line<E>(X + off, lane, A);
+      if ((MODE & UPD) && lane == 0) {
+        stm::fence_async_smem();
+        stm::mbar_expect_tx(&io.mb[1], (unsigned)C::LINEB);
+        stm::bulk_g2s(io.ts, LT + off, (unsigned)C::LINEB, &io.mb[1]);
+      }
+      load_line<E>(X + off, lane, A);  // E/4 coalesced LDG.128, all in flight at once
+      if (t) t[1] = stm::gtimer() + (A[0] == 12345.f);
       if (MODE & UPD) {
         const int R = line_apply<E>(A, T, lane);
+        if (t) t[2] = stm::gtimer() + (R == 12345);
         const float Rl = (float)R * LN2;
         double ep = 0.0;
-        const float4* lt4 = reinterpret_cast<const float4*>(LT + off);
-        const float4* yo4 = reinterpret_cast<const float4*>((MODE & CHK) ? Yold + off : LT + off);
+        stm::mbar_wait(&io.mb[1], io.ph1);
+        io.ph1 ^= 1u;
+        if (t) t[3] = stm::gtimer();
+        const float4* lt4 = reinterpret_cast<const float4*>(io.ts);
         int b = 0;
 #pragma unroll
-        for (int j = 0; j < E / 4; ++j) {
-          const float4 t4 = __ldcg(lt4 + j * 32 + lane);
-          float4 o4;
-          if (MODE & CHK) o4 = __ldcg(yo4 + j * 32 + lane);
-          const float tl[4] = {t4.x, t4.y, t4.z, t4.w};
-          const float yo[4] = {o4.x, o4.y, o4.z, o4.w};
+        for (int j = 0; j < E / 8; ++j) {
+          if ((j & 1) == 0) __syncwarp();  // bounds the hoisting of the shared loads (registers)
+          const float4 t0 = lt4[(j * 32 + lane) * 2], t1 = lt4[(j * 32 + lane) * 2 + 1];
+          float yo[8];
+          if (MODE & CHK) ldg8(Yold + off + (j * 32 + lane) * 8, yo);  // check passes only
+          const float tl[8] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w};
 #pragma unroll
-          for (int r = 0; r < 4; ++r) {
-            const int e = 4 * j + r;
+          for (int r = 0; r < 8; ++r) {
+            const int e = 8 * j + r;
             const float Y = fmaf(sep::lg2f(A[e]), LN2, Rl);
             if (MODE & CHK) {
               const float ea = sep::ex2f((yo[r] + Y) * LOG2E);
@@ -256,22 +290,23 @@ __device__ __forceinline__ void fused_pass(sep::Ctx& c, const AxT& T, const floa
               ep += fabs((double)ea - (double)eb);
             }
             const float v = (tl[r] == -INFINITY) ? -INFINITY : tl[r] - Y;
-            if (MODE & WR) b |= (v != v) | (v == INFINITY);
+            b |= (v != v) | (v == INFINITY);
             A[e] = v;
           }
         }
-        if (MODE & WR) {
-          store_line<E>(Yout + off, lane, A);
-          if (b) bad = 1;
-        }
+        if (MODE & WR) store_line<E>(Yout + off, lane, A);
+        if (b) bad = 1;
         if (MODE & CHK) {
           ep = warp_sum(ep);
           if (lane == 0) c.s.red[w] = ep;
         }
       }
+      if (t) t[4] = stm::gtimer() + (A[1] == 12345.f);
       if (MODE & FUSE) {
         const int R2 = line_apply<E>(A, T, lane);
+        if (t) t[5] = stm::gtimer() + (R2 == 12345);
         const float Rl2 = (float)R2 * LN2;
+        __syncwarp();  // every lane has read its target chunk (the stage aliases it)
         float4* st = reinterpret_cast<float4*>(stage + (size_t)w * C::SLINE + lane * C::SROW);
 #pragma unroll
         for (int j = 0; j < E / 4; ++j)
@@ -286,8 +321,12 @@ __device__ __forceinline__ void fused_pass(sep::Ctx& c, const AxT& T, const floa
         for (int j = 0; j < E / 4; ++j) st[j] = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
       }
     }
-    if ((MODE & (CHK | FUSE)) == 0) continue;
+    if ((MODE & (CHK | FUSE)) == 0) {
+      __syncwarp();
+      continue;
+    }
     __syncthreads();
+    if (t) t[6] = stm::gtimer();
     if (MODE & CHK) {  // line errors in line order (deterministic)
       if (c.tid == 0) {
         double s = 0.0;
@@ -303,12 +342,11 @@ __device__ __forceinline__ void fused_pass(sep::Ctx& c, const AxT& T, const floa
         float v[W];
 #pragma unroll
         for (int k = 0; k < W; ++k) v[k] = stage[(size_t)k * C::SLINE + sp];
-        float4* o = reinterpret_cast<float4*>(Zout + (size_t)p * C::LP);
-        o[(e0 >> 2) * 32 + lc] = make_float4(v[0], v[1], v[2], v[3]);
-        o[((e0 >> 2) + 1) * 32 + lc] = make_float4(v[4], v[5], v[6], v[7]);
+        stg8(Zout + (size_t)p * C::LP + ((e0 >> 3) * 32 + lc) * 8, v);
       }
     }
     __syncthreads();
+    if (t) t[7] = stm::gtimer();
   }
 }
 
@@ -352,7 +390,7 @@ __device__ __forceinline__ void fill(const sep::Ctx& c, float* dst, size_t cnt, 
 
 // ------------------------------------------------------------ the kernel (solve only)
 template <int E>
-__global__ void __launch_bounds__(NT, 1) fs1_sep2dw_kernel(const __grid_constant__ Sep2dParams P) {
+__global__ void __launch_bounds__(NT, 2) fs1_sep2dw_kernel(const __grid_constant__ Sep2dParams P) {
   using C = Cfg<E>;
   extern __shared__ __align__(128) unsigned char smem[];
   sep::Ctx c;
@@ -367,6 +405,16 @@ __global__ void __launch_bounds__(NT, 1) fs1_sep2dw_kernel(const __grid_constant
   c.s.xi = reinterpret_cast<int*>(smem + C::OFF_XI);
   c.s.red = reinterpret_cast<double*>(smem + C::OFF_RED);
   c.s.ired = reinterpret_cast<int*>(smem + C::OFF_IRED);
+  WarpIO io;
+  io.ts = c.s.stage + (size_t)c.warp * C::SLINE;
+  io.mb = reinterpret_cast<uint64_t*>(smem + C::OFF_MBAR) + 2 * c.warp;
+  io.ph0 = io.ph1 = 0;
+  if (c.lane == 0) {
+    stm::mbar_init(&io.mb[0], 1);
+    stm::mbar_init(&io.mb[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
   const int n = P.n, m = P.m, G = P.G;
   const float* A = reinterpret_cast<const float*>(P.a);
   const float* Bv = reinterpret_cast<const float*>(P.b);
@@ -400,26 +448,36 @@ __global__ void __launch_bounds__(NT, 1) fs1_sep2dw_kernel(const __grid_constant
   double dummy = 0.0;
   int bad = 0;
   // Z1 = K1 on the columns of F, transposed
-  fused_pass<E, FUSE>(c, T1, Fp, nullptr, nullptr, nullptr, Z1, m, n, G, dummy, bad);
+  fused_pass<E, FUSE>(c, io, T1, Fp, nullptr, nullptr, nullptr, Z1, m, n, G, dummy, bad);
   stm::grid_barrier(P.bar, G, c.gen);
 
   int l = 0, qi = 0, flag = 0;
   double errv = NAN;
   const bool use_tol = P.tol > 0.0;
+  // the loop top checks at l >= itr_max, or every check_interval iterations with tol > 0
+  auto is_check = [&](int k) { return (k >= P.itr_max) || (use_tol && (k % P.check_interval) == 0); };
   while (true) {
-    const bool check = (l >= P.itr_max) || (use_tol && (l % P.check_interval) == 0);
+    const bool check = is_check(l);
     const bool last = l >= P.itr_max;
+    // F^(l+1), G^(l+1) are stored only when the next loop top can stop on them (a check
+    // reads psi^(l+1) and may return the state); otherwise they live in registers only
+    // long enough to produce the next pass's input (Z1, Z2).
+    const bool keep = is_check(l + 1);
     float* Gi = qi ? P.Gt1 : P.Gt0;
     float* Go = qi ? P.Gt0 : P.Gt1;
     double es = 0.0;
     bad = 0;
     // ---- pass R: psi half-step (Alg. 2 lines 3-7) + first pass of the phi half-step
-    if (!check) fused_pass<E, UPD | WR | FUSE>(c, T2, Z1, LBt, nullptr, Go, Z2, n, m, G, es, bad);
-    else if (!last) fused_pass<E, UPD | WR | CHK | FUSE>(c, T2, Z1, LBt, Gi, Go, Z2, n, m, G, es, bad);
-    else fused_pass<E, UPD | CHK>(c, T2, Z1, LBt, Gi, Go, Z2, n, m, G, es, bad);
+    if (last) fused_pass<E, UPD | CHK>(c, io, T2, Z1, LBt, Gi, Go, Z2, n, m, G, es, bad);
+    else if (check && keep) fused_pass<E, UPD | WR | CHK | FUSE>(c, io, T2, Z1, LBt, Gi, Go, Z2, n, m, G, es, bad);
+    else if (check) fused_pass<E, UPD | CHK | FUSE>(c, io, T2, Z1, LBt, Gi, Go, Z2, n, m, G, es, bad);
+    else if (keep) fused_pass<E, UPD | WR | FUSE>(c, io, T2, Z1, LBt, nullptr, Go, Z2, n, m, G, es, bad);
+    else fused_pass<E, UPD | FUSE>(c, io, T2, Z1, LBt, nullptr, Go, Z2, n, m, G, es, bad,
+                                   (P.tdbg && l == 5) ? P.tdbg : nullptr);
     bad = __syncthreads_or(bad);
     int f;
     const double e = sep::grid_sum(c, P, es, 0, f, bad);
+    if (P.tdbg && l == 5 && c.tid == 0) P.tdbg[(size_t)G * W * 16 + c.r] = stm::gtimer();
     if (check) {
       errv = e;
       if (last || errv <= P.tol) {
@@ -427,11 +485,12 @@ __global__ void __launch_bounds__(NT, 1) fs1_sep2dw_kernel(const __grid_constant
         break;
       }
     }
-    qi ^= 1;  // psi^(l+1) is current
+    if (keep) qi ^= 1;  // psi^(l+1) is the stored state
     if (f) { ++l; flag = 2; break; }
     // ---- pass C: phi half-step (lines 8-12) + first pass of the next psi half-step
     bad = 0;
-    fused_pass<E, UPD | WR | FUSE>(c, T1, Z2, LA, nullptr, Fp, Z1, m, n, G, es, bad);
+    if (keep) fused_pass<E, UPD | WR | FUSE>(c, io, T1, Z2, LA, nullptr, Fp, Z1, m, n, G, es, bad);
+    else fused_pass<E, UPD | FUSE>(c, io, T1, Z2, LA, nullptr, Fp, Z1, m, n, G, es, bad);
     bad = __syncthreads_or(bad);
     sep::grid_sum(c, P, 0.0, 1, f, bad);
     ++l;  // line 13
