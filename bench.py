@@ -45,6 +45,7 @@ def parse():
     ap.add_argument("--batch", type=int, default=None, help="pairs per GPU (default: config)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--kernel", type=int, default=0, help="test-only plan override (0 = automatic choice)")
     return ap.parse_args()
 
 
@@ -228,7 +229,7 @@ def run_fs1(args, cfg):
     shape = (cfg.n, cfg.m) if cfg.ndim == 2 else None
     spec = fs1.Spec(ndim=cfg.ndim, n=cfg.n, m=cfg.m, h1=cfg.h1, h2=cfg.h2, eps=cfg.eps, batch=B,
                     dtype=tdt, domain=cfg.domain, input_is_log=cfg.input_is_log,
-                    itr_max=cfg.itr_max, tol=cfg.tol)
+                    itr_max=cfg.itr_max, tol=cfg.tol, kernel=args.kernel)
     plan = fs1.plan(spec, local)
     u, v = torch.empty_like(a), torch.empty_like(b)
     iters = torch.empty(B, dtype=torch.int32, device=dev)

@@ -225,8 +225,9 @@ fs1_status plan_sep2d(fs1_plan_s* p, int device, int force) {
     const Sep2dwEntry* tab = sep2dw_table(&cnt);
     for (int i = 0; i < cnt; ++i) {
       const int E = tab[i].E;
+      if (force >= 20 && i != force - 20) continue;
       if (32LL * E < std::max(d.n, d.m) || c1 * E > 40.0 || c2 * E > 40.0) continue;
-      if (p->sw && p->sw->E <= E) continue;
+      if (p->sw) continue;
       if (cudaFuncSetAttribute(tab[i].fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tab[i].smem) !=
           cudaSuccess)
         return FS1_ERR_CUDA;
@@ -253,7 +254,7 @@ fs1_status plan_sep2d(fs1_plan_s* p, int device, int force) {
           if (P.wax[ax].Lm[k] >= 2.0f) { P.wax[ax].Lm[k] *= 0.5f; P.wax[ax].Le[k] += 1; }
         }
       }
-      snprintf(p->info.kernel, sizeof(p->info.kernel), "sep2dw_f32_log_E%d_W8", E);
+      snprintf(p->info.kernel, sizeof(p->info.kernel), "sep2dw_f32_log_E%d_W8_B%d", E, p->sw->minb);
       p->info.chunk = E;
       p->info.ctas_per_problem = p->gridw;
       p->info.grid = p->gridw;

@@ -42,7 +42,7 @@ int sep2d_lmax();
 
 // K3w warp-per-line separable 2D solve (fs1_sep2dw.cu), E in {8, 16, 32, 64}
 struct Sep2dwEntry {
-  int E;
+  int E, minb;
   const void* fn;
   size_t smem;
   cudaError_t (*launch)(const Sep2dParams&, int grid, cudaStream_t);

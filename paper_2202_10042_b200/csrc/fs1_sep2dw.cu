@@ -6,18 +6,20 @@
 
 namespace fs1 {
 
-template <int E>
+template <int E, int MINB>
 cudaError_t launch_sep2dw_t(const Sep2dParams& P, int grid, cudaStream_t st) {
   void* args[] = {const_cast<Sep2dParams*>(&P)};
-  return cudaLaunchCooperativeKernel((const void*)&sepw::fs1_sep2dw_kernel<E>, dim3(grid), dim3(sepw::NT),
-                                     args, sepw::Cfg<E>::SMEM, st);
+  return cudaLaunchCooperativeKernel((const void*)&sepw::fs1_sep2dw_kernel<E, MINB>, dim3(grid),
+                                     dim3(sepw::NT), args, sepw::Cfg<E>::SMEM, st);
 }
+#define FS1_SEPW(E, MINB) \
+  { E, MINB, (const void*)&sepw::fs1_sep2dw_kernel<E, MINB>, sepw::Cfg<E>::SMEM, &launch_sep2dw_t<E, MINB> }
 
+// auto choice: the first entry (in order) whose 32 E covers both axes; a second
+// E = 64 build with one CTA per SM (255 registers, no spills) is selectable by the
+// test-only plan override 20 + index.
 static const Sep2dwEntry kSepw[] = {
-    {8, (const void*)&sepw::fs1_sep2dw_kernel<8>, sepw::Cfg<8>::SMEM, &launch_sep2dw_t<8>},
-    {16, (const void*)&sepw::fs1_sep2dw_kernel<16>, sepw::Cfg<16>::SMEM, &launch_sep2dw_t<16>},
-    {32, (const void*)&sepw::fs1_sep2dw_kernel<32>, sepw::Cfg<32>::SMEM, &launch_sep2dw_t<32>},
-    {64, (const void*)&sepw::fs1_sep2dw_kernel<64>, sepw::Cfg<64>::SMEM, &launch_sep2dw_t<64>},
+    FS1_SEPW(8, 2), FS1_SEPW(16, 2), FS1_SEPW(32, 2), FS1_SEPW(64, 2), FS1_SEPW(64, 1),
 };
 const Sep2dwEntry* sep2dw_table(int* count) {
   *count = (int)(sizeof(kSepw) / sizeof(kSepw[0]));

@@ -389,8 +389,8 @@ __device__ __forceinline__ void fill(const sep::Ctx& c, float* dst, size_t cnt, 
 }
 
 // ------------------------------------------------------------ the kernel (solve only)
-template <int E>
-__global__ void __launch_bounds__(NT, 2) fs1_sep2dw_kernel(const __grid_constant__ Sep2dParams P) {
+template <int E, int MINB>
+__global__ void __launch_bounds__(NT, MINB) fs1_sep2dw_kernel(const __grid_constant__ Sep2dParams P) {
   using C = Cfg<E>;
   extern __shared__ __align__(128) unsigned char smem[];
   sep::Ctx c;
