@@ -1,0 +1,85 @@
+/* fs1_shard.h — C ABI of the sharded single-problem FS-1 solve (libfs1.so).
+ *
+ * One 1D problem too large for one GPU (north_star: "for single
+ * problems too large for one GPU, to exchange per-shard scan carries") is split
+ * into `world` contiguous segments of whole 256-point tiles, one per rank (GPU).
+ * Every K x of Algorithm 1 is the forward and backward
+ * recursion of Eq. "recursion" over the whole grid; a segment
+ * needs from the others only their totals (forward total at the segment end,
+ * backward total at its start: 4 doubles per rank).  So each half-step is
+ *
+ *     all-gather the ranks' totals of x  ->  fs1_shard_half  ->  totals of y
+ *
+ * and the caller (the Python driver, paper_2202_10042_b200/shard.py) moves the
+ * totals between ranks with one NCCL all-gather per half-step and owns the loop
+ * control (Algorithm 1's while, with the readings of DESIGN.md R2-R6).
+ *
+ * Supported: ndim 1, FS1_F64, FS1_LOG, batch 1, check_interval >= 1, no warm
+ * start.  Arrays are segment slices of the global problem, device pointers,
+ * caller-owned; every call is asynchronous on `stream` and never allocates.
+ * Totals and partial results are device arrays of doubles (exponents stored as
+ * exact doubles).
+ */
+#ifndef FS1_SHARD_H
+#define FS1_SHARD_H
+
+#include "fs1.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct fs1_shard_s fs1_shard_t;
+
+/* fs1_shard_plan — plan rank `rank` of `world` for the global problem `desc`.
+ *   seg_lo, seg_len : receive this rank's segment [seg_lo, seg_lo + seg_len) of
+ *                     the N points (tiles are split as evenly as possible; the
+ *                     segment may be empty only if world > tiles: FS1_ERR_ARG).
+ *   workspace_bytes : device workspace fs1_shard_* need (256-byte aligned).
+ * Errors: FS1_ERR_ARG (world < 1, rank out of range, batch != 1, warm start),
+ * FS1_ERR_EPS, FS1_ERR_UNSUPPORTED (dtype/domain/ndim; h/eps x 256 > 600, the
+ * per-tile fp64 range of DESIGN.md §5.3).                                          */
+fs1_status fs1_shard_plan(const fs1_desc* desc, int world, int rank, int device, fs1_shard_t** out,
+                          size_t* workspace_bytes, int64_t* seg_lo, int64_t* seg_len);
+
+/* fs1_shard_init — load a, b (segment slices, log-weights if desc.input_is_log),
+ * set phi0 = psi0 = 1/N and write phi0's segment totals to tot4
+ * (device, 4 doubles).                                                             */
+fs1_status fs1_shard_init(const fs1_shard_t* s, const void* a_seg, const void* b_seg, double* tot4,
+                          void* workspace, void* stream);
+
+/* fs1_shard_half — one half-step on this segment.
+ *   which   : 0 = psi update psi = b ./ (K^T phi),
+ *             1 = phi update phi = a ./ (K psi).
+ *   hs      : half-step counter (0 for the first psi step; +1 per call that writes).
+ *   check   : also compute this rank's part of the marginal error
+ *             sum_i |psi_i (K^T phi)_i - b_i| with psi = buffer psi_in.
+ *   write   : produce y (0 only for the final check at l = itr_max).
+ *   l1      : iteration recorded if y becomes non-finite (l + 1).
+ *   psi_in, psi_out : psi buffers (0/1): which=0 reads psi_in (check) and writes
+ *             psi_out; which=1 reads psi_in.
+ *   all_tot : device [world][4] totals of x from every rank (the all-gather).
+ *   tot4    : device out, totals of y (write = 1).
+ *   errflag : device out [2] = {error partial of this rank, first iteration l1 whose
+ *             state became non-finite on this rank (0: none)}.                    */
+fs1_status fs1_shard_half(const fs1_shard_t* s, int which, int hs, int check, int write, int l1, int psi_in,
+                          int psi_out, const double* all_tot, double* tot4, double* errflag, void* workspace,
+                          void* stream);
+
+/* fs1_shard_cost_totals — Jordan-block pair totals of psi (buffer `psi`) for the
+ * return line (R7): device out tot8 = 8 doubles.          */
+fs1_status fs1_shard_cost_totals(const fs1_shard_t* s, int psi, double* tot8, void* workspace, void* stream);
+
+/* fs1_shard_finish — this rank's cost partial h sum_k phi_k (W psi)_k over the
+ * segment (all_tot8: device [world][8] from fs1_shard_cost_totals), and F = log phi,
+ * G = log psi of the segment into u_seg, v_seg (device fp64).  The cost is the sum
+ * of the partials over ranks (fixed rank order).  cost_partial may be NULL.        */
+fs1_status fs1_shard_finish(const fs1_shard_t* s, int psi, const double* all_tot8, void* u_seg, void* v_seg,
+                            double* cost_partial, void* workspace, void* stream);
+
+void fs1_shard_destroy(fs1_shard_t* s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FS1_SHARD_H */

@@ -17,7 +17,10 @@ FS1_SCALING, FS1_LOG = 0, 1
 FLAG_CONVERGED, FLAG_NONFINITE, FLAG_ITR_MAX = 1, 2, 4
 
 EXPORTS = ["fs1_plan", "fs1_solve", "fs1_cost", "fs1_apply", "fs1_plan_info",
-           "fs1_plan_destroy", "fs1_status_string", "fs1_abi_version"]
+           "fs1_plan_destroy", "fs1_status_string", "fs1_abi_version",
+           # include/fs1_shard.h
+           "fs1_shard_plan", "fs1_shard_init", "fs1_shard_half", "fs1_shard_cost_totals",
+           "fs1_shard_finish", "fs1_shard_destroy"]
 
 
 class Desc(ctypes.Structure):
@@ -88,5 +91,20 @@ def lib():
         L.fs1__plan_kind.argtypes = [ctypes.POINTER(Desc), ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp),
                                      ctypes.POINTER(ctypes.c_size_t)]
         L.fs1__plan_kind.restype = st
+        # include/fs1_shard.h
+        i64p = ctypes.POINTER(ctypes.c_int64)
+        L.fs1_shard_plan.argtypes = [ctypes.POINTER(Desc), st, st, st, ctypes.POINTER(vp),
+                                     ctypes.POINTER(ctypes.c_size_t), i64p, i64p]
+        L.fs1_shard_plan.restype = st
+        L.fs1_shard_init.argtypes = [vp] * 6
+        L.fs1_shard_init.restype = st
+        L.fs1_shard_half.argtypes = [vp, st, st, st, st, st, st, st, vp, vp, vp, vp, vp]
+        L.fs1_shard_half.restype = st
+        L.fs1_shard_cost_totals.argtypes = [vp, st, vp, vp, vp]
+        L.fs1_shard_cost_totals.restype = st
+        L.fs1_shard_finish.argtypes = [vp, st, vp, vp, vp, vp, vp, vp]
+        L.fs1_shard_finish.restype = st
+        L.fs1_shard_destroy.argtypes = [vp]
+        L.fs1_shard_destroy.restype = None
         _lib = L
     return _lib

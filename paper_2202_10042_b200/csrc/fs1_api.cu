@@ -317,6 +317,7 @@ double powl_d(long double c, long double L) { return (double)expl(-c * L); }
 
 void fill_persist_tables(PersistParams& P, double c, int E) {
   const long double C = (long double)c;
+  P.lamH = powl_d(C, (long double)(E / 2));
   for (int k = 0; k < 5; ++k) {
     const long double L = (long double)E * (1 << k);
     P.lvA[k] = powl_d(C, ceill(L / 2));

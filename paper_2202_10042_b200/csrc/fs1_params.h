@@ -20,6 +20,7 @@ struct PersistParams {
   long long n;       // grid points per problem
   long long batch;
   double lam;        // lambda = e^{-h/eps}
+  double lamH;       // lambda^{E/2}: carry between the two halves of a thread chunk (ILP)
   double h;
   double tol;
   int itr_max;
@@ -124,6 +125,26 @@ struct Sep2dParams {
     float Lm[5];      // lambda_k^{E 2^j} = Lm 2^Le (Remark 3.3)
     int Le[5];
   } wax[2];
+};
+
+// One 1D problem sharded over ranks by contiguous whole-tile segments (K2s,
+// fs1_shard.cuh), fp64 log domain.  Per-rank scalars and tables; the workspace
+// pointers live in the host plan and are passed per launch.
+struct ShardParams {
+  long long n;       // global points N
+  long long lo;      // first global point of this segment (multiple of 256)
+  long long len;     // segment points (T * 256; the last segment's tail past N is padding)
+  long long T0;      // global index of the first tile
+  long long Ttot;    // global tiles
+  int T;             // tiles of this segment
+  int world, rank;
+  double lam, h;
+  double lvd[5];       // lambda^{8 2^k}
+  double lvm8[5];      // ... as (mantissa, exponent)
+  int lve8[5];
+  double lanepow[32];  // lambda^{8 l}
+  double t2m[40];      // lambda^{256 2^j} = t2m 2^t2e (Remark 3.3)
+  int t2e[40];
 };
 
 }  // namespace fs1

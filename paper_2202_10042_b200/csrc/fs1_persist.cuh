@@ -204,61 +204,85 @@ template <class T, int E, int WARPS, bool LOGD> struct Half {
 
   struct Ctx {
     int tid, lane, warp, nv, slot;
-    T lam;
+    T lam, lamH;
     T lA, lB, rA, rB;        // scaling: lane powers
     ER<double> lP, rP;       // log: lane powers
     double* xm;
     int* xi;
   };
 
+  // 3. the recursions from the exact carries, each as two independent chains over the
+  //    chunk halves (ILP): the second half's forward carry is lam^{E/2} cf + f0 and the
+  //    first half's backward carry lam^{E/2} cb + g1 (f0, g1: half aggregates).
   template <bool CHECK, bool MASK, bool SLOW>
   __device__ __forceinline__ static double passes(const Ctx& c, const T (&x)[E], T (&y)[E], int ye,
                                                   const Vt* tgt, int te, Vt* sK, T cf, T cb, T s,
-                                                  int R, int& kexp_out) {
-    const T lam = c.lam;
+                                                  T f0, T g1, int R, int& kexp_out) {
+    constexpr int H = E / 2;
+    constexpr int VEC = PS::VEC;
+    const T lam = c.lam, lH = c.lamH;
+    auto xs = [&](int e) { return SLOW ? x[e] * s : x[e]; };
 
-    // 3a. forward recursion from the carry: p_k = lam p_{k-1} + x_k (Alg. 1 line 5 / 10)
-    T p = cf;
+    // 3a. forward recursion p_k = lam p_{k-1} + x_k (Alg. 1 line 5 / 10)
+    T p = cf, q = fma(lH, cf, SLOW ? f0 * s : f0);
 #pragma unroll
-    for (int e = 0; e < E; ++e) { p = fma(lam, p, SLOW ? x[e] * s : x[e]); y[e] = p; }
+    for (int e = 0; e < H; ++e) {
+      p = fma(lam, p, xs(e));
+      y[e] = p;
+      q = fma(lam, q, xs(H + e));
+      y[H + e] = q;
+    }
 
     // 3b. backward recursion t_k = lam t_{k+1} + x_k, K x = p + lam t_{k+1} (line 6 / 11),
     //     fused with the update y = tgt / Kx (line 7 / 12)
-    T tn = cb;
+    T ta = cb, tb = fma(lH, cb, SLOW ? g1 * s : g1);
     double errp = 0.0;
     T sc = T(1);
     int kexp = 0;
     T errs = T(1);
     if constexpr (CHECK && LOGD) errs = Tt::pow2(max(min(ye + R - te, 120), -120));
     const int sw = PS::swz(c.tid);
+    T tva[VEC], tvb[VEC], yoa[VEC], yob[VEC];
 #pragma unroll
-    for (int j = PS::V - 1; j >= 0; --j) {
-      T tv[PS::VEC];
-      Tt::unpack(tgt[c.tid * PS::V + (j ^ sw)], tv);
-      T yo[PS::VEC];
-      if constexpr (CHECK) Tt::unpack(sK[c.tid * PS::V + (j ^ sw)], yo);
-#pragma unroll
-      for (int r = PS::VEC - 1; r >= 0; --r) {
-        const int e = j * PS::VEC + r;
-        const T kx = fma(lam, tn, y[e]);
-        tn = fma(lam, tn, SLOW ? x[e] * s : x[e]);
-        if constexpr (LOGD) {
-          if (e == E - 1) {
-            kexp = Tt::expo(kx);
-            sc = Tt::pow2(kexp);
-          }
-        }
+    for (int i = 0; i < H; ++i) {
+      const int ea = E - 1 - i, eb = H - 1 - i;
+      if (i % VEC == 0) {
+        Tt::unpack(tgt[c.tid * PS::V + ((ea / VEC) ^ sw)], tva);
+        Tt::unpack(tgt[c.tid * PS::V + ((eb / VEC) ^ sw)], tvb);
         if constexpr (CHECK) {
-          y[e] = kx;
-          const bool valid = !MASK || e < c.nv;
-          if (valid) errp += (double)fabs(fma(yo[r] * errs, kx, -tv[r]));
-        } else {
-          T val;
-          if constexpr (LOGD) val = (tv[r] * sc) * Tt::rcp(kx);
-          else val = tv[r] * Tt::rcp(kx);
-          if (MASK && e >= c.nv) val = T(0);
-          y[e] = val;
+          Tt::unpack(sK[c.tid * PS::V + ((ea / VEC) ^ sw)], yoa);
+          Tt::unpack(sK[c.tid * PS::V + ((eb / VEC) ^ sw)], yob);
         }
+      }
+      const int ra = ea % VEC, rb = eb % VEC;
+      const T kxa = fma(lam, ta, y[ea]);
+      ta = fma(lam, ta, xs(ea));
+      const T kxb = fma(lam, tb, y[eb]);
+      tb = fma(lam, tb, xs(eb));
+      if constexpr (LOGD) {
+        if (i == 0) {
+          kexp = Tt::expo(kxa);
+          sc = Tt::pow2(kexp);
+        }
+      }
+      if constexpr (CHECK) {
+        y[ea] = kxa;
+        y[eb] = kxb;
+        if (!MASK || ea < c.nv) errp += (double)fabs(fma(yoa[ra] * errs, kxa, -tva[ra]));
+        if (!MASK || eb < c.nv) errp += (double)fabs(fma(yob[rb] * errs, kxb, -tvb[rb]));
+      } else {
+        T va, vb;
+        if constexpr (LOGD) {
+          va = (tva[ra] * sc) * Tt::rcp(kxa);
+          vb = (tvb[rb] * sc) * Tt::rcp(kxb);
+        } else {
+          va = tva[ra] * Tt::rcp(kxa);
+          vb = tvb[rb] * Tt::rcp(kxb);
+        }
+        if (MASK && ea >= c.nv) va = T(0);
+        if (MASK && eb >= c.nv) vb = T(0);
+        y[ea] = va;
+        y[eb] = vb;
       }
     }
     kexp_out = kexp;
@@ -271,13 +295,19 @@ template <class T, int E, int WARPS, bool LOGD> struct Half {
   __device__ __forceinline__ static double run(const Ctx& c, const PersistParams& P, const T (&x)[E],
                                                int xe, T (&y)[E], int& ye, const Vt* tgt, int te,
                                                Vt* sK, int par, T& acc, int& R_out, int& k_out) {
-    const T lam = c.lam;
-    // 1. chunk aggregates (Horner; Eq. recursion with zero carries)
-    T f = T(0), g = T(0);
+    const T lam = c.lam, lH = c.lamH;
+    constexpr int H = E / 2;
+    // 1. chunk aggregates (Horner; Eq. recursion with zero carries), four independent
+    //    chains over the halves: f = lam^H f0 + f1 at the chunk end, g = g0 + lam^H g1
+    T f0 = T(0), f1 = T(0), g0 = T(0), g1 = T(0);
 #pragma unroll
-    for (int e = 0; e < E; ++e) f = fma(lam, f, x[e]);
-#pragma unroll
-    for (int e = E - 1; e >= 0; --e) g = fma(lam, g, x[e]);
+    for (int e = 0; e < H; ++e) {
+      f0 = fma(lam, f0, x[e]);
+      f1 = fma(lam, f1, x[H + e]);
+      g0 = fma(lam, g0, x[H - 1 - e]);
+      g1 = fma(lam, g1, x[E - 1 - e]);
+    }
+    const T f = fma(lH, f0, f1), g = fma(lH, g1, g0);
     acc = f + g;  // non-finite input detection (x >= 0: inf and NaN propagate)
 
     // 2. carries
@@ -303,8 +333,8 @@ template <class T, int E, int WARPS, bool LOGD> struct Half {
     if constexpr (CHECK) PS::sts(sK, c.tid, y);  // keep y_old
     double errp;
     int kexp;
-    if (!LOGD || !slow) errp = passes<CHECK, MASK, false>(c, x, y, ye, tgt, te, sK, cf, cb, s, R, kexp);
-    else errp = passes<CHECK, MASK, true>(c, x, y, ye, tgt, te, sK, cf, cb, s, R, kexp);
+    if (!LOGD || !slow) errp = passes<CHECK, MASK, false>(c, x, y, ye, tgt, te, sK, cf, cb, s, f0, g1, R, kexp);
+    else errp = passes<CHECK, MASK, true>(c, x, y, ye, tgt, te, sK, cf, cb, s, f0, g1, R, kexp);
     if constexpr (LOGD) {
       if constexpr (CHECK) errp *= pow2d(te);
       if (!CHECK) ye = (te == ZE) ? ZE : te - R - kexp;
@@ -539,6 +569,7 @@ __global__ void __launch_bounds__(32 * WARPS, (16 / WARPS > 0 ? 16 / WARPS : 1))
   const long long g0 = (long long)c.tid * E;
   c.nv = (int)max(0LL, min((long long)E, n - g0));
   c.lam = (T)P.lam;
+  c.lamH = (T)P.lamH;
   c.xm = xm;
   c.xi = xi;
   if constexpr (!LOGD) {

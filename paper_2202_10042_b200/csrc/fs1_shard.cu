@@ -1,0 +1,221 @@
+// fs1_shard.cu — C ABI of include/fs1_shard.h: plans, workspace layout and launches
+// of the sharded single-problem kernels (fs1_shard.cuh).
+#include <cuda_runtime.h>
+#include <limits.h>
+#include <math.h>
+#include <string.h>
+
+#include <algorithm>
+#include <new>
+
+#include "../../include/fs1_shard.h"
+#include "fs1_shard.cuh"
+
+using namespace fs1;
+
+namespace {
+
+size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+void er_pow_l(long double c, long double L, double* m, int* e) {
+  if (L == 0) {
+    *m = 1.0;
+    *e = 0;
+    return;
+  }
+  const long double x = -L * c / logl(2.0L);
+  const long double f = floorl(x);
+  *m = (double)exp2l(x - f);
+  *e = (int)f;
+  if (*m >= 2.0) { *m *= 0.5; *e += 1; }
+}
+
+// workspace layout of one rank
+struct Ws {
+  size_t Am, Bm, Pm, Q0, Q1, AX, BX, PX, QX0, QX1, tzA, tzB;
+  size_t Fm[2], Bmt[2], Fe[2], Be[2];
+  size_t Jm, Je, part, parte, flag, total;
+};
+Ws ws_layout(long long T, int grid) {
+  Ws w;
+  size_t o = 0;
+  const size_t vd = al256((size_t)T * shd::TILE * 8), ti = al256((size_t)T * 4), td = al256((size_t)T * 8);
+  w.Am = o; o += vd; w.Bm = o; o += vd; w.Pm = o; o += vd; w.Q0 = o; o += vd; w.Q1 = o; o += vd;
+  w.AX = o; o += ti; w.BX = o; o += ti; w.PX = o; o += ti; w.QX0 = o; o += ti; w.QX1 = o; o += ti;
+  w.tzA = o; o += al256((size_t)T); w.tzB = o; o += al256((size_t)T);
+  for (int k = 0; k < 2; ++k) {
+    w.Fm[k] = o; o += td; w.Bmt[k] = o; o += td; w.Fe[k] = o; o += ti; w.Be[k] = o; o += ti;
+  }
+  w.Jm = o; o += 4 * td; w.Je = o; o += 4 * ti;
+  w.part = o; o += al256((size_t)grid * 8);
+  w.parte = o; o += al256((size_t)grid * 4);
+  w.flag = o; o += 256;
+  w.total = o;
+  return w;
+}
+
+}  // namespace
+
+struct fs1_shard_s {
+  fs1_desc d;
+  int device;
+  int grid;  // CTAs of the tile kernels
+  ShardParams P;
+  Ws w;
+};
+
+template <class T> static T* at(void* ws, size_t off) { return reinterpret_cast<T*>((char*)ws + off); }
+
+extern "C" {
+
+fs1_status fs1_shard_plan(const fs1_desc* desc, int world, int rank, int device, fs1_shard_t** out,
+                          size_t* workspace_bytes, int64_t* seg_lo, int64_t* seg_len) {
+  if (!desc || !out) return FS1_ERR_ARG;
+  const fs1_desc& d = *desc;
+  if (world < 1 || rank < 0 || rank >= world || d.batch != 1 || d.warm_start || d.n < 1 || d.itr_max < 0 ||
+      d.tol < 0 || d.check_interval < 1)
+    return FS1_ERR_ARG;
+  if (!(d.eps > 0) || !(d.h1 > 0) || !isfinite(d.eps) || !isfinite(d.h1)) return FS1_ERR_EPS;
+  if (d.ndim != 1 || d.m != 1 || d.dtype != FS1_F64 || d.domain != FS1_LOG) return FS1_ERR_UNSUPPORTED;
+  const double c = d.h1 / d.eps;
+  if (c * shd::TILE > 600.0) return FS1_ERR_UNSUPPORTED;
+  const long long Ttot = (d.n + shd::TILE - 1) / shd::TILE;
+  const long long T0 = (long long)rank * Ttot / world, T1 = (long long)(rank + 1) * Ttot / world;
+  if (T1 <= T0 || T1 - T0 > INT_MAX / shd::TILE) return FS1_ERR_ARG;
+  int sms = 0;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return FS1_ERR_CUDA;
+  fs1_shard_s* s = new (std::nothrow) fs1_shard_s();
+  if (!s) return FS1_ERR_CUDA;
+  s->d = d;
+  s->device = device;
+  ShardParams& P = s->P;
+  memset(&P, 0, sizeof(P));
+  P.n = d.n;
+  P.T0 = T0;
+  P.T = (int)(T1 - T0);
+  P.Ttot = Ttot;
+  P.lo = T0 * shd::TILE;
+  P.len = (long long)P.T * shd::TILE;
+  P.world = world;
+  P.rank = rank;
+  P.lam = exp(-c);
+  P.h = d.h1;
+  const long double C = (long double)c;
+  for (int k = 0; k < 5; ++k) {
+    P.lvd[k] = (double)expl(-C * (long double)(8 << k));
+    er_pow_l(C, (long double)(8 << k), &P.lvm8[k], &P.lve8[k]);
+  }
+  for (int l = 0; l < 32; ++l) P.lanepow[l] = (double)expl(-C * (long double)(8 * l));
+  for (int j = 0; j < 40; ++j) er_pow_l(C, (long double)shd::TILE * ldexpl(1.0L, j), &P.t2m[j], &P.t2e[j]);
+  s->grid = (int)std::min<long long>((long long)sms * 4, std::max<long long>(1, (P.T + shd::NW - 1) / shd::NW));
+  s->w = ws_layout(P.T, s->grid);
+  if (workspace_bytes) *workspace_bytes = s->w.total;
+  if (seg_lo) *seg_lo = P.lo;
+  if (seg_len) *seg_len = std::min<long long>(P.len, d.n - P.lo);
+  *out = s;
+  return FS1_OK;
+}
+
+fs1_status fs1_shard_init(const fs1_shard_t* s, const void* a_seg, const void* b_seg, double* tot4, void* ws,
+                          void* stream) {
+  if (!s || !a_seg || !b_seg || !tot4 || !ws || ((uintptr_t)ws & 255)) return FS1_ERR_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  const ShardParams& P = s->P;
+  const Ws& w = s->w;
+  const int kin = s->d.input_is_log ? 1 : 0;
+  int flag0[2] = {0, INT_MAX};
+  if (cudaMemcpyAsync(at<int>(ws, w.flag), flag0, sizeof(flag0), cudaMemcpyHostToDevice, st) != cudaSuccess)
+    return FS1_ERR_CUDA;
+  const dim3 g(s->grid), b(32 * shd::NW);
+  shd::k_load<<<g, b, 0, st>>>(P, (const double*)a_seg, kin, 0.0, at<double>(ws, w.Am), at<int>(ws, w.AX),
+                               at<unsigned char>(ws, w.tzA), nullptr, nullptr, nullptr, nullptr);
+  shd::k_load<<<g, b, 0, st>>>(P, (const double*)b_seg, kin, 0.0, at<double>(ws, w.Bm), at<int>(ws, w.BX),
+                               at<unsigned char>(ws, w.tzB), nullptr, nullptr, nullptr, nullptr);
+  const double init = 1.0 / (double)P.n;  // phi0 = psi0 = 1/N
+  shd::k_load<<<g, b, 0, st>>>(P, nullptr, 2, init, at<double>(ws, w.Pm), at<int>(ws, w.PX), nullptr,
+                               at<double>(ws, w.Fm[0]), at<int>(ws, w.Fe[0]), at<double>(ws, w.Bmt[0]),
+                               at<int>(ws, w.Be[0]));
+  shd::k_load<<<g, b, 0, st>>>(P, nullptr, 2, init, at<double>(ws, w.Q0), at<int>(ws, w.QX0), nullptr, nullptr,
+                               nullptr, nullptr, nullptr);
+  shd::k_scan<<<1, shd::SCAN_NT, 0, st>>>(P, at<double>(ws, w.Fm[0]), at<int>(ws, w.Fe[0]),
+                                          at<double>(ws, w.Bmt[0]), at<int>(ws, w.Be[0]), tot4);
+  return cudaGetLastError() == cudaSuccess ? FS1_OK : FS1_ERR_CUDA;
+}
+
+fs1_status fs1_shard_half(const fs1_shard_t* s, int which, int hs, int check, int write, int l1, int psi_in,
+                          int psi_out, const double* all_tot, double* tot4, double* errflag, void* ws,
+                          void* stream) {
+  if (!s || !all_tot || !ws || ((uintptr_t)ws & 255) || (which != 0 && which != 1) || hs < 0 ||
+      (psi_in & ~1) || (psi_out & ~1) || (write && !tot4) || (check && !errflag))
+    return FS1_ERR_ARG;
+  if (which == 1 && check) return FS1_ERR_ARG;  // the check rides on the psi half-step (R3)
+  cudaStream_t st = (cudaStream_t)stream;
+  const ShardParams& P = s->P;
+  const Ws& w = s->w;
+  const int si = hs & 1, so = si ^ 1;
+  const size_t Qoff[2] = {w.Q0, w.Q1}, QXoff[2] = {w.QX0, w.QX1};
+  shd::HalfIO io;
+  memset(&io, 0, sizeof(io));
+  io.CFm = at<double>(ws, w.Fm[si]); io.CFe = at<int>(ws, w.Fe[si]);
+  io.CBm = at<double>(ws, w.Bmt[si]); io.CBe = at<int>(ws, w.Be[si]);
+  io.FAm = at<double>(ws, w.Fm[so]); io.FAe = at<int>(ws, w.Fe[so]);
+  io.BAm = at<double>(ws, w.Bmt[so]); io.BAe = at<int>(ws, w.Be[so]);
+  io.allT = all_tot;
+  io.part = at<double>(ws, w.part);
+  io.flag = at<int>(ws, w.flag);
+  io.l = l1;
+  if (which == 0) {  // psi = b ./ (K^T phi)
+    io.xm = at<double>(ws, w.Pm); io.xX = at<int>(ws, w.PX);
+    io.tm = at<double>(ws, w.Bm); io.tX = at<int>(ws, w.BX); io.tz = at<unsigned char>(ws, w.tzB);
+    io.om = at<double>(ws, Qoff[psi_in]); io.oX = at<int>(ws, QXoff[psi_in]);
+    io.ym = at<double>(ws, Qoff[psi_out]); io.yX = at<int>(ws, QXoff[psi_out]);
+  } else {           // phi = a ./ (K psi)
+    io.xm = at<double>(ws, Qoff[psi_in]); io.xX = at<int>(ws, QXoff[psi_in]);
+    io.tm = at<double>(ws, w.Am); io.tX = at<int>(ws, w.AX); io.tz = at<unsigned char>(ws, w.tzA);
+    io.ym = at<double>(ws, w.Pm); io.yX = at<int>(ws, w.PX);
+  }
+  if (check && write && which == 0 && psi_in == psi_out) return FS1_ERR_ARG;  // psi^(l) must survive
+  const dim3 g(s->grid), b(32 * shd::NW);
+  if (check && write) shd::k_half<true, true><<<g, b, 0, st>>>(P, io);
+  else if (check) shd::k_half<true, false><<<g, b, 0, st>>>(P, io);
+  else if (write) shd::k_half<false, true><<<g, b, 0, st>>>(P, io);
+  if (write)
+    shd::k_scan<<<1, shd::SCAN_NT, 0, st>>>(P, io.FAm, io.FAe, io.BAm, io.BAe, tot4);
+  if (check) shd::k_reduce<<<1, 32, 0, st>>>(io.part, s->grid, io.flag, errflag);
+  return cudaGetLastError() == cudaSuccess ? FS1_OK : FS1_ERR_CUDA;
+}
+
+fs1_status fs1_shard_cost_totals(const fs1_shard_t* s, int psi, double* tot8, void* ws, void* stream) {
+  if (!s || !tot8 || !ws || ((uintptr_t)ws & 255) || (psi & ~1)) return FS1_ERR_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  const Ws& w = s->w;
+  const size_t Qoff[2] = {w.Q0, w.Q1}, QXoff[2] = {w.QX0, w.QX1};
+  shd::k_cost_tiles<<<s->grid, 32 * shd::NW, 0, st>>>(s->P, at<double>(ws, Qoff[psi]), at<int>(ws, QXoff[psi]),
+                                                      at<double>(ws, w.Jm), at<int>(ws, w.Je));
+  shd::k_cost_scan<<<1, shd::SCAN_NT, 0, st>>>(s->P, at<double>(ws, w.Jm), at<int>(ws, w.Je), tot8);
+  return cudaGetLastError() == cudaSuccess ? FS1_OK : FS1_ERR_CUDA;
+}
+
+fs1_status fs1_shard_finish(const fs1_shard_t* s, int psi, const double* all_tot8, void* u_seg, void* v_seg,
+                            double* cost_partial, void* ws, void* stream) {
+  if (!s || !ws || ((uintptr_t)ws & 255) || (psi & ~1) || !u_seg || !v_seg) return FS1_ERR_ARG;
+  if (cost_partial && !all_tot8) return FS1_ERR_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  const Ws& w = s->w;
+  const size_t Qoff[2] = {w.Q0, w.Q1}, QXoff[2] = {w.QX0, w.QX1};
+  if (cost_partial) {
+    shd::k_cost_dot<<<s->grid, 32 * shd::NW, 0, st>>>(s->P, at<double>(ws, Qoff[psi]), at<int>(ws, QXoff[psi]),
+                                                      at<double>(ws, w.Pm), at<int>(ws, w.PX), at<double>(ws, w.Jm),
+                                                      at<int>(ws, w.Je), all_tot8, at<double>(ws, w.part),
+                                                      at<int>(ws, w.parte));
+    shd::k_cost_reduce<<<1, 32, 0, st>>>(s->P, at<double>(ws, w.part), at<int>(ws, w.parte), s->grid, cost_partial);
+  }
+  shd::k_store<<<s->grid, 32 * shd::NW, 0, st>>>(s->P, at<double>(ws, w.Pm), at<int>(ws, w.PX), (double*)u_seg);
+  shd::k_store<<<s->grid, 32 * shd::NW, 0, st>>>(s->P, at<double>(ws, Qoff[psi]), at<int>(ws, QXoff[psi]),
+                                                 (double*)v_seg);
+  return cudaGetLastError() == cudaSuccess ? FS1_OK : FS1_ERR_CUDA;
+}
+
+void fs1_shard_destroy(fs1_shard_t* s) { delete s; }
+
+}  // extern "C"

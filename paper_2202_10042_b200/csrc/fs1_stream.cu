@@ -17,8 +17,8 @@ static cudaError_t launch_stream_t(const StreamParams& P, int grid, size_t smem,
   StreamEntry { NW, S, (const void*)&stm::fs1_stream_kernel<NW, S>, &launch_stream_t<NW, S> }
 
 static const StreamEntry kStream[] = {
-    FS1_STREAM_ENTRY(16, 2),   // measured fastest at C3 (86 us per half-step)
-    FS1_STREAM_ENTRY(12, 3),
+    FS1_STREAM_ENTRY(12, 3),   // measured fastest at C3 (88 us per half-step; 16x2: 95 us)
+    FS1_STREAM_ENTRY(16, 2),
     FS1_STREAM_ENTRY(8, 4),
     FS1_STREAM_ENTRY(8, 2),
 };
