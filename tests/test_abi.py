@@ -1,5 +1,5 @@
 """CPU-side checks of the C ABI: the library loads, exports every symbol
-include/fs1.h declares, and rejects invalid descriptions before touching CUDA."""
+include/*.h declares, and rejects invalid descriptions before touching CUDA."""
 import ctypes
 import os
 import re
@@ -12,8 +12,12 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def _header_functions():
-    src = open(os.path.join(ROOT, "include", "fs1.h")).read()
-    return sorted(set(re.findall(r"^\s*(?:fs1_status|void|const char\*|int)\s+(fs1_\w+)\s*\(", src, re.M)))
+    names = set()
+    for h in sorted(os.listdir(os.path.join(ROOT, "include"))):
+        if h.endswith(".h"):
+            src = open(os.path.join(ROOT, "include", h)).read()
+            names |= set(re.findall(r"^\s*(?:fs1_status|void|const char\*|int)\s+(fs1_\w+)\s*\(", src, re.M))
+    return sorted(names)
 
 
 def test_library_exports_every_header_symbol():
