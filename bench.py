@@ -337,7 +337,18 @@ def run_fs1(args, cfg):
                                 "kernel_ms": kern_avg_s * 1e3,
                                 "peak_source": f"derived: {props.multi_processor_count} SMs x "
                                                f"{clk_mhz:.0f} MHz x 16 MUFU/clk / 2 rcp per update"}
-        if info["kernel"].startswith(("stream", "sep2d")):
+        if info["kernel"].startswith("sep2dw"):
+            # K3w keeps its 64 MiB working set in L2 (measured DRAM traffic 0.4 GB per
+            # 300-iteration solve), so its bound is the MUFU pipe: per
+            # update 8 MUFU ops (ex2 in and lg2 out of each of the 4 line applies).
+            clk_mhz = peaks.get("sm_max_mhz", 1965.0)
+            peak = props.multi_processor_count * clk_mhz * 1e6 * MUFU_PER_SM_CLK / 8.0 / 1e9
+            line["roofline"] = {"bound": "alu", "achieved": kern_ups / 1e9, "peak": peak,
+                                "unit": "Gupdate/s", "frac": kern_ups / 1e9 / peak,
+                                "traffic": profile_traffic(cfg.name), "kernel_ms": kern_avg_s * 1e3,
+                                "peak_source": f"derived: {props.multi_processor_count} SMs x {clk_mhz:.0f} MHz "
+                                               f"x 16 MUFU/clk / 8 MUFU per update"}
+        elif info["kernel"].startswith(("stream", "sep2d")):
             # HBM roofline: SURVEY.md §8(d)'s 6 words per update (read x,
             # tgt and write y in both half-steps) x N x iterations; the once-per-solve
             # prologue, exit check, cost and epilogue passes (16 words per point) are
