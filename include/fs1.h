@@ -116,7 +116,7 @@ typedef struct {
  * multi-CTA HBM-streaming scan kernel; 2D -> the separable kernel.
  * Log domain range limits: a persistent chunk of E points needs
  * c E <= 40 (fp32) / 300 (fp64) and c 32 E <= 650 with c = h/eps; fs1_solve on a
- * streaming plan (fp64 log) needs c x 256 <= 600 and returns FS1_ERR_UNSUPPORTED
+ * streaming plan (fp64 log) needs c (min(n, 256) - 1) <= 600 and returns FS1_ERR_UNSUPPORTED
  * otherwise (fs1_apply has no such limit: its range is that of the data).
  * Returns FS1_ERR_ARG / FS1_ERR_EPS / FS1_ERR_UNSUPPORTED / FS1_ERR_CUDA.    */
 fs1_status fs1_plan(const fs1_desc* desc, int device, fs1_plan_t** out, size_t* workspace_bytes);

@@ -37,7 +37,7 @@ typedef struct fs1_shard_s fs1_shard_t;
  *                     segment may be empty only if world > tiles: FS1_ERR_ARG).
  *   workspace_bytes : device workspace fs1_shard_* need (256-byte aligned).
  * Errors: FS1_ERR_ARG (world < 1, rank out of range, batch != 1, warm start),
- * FS1_ERR_EPS, FS1_ERR_UNSUPPORTED (dtype/domain/ndim; h/eps x 256 > 600, the
+ * FS1_ERR_EPS, FS1_ERR_UNSUPPORTED (dtype/domain/ndim; h/eps (min(n, 256) - 1) > 600, the
  * per-tile fp64 range of DESIGN.md §5.3).                                          */
 fs1_status fs1_shard_plan(const fs1_desc* desc, int world, int rank, int device, fs1_shard_t** out,
                           size_t* workspace_bytes, int64_t* seg_lo, int64_t* seg_len);

@@ -592,8 +592,10 @@ fs1_status fs1_solve(const fs1_plan_t* plan, const void* a, const void* b, void*
     if (plan->d.domain != FS1_LOG) return FS1_ERR_UNSUPPORTED;
     // one binary exponent per 256-point tile holds a tile of the potentials in fp64
     // only if they can vary by at most c x 256 <= 600 nats across it: Sinkhorn's
-    // potentials are c-Lipschitz up to log a, log b (R25)
-    if (plan->d.h1 / plan->d.eps * TILE > 600.0) return FS1_ERR_UNSUPPORTED;
+    // potentials are c-Lipschitz up to log a, log b (R25); a tile spans
+    // min(n, 256) - 1 cells
+    if (plan->d.h1 / plan->d.eps * (double)(std::min<long long>(plan->d.n, TILE) - 1) > 600.0)
+      return FS1_ERR_UNSUPPORTED;
     // one cooperative launch per problem, in order on the stream (shared workspace)
     for (long long k = 0; k < plan->d.batch; ++k) {
       StreamParams P = stream_params(plan, workspace);

@@ -150,16 +150,11 @@ template <class T, int E, int WARPS, bool LOGD> struct Persist {
     double G = (double)Ga.m * pow2d(Ga.e - Rw);
 #pragma unroll
     for (int k = 0; k < 5; ++k) {
-      const int d = 1 << k;
-      double up = __shfl_up_sync(FULL, F, d);
-      double dn = __shfl_down_sync(FULL, G, d);
-      if (lane >= d) F = fma(up, P.lvd[k], F);
-      if (lane + d < 32) G = fma(dn, P.lvd[k], G);
+      F = scan_up(F, 1u << k, P.lvd[k]);
+      G = scan_down(G, 1u << k, P.lvd[k]);
     }
-    double cfd = __shfl_up_sync(FULL, F, 1);
-    double cbd = __shfl_down_sync(FULL, G, 1);
-    if (lane == 0) cfd = 0.0;
-    if (lane == 31) cbd = 0.0;
+    const double cfd = prev_or0(F);
+    const double cbd = next_or0(G);
     cf = er_norm<double>(cfd, Rw);
     cb = er_norm<double>(cbd, Rw);
     if constexpr (WARPS > 1) {
@@ -204,85 +199,95 @@ template <class T, int E, int WARPS, bool LOGD> struct Half {
 
   struct Ctx {
     int tid, lane, warp, nv, slot;
-    T lam, lamH;
+    T lam, lamS;  // lambda, lambda^S (S = E / NCH: one sub-chain run)
     T lA, lB, rA, rB;        // scaling: lane powers
     ER<double> lP, rP;       // log: lane powers
     double* xm;
     int* xi;
   };
 
-  // 3. the recursions from the exact carries, each as two independent chains over the
-  //    chunk halves (ILP): the second half's forward carry is lam^{E/2} cf + f0 and the
-  //    first half's backward carry lam^{E/2} cb + g1 (f0, g1: half aggregates).
+  // Sub-chains of a thread chunk (ILP): the chunk is split into NCH runs of S = E/NCH
+  // points whose recursions run interleaved; run c enters with the carry
+  // lam^S (carry of run c-1) + (run c-1's aggregate).  S stays a multiple of the
+  // shared-memory vector width.
+  static constexpr int NCH = (E / PS::VEC >= 4) ? 4 : ((E / PS::VEC >= 2) ? 2 : 1);
+  static constexpr int S = E / NCH;
+
+  // 3. the recursions from the exact carries (fq: forward run aggregates, gq: backward)
   template <bool CHECK, bool MASK, bool SLOW>
   __device__ __forceinline__ static double passes(const Ctx& c, const T (&x)[E], T (&y)[E], int ye,
                                                   const Vt* tgt, int te, Vt* sK, T cf, T cb, T s,
-                                                  T f0, T g1, int R, int& kexp_out) {
-    constexpr int H = E / 2;
+                                                  const T (&fq)[NCH], const T (&gq)[NCH], int R,
+                                                  int& kexp_out) {
     constexpr int VEC = PS::VEC;
-    const T lam = c.lam, lH = c.lamH;
+    const T lam = c.lam, lS = c.lamS;
     auto xs = [&](int e) { return SLOW ? x[e] * s : x[e]; };
 
     // 3a. forward recursion p_k = lam p_{k-1} + x_k (Alg. 1 line 5 / 10)
-    T p = cf, q = fma(lH, cf, SLOW ? f0 * s : f0);
+    T p[NCH];
+    p[0] = cf;
 #pragma unroll
-    for (int e = 0; e < H; ++e) {
-      p = fma(lam, p, xs(e));
-      y[e] = p;
-      q = fma(lam, q, xs(H + e));
-      y[H + e] = q;
+    for (int r = 1; r < NCH; ++r) p[r] = fma(lS, p[r - 1], SLOW ? fq[r - 1] * s : fq[r - 1]);
+#pragma unroll
+    for (int e = 0; e < S; ++e) {
+#pragma unroll
+      for (int r = 0; r < NCH; ++r) {
+        p[r] = fma(lam, p[r], xs(r * S + e));
+        y[r * S + e] = p[r];
+      }
     }
 
     // 3b. backward recursion t_k = lam t_{k+1} + x_k, K x = p + lam t_{k+1} (line 6 / 11),
     //     fused with the update y = tgt / Kx (line 7 / 12)
-    T ta = cb, tb = fma(lH, cb, SLOW ? g1 * s : g1);
+    T t[NCH];
+    t[NCH - 1] = cb;
+#pragma unroll
+    for (int r = NCH - 2; r >= 0; --r) t[r] = fma(lS, t[r + 1], SLOW ? gq[r + 1] * s : gq[r + 1]);
     double errp = 0.0;
     T sc = T(1);
     int kexp = 0;
     T errs = T(1);
     if constexpr (CHECK && LOGD) errs = Tt::pow2(max(min(ye + R - te, 120), -120));
     const int sw = PS::swz(c.tid);
-    T tva[VEC], tvb[VEC], yoa[VEC], yob[VEC];
+    T tv[NCH][VEC], yo[NCH][VEC];
 #pragma unroll
-    for (int i = 0; i < H; ++i) {
-      const int ea = E - 1 - i, eb = H - 1 - i;
+    for (int i = 0; i < S; ++i) {
       if (i % VEC == 0) {
-        Tt::unpack(tgt[c.tid * PS::V + ((ea / VEC) ^ sw)], tva);
-        Tt::unpack(tgt[c.tid * PS::V + ((eb / VEC) ^ sw)], tvb);
-        if constexpr (CHECK) {
-          Tt::unpack(sK[c.tid * PS::V + ((ea / VEC) ^ sw)], yoa);
-          Tt::unpack(sK[c.tid * PS::V + ((eb / VEC) ^ sw)], yob);
+#pragma unroll
+        for (int r = 0; r < NCH; ++r) {
+          const int e = r * S + S - 1 - i;
+          Tt::unpack(tgt[c.tid * PS::V + ((e / VEC) ^ sw)], tv[r]);
+          if constexpr (CHECK) Tt::unpack(sK[c.tid * PS::V + ((e / VEC) ^ sw)], yo[r]);
         }
       }
-      const int ra = ea % VEC, rb = eb % VEC;
-      const T kxa = fma(lam, ta, y[ea]);
-      ta = fma(lam, ta, xs(ea));
-      const T kxb = fma(lam, tb, y[eb]);
-      tb = fma(lam, tb, xs(eb));
-      if constexpr (LOGD) {
-        if (i == 0) {
-          kexp = Tt::expo(kxa);
-          sc = Tt::pow2(kexp);
-        }
-      }
-      if constexpr (CHECK) {
-        y[ea] = kxa;
-        y[eb] = kxb;
-        if (!MASK || ea < c.nv) errp += (double)fabs(fma(yoa[ra] * errs, kxa, -tva[ra]));
-        if (!MASK || eb < c.nv) errp += (double)fabs(fma(yob[rb] * errs, kxb, -tvb[rb]));
-      } else {
-        T va, vb;
+      T kx[NCH];
+#pragma unroll
+      for (int rr = 0; rr < NCH; ++rr) {
+        const int r = NCH - 1 - rr;  // the chunk's last point first: its Kx sets kexp
+        const int e = r * S + S - 1 - i;
+        kx[r] = fma(lam, t[r], y[e]);
+        t[r] = fma(lam, t[r], xs(e));
         if constexpr (LOGD) {
-          va = (tva[ra] * sc) * Tt::rcp(kxa);
-          vb = (tvb[rb] * sc) * Tt::rcp(kxb);
-        } else {
-          va = tva[ra] * Tt::rcp(kxa);
-          vb = tvb[rb] * Tt::rcp(kxb);
+          if (i == 0 && r == NCH - 1) {
+            kexp = Tt::expo(kx[r]);
+            sc = Tt::pow2(kexp);
+          }
         }
-        if (MASK && ea >= c.nv) va = T(0);
-        if (MASK && eb >= c.nv) vb = T(0);
-        y[ea] = va;
-        y[eb] = vb;
+      }
+#pragma unroll
+      for (int r = 0; r < NCH; ++r) {
+        const int e = r * S + S - 1 - i;
+        const int q = e % VEC;
+        if constexpr (CHECK) {
+          y[e] = kx[r];
+          if (!MASK || e < c.nv) errp += (double)fabs(fma(yo[r][q] * errs, kx[r], -tv[r][q]));
+        } else {
+          T v;
+          if constexpr (LOGD) v = (tv[r][q] * sc) * Tt::rcp(kx[r]);
+          else v = tv[r][q] * Tt::rcp(kx[r]);
+          if (MASK && e >= c.nv) v = T(0);
+          y[e] = v;
+        }
       }
     }
     kexp_out = kexp;
@@ -295,19 +300,25 @@ template <class T, int E, int WARPS, bool LOGD> struct Half {
   __device__ __forceinline__ static double run(const Ctx& c, const PersistParams& P, const T (&x)[E],
                                                int xe, T (&y)[E], int& ye, const Vt* tgt, int te,
                                                Vt* sK, int par, T& acc, int& R_out, int& k_out) {
-    const T lam = c.lam, lH = c.lamH;
-    constexpr int H = E / 2;
-    // 1. chunk aggregates (Horner; Eq. recursion with zero carries), four independent
-    //    chains over the halves: f = lam^H f0 + f1 at the chunk end, g = g0 + lam^H g1
-    T f0 = T(0), f1 = T(0), g0 = T(0), g1 = T(0);
+    const T lam = c.lam, lS = c.lamS;
+    // 1. chunk aggregates (Horner; Eq. recursion with zero carries), 2 NCH independent
+    //    chains over the runs: fq[r] forward at the run end, gq[r] backward at its start
+    T fq[NCH], gq[NCH];
 #pragma unroll
-    for (int e = 0; e < H; ++e) {
-      f0 = fma(lam, f0, x[e]);
-      f1 = fma(lam, f1, x[H + e]);
-      g0 = fma(lam, g0, x[H - 1 - e]);
-      g1 = fma(lam, g1, x[E - 1 - e]);
+    for (int r = 0; r < NCH; ++r) fq[r] = gq[r] = T(0);
+#pragma unroll
+    for (int e = 0; e < S; ++e) {
+#pragma unroll
+      for (int r = 0; r < NCH; ++r) {
+        fq[r] = fma(lam, fq[r], x[r * S + e]);
+        gq[r] = fma(lam, gq[r], x[r * S + S - 1 - e]);
+      }
     }
-    const T f = fma(lH, f0, f1), g = fma(lH, g1, g0);
+    T f = fq[0], g = gq[NCH - 1];
+#pragma unroll
+    for (int r = 1; r < NCH; ++r) f = fma(lS, f, fq[r]);
+#pragma unroll
+    for (int r = NCH - 2; r >= 0; --r) g = fma(lS, g, gq[r]);
     acc = f + g;  // non-finite input detection (x >= 0: inf and NaN propagate)
 
     // 2. carries
@@ -333,8 +344,8 @@ template <class T, int E, int WARPS, bool LOGD> struct Half {
     if constexpr (CHECK) PS::sts(sK, c.tid, y);  // keep y_old
     double errp;
     int kexp;
-    if (!LOGD || !slow) errp = passes<CHECK, MASK, false>(c, x, y, ye, tgt, te, sK, cf, cb, s, f0, g1, R, kexp);
-    else errp = passes<CHECK, MASK, true>(c, x, y, ye, tgt, te, sK, cf, cb, s, f0, g1, R, kexp);
+    if (!LOGD || !slow) errp = passes<CHECK, MASK, false>(c, x, y, ye, tgt, te, sK, cf, cb, s, fq, gq, R, kexp);
+    else errp = passes<CHECK, MASK, true>(c, x, y, ye, tgt, te, sK, cf, cb, s, fq, gq, R, kexp);
     if constexpr (LOGD) {
       if constexpr (CHECK) errp *= pow2d(te);
       if (!CHECK) ye = (te == ZE) ? ZE : te - R - kexp;
@@ -569,7 +580,11 @@ __global__ void __launch_bounds__(32 * WARPS, (16 / WARPS > 0 ? 16 / WARPS : 1))
   const long long g0 = (long long)c.tid * E;
   c.nv = (int)max(0LL, min((long long)E, n - g0));
   c.lam = (T)P.lam;
-  c.lamH = (T)P.lamH;
+  {
+    double l = 1.0;  // lambda^S by stepwise multiplication (Remark 3.3)
+    for (int k = 0; k < H::S; ++k) l *= P.lam;
+    c.lamS = (T)l;
+  }
   c.xm = xm;
   c.xi = xi;
   if constexpr (!LOGD) {

@@ -78,7 +78,7 @@ fs1_status fs1_shard_plan(const fs1_desc* desc, int world, int rank, int device,
   if (!(d.eps > 0) || !(d.h1 > 0) || !isfinite(d.eps) || !isfinite(d.h1)) return FS1_ERR_EPS;
   if (d.ndim != 1 || d.m != 1 || d.dtype != FS1_F64 || d.domain != FS1_LOG) return FS1_ERR_UNSUPPORTED;
   const double c = d.h1 / d.eps;
-  if (c * shd::TILE > 600.0) return FS1_ERR_UNSUPPORTED;
+  if (c * (double)(std::min<long long>(d.n, shd::TILE) - 1) > 600.0) return FS1_ERR_UNSUPPORTED;
   const long long Ttot = (d.n + shd::TILE - 1) / shd::TILE;
   const long long T0 = (long long)rank * Ttot / world, T1 = (long long)(rank + 1) * Ttot / world;
   if (T1 <= T0 || T1 - T0 > INT_MAX / shd::TILE) return FS1_ERR_ARG;
@@ -123,9 +123,7 @@ fs1_status fs1_shard_init(const fs1_shard_t* s, const void* a_seg, const void* b
   const ShardParams& P = s->P;
   const Ws& w = s->w;
   const int kin = s->d.input_is_log ? 1 : 0;
-  int flag0[2] = {0, INT_MAX};
-  if (cudaMemcpyAsync(at<int>(ws, w.flag), flag0, sizeof(flag0), cudaMemcpyHostToDevice, st) != cudaSuccess)
-    return FS1_ERR_CUDA;
+  shd::k_init_flag<<<1, 1, 0, st>>>(at<int>(ws, w.flag));
   const dim3 g(s->grid), b(32 * shd::NW);
   shd::k_load<<<g, b, 0, st>>>(P, (const double*)a_seg, kin, 0.0, at<double>(ws, w.Am), at<int>(ws, w.AX),
                                at<unsigned char>(ws, w.tzA), nullptr, nullptr, nullptr, nullptr);

@@ -80,8 +80,8 @@ __device__ __forceinline__ void lane_scan(const ShardParams& P, const double (&v
   Gi = g;
 #pragma unroll
   for (int k = 0; k < 5; ++k) {
-    Fi = stm::scan_up(Fi, 1u << k, P.lvd[k]);
-    Gi = stm::scan_down(Gi, 1u << k, P.lvd[k]);
+    Fi = scan_up(Fi, 1u << k, P.lvd[k]);
+    Gi = scan_down(Gi, 1u << k, P.lvd[k]);
   }
 }
 
@@ -296,8 +296,8 @@ __global__ void __launch_bounds__(32 * NW) k_half(const ShardParams P, const Hal
     }
     double Fi, Gi;
     lane_scan(P, xv, Fi, Gi);
-    const double cf = fma(lp, cfr, stm::prev_or0(Fi));
-    const double cb = fma(rp, cbr, stm::next_or0(Gi));
+    const double cf = fma(lp, cfr, prev_or0(Fi));
+    const double cb = fma(rp, cbr, next_or0(Gi));
     // forward p_k = lam p_{k-1} + x_k; backward t_k = lam t_{k+1} + x_k, K x = p + lam t_{k+1}
     double pf[E];
     double p = cf;
@@ -362,6 +362,11 @@ __global__ void __launch_bounds__(32 * NW) k_half(const ShardParams P, const Hal
     atomicOr(&io.flag[0], 1);
     atomicMin(&io.flag[1], io.l);
   }
+}
+
+__global__ void k_init_flag(int* flag) {
+  flag[0] = 0;
+  flag[1] = 0x7fffffff;
 }
 
 // deterministic sum of the per-CTA partials (fixed order) -> out[0]; out[1] = the first

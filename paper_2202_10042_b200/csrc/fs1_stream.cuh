@@ -132,60 +132,7 @@ __device__ __forceinline__ void fence_async() { asm volatile("fence.proxy.async;
 __device__ __forceinline__ void fence_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
-// Warp scan step without selects: the shuffle's in-range predicate guards the FMA.
-// up:   v + m * v[lane - d]  (lane >= d), else v
-// down: v + m * v[lane + d]  (lane + d < 32), else v
-__device__ __forceinline__ double scan_up(double v, unsigned d, double m) {
-  double r = v;
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t.reg .b32 lo, hi, a, b;\n\t.reg .f64 s;\n\t"
-      "mov.b64 {lo, hi}, %1;\n\t"
-      "shfl.sync.up.b32 a|p, lo, %2, 0, -1;\n\t"
-      "shfl.sync.up.b32 b, hi, %2, 0, -1;\n\t"
-      "mov.b64 s, {a, b};\n\t"
-      "@p fma.rn.f64 %0, %3, s, %1;\n\t}"
-      : "+d"(r)
-      : "d"(v), "r"(d), "d"(m));
-  return r;
-}
-__device__ __forceinline__ double scan_down(double v, unsigned d, double m) {
-  double r = v;
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t.reg .b32 lo, hi, a, b;\n\t.reg .f64 s;\n\t"
-      "mov.b64 {lo, hi}, %1;\n\t"
-      "shfl.sync.down.b32 a|p, lo, %2, 31, -1;\n\t"
-      "shfl.sync.down.b32 b, hi, %2, 31, -1;\n\t"
-      "mov.b64 s, {a, b};\n\t"
-      "@p fma.rn.f64 %0, %3, s, %1;\n\t}"
-      : "+d"(r)
-      : "d"(v), "r"(d), "d"(m));
-  return r;
-}
-// exclusive neighbours: v[lane-1] (0 at lane 0) and v[lane+1] (0 at lane 31)
-__device__ __forceinline__ double prev_or0(double v) {
-  double r = 0.0;
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t.reg .b32 lo, hi, a, b;\n\t"
-      "mov.b64 {lo, hi}, %1;\n\t"
-      "shfl.sync.up.b32 a|p, lo, 1, 0, -1;\n\t"
-      "shfl.sync.up.b32 b, hi, 1, 0, -1;\n\t"
-      "@p mov.b64 %0, {a, b};\n\t}"
-      : "+d"(r)
-      : "d"(v));
-  return r;
-}
-__device__ __forceinline__ double next_or0(double v) {
-  double r = 0.0;
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t.reg .b32 lo, hi, a, b;\n\t"
-      "mov.b64 {lo, hi}, %1;\n\t"
-      "shfl.sync.down.b32 a|p, lo, 1, 31, -1;\n\t"
-      "shfl.sync.down.b32 b, hi, 1, 31, -1;\n\t"
-      "@p mov.b64 %0, {a, b};\n\t}"
-      : "+d"(r)
-      : "d"(v));
-  return r;
-}
+// scan_up / scan_down / prev_or0 / next_or0: fs1_common.cuh
 // t / x without branches: hardware reciprocal estimate, one Newton step, one
 // residual correction of the quotient (< 1 ulp; x = 0 or non-finite -> non-finite).
 __device__ __forceinline__ double fdiv(double t, double x) {
