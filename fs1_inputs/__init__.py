@@ -1,4 +1,5 @@
-"""Seeded synthetic inputs for the five BASELINE.json configurations.
+"""Seeded synthetic inputs for the five BASELINE.json configurations and the paper's
+1D random-distribution workload (E1).
 
 This module is shared by the oracle side (tests, golden scripts) and the CUDA
 side (tests, bench).  It holds NO arithmetic of the method (no kernel, no
@@ -37,6 +38,8 @@ class Config:
     tol: float
     input_is_log: bool
     description: str
+    h: float = 0.0        # axis-1 spacing when not 1/n (E1: 6/(N-1) on [-3, 3])
+    seed_index: int = 0   # seed_c = SEED_BASE + seed_index (0: the digit of "cK")
 
     @property
     def size(self) -> int:
@@ -44,7 +47,7 @@ class Config:
 
     @property
     def h1(self) -> float:
-        return 1.0 / self.n
+        return self.h if self.h else 1.0 / self.n
 
     @property
     def h2(self) -> float:
@@ -74,6 +77,20 @@ CONFIGS = {
                  "batch 65536 pairs (8192 per GPU at 8 GPUs), 1D N=4096 fp32 log domain, "
                  "lognormal(0,1) bin weights, eps=1e-3, 1000 iters"),
 }
+
+# The paper's 1D random distributions (Table 1 :361-378): grid
+# x_i = (i-1) dx - 3, dx = 6/(N-1) on [-3, 3]; u_i, v_j iid U[0,1], normalised; eps = 1e-3;
+# 1000 iterations; 100 trials (here: one batch of 100 pairs).  fp64 scaling domain, the
+# paper's unstabilised FS-1 (its precision is unstated, fp64 implied, R20).
+for _k, _n in enumerate((500, 2000, 8000)):
+    CONFIGS[f"e1_{_n}"] = Config(
+        f"e1_{_n}", 1, _n, 1, 100, "f64", "scaling", 1e-3, 1000, 0.0, False,
+        f"paper E1 (Table 1): 100 trials, 1D N={_n} on [-3,3], dx=6/(N-1), u,v iid U[0,1] "
+        f"normalised, eps=1e-3, 1000 iters, fp64 scaling domain", h=6.0 / (_n - 1), seed_index=11 + _k)
+
+# the paper's FS-1 time per trial on its CPU (Table 1; Xeon Gold 5117):
+# context for the E1 bench lines (updates/s = N x 1000 / time)
+PAPER_TABLE1_SECONDS = {"e1_500": 8.70e-3, "e1_2000": 4.25e-2, "e1_8000": 1.53e-1}
 
 
 def pair_rng(cfg_index: int, pair: int) -> np.random.Generator:
@@ -151,12 +168,18 @@ def _c5_hist(rng, n):
     return w / w.sum()
 
 
+def _e1_hist(rng, n):
+    w = rng.uniform(0.0, 1.0, size=n)
+    return w / w.sum()
+
+
 _DRAW = {
     "c1": lambda rng, cfg: _c1_hist(rng, cfg.n),
     "c2": lambda rng, cfg: _c2_hist(rng, cfg.n),
     "c3": lambda rng, cfg: _c3_loghist(rng, cfg.n),
     "c4": lambda rng, cfg: _c4_loghist(rng, cfg.n, cfg.m),
     "c5": lambda rng, cfg: _c5_hist(rng, cfg.n),
+    "e1": lambda rng, cfg: _e1_hist(rng, cfg.n),
 }
 
 
@@ -167,11 +190,13 @@ def pair(cfg: Config | str, p: int, n: int | None = None):
     if isinstance(cfg, str):
         cfg = CONFIGS[cfg]
     if n is not None and n != cfg.n:
-        cfg = dataclasses.replace(cfg, n=n, m=(n if cfg.ndim == 2 else 1))
-    idx = int(cfg.name[1:])
+        cfg = dataclasses.replace(cfg, n=n, m=(n if cfg.ndim == 2 else 1),
+                                  h=(6.0 / (n - 1) if cfg.h and n > 1 else cfg.h))
+    idx = cfg.seed_index or int(cfg.name[1:])
     rng = pair_rng(idx, p)
-    a = _DRAW[cfg.name](rng, cfg)
-    b = _DRAW[cfg.name](rng, cfg)
+    draw = _DRAW[cfg.name.split("_")[0]]
+    a = draw(rng, cfg)
+    b = draw(rng, cfg)
     return a, b
 
 

@@ -388,6 +388,18 @@ __device__ __forceinline__ void fill(const sep::Ctx& c, float* dst, size_t cnt, 
   for (size_t k = (size_t)c.r * NT + c.tid; k < cnt; k += (size_t)G * NT) dst[k] = v;
 }
 
+// Grid barrier that also ORs one flag over the CTAs (non-check passes: no error sum).
+// bar[1] is a sticky word (zeroed at launch with the barrier counter).
+__device__ __forceinline__ int grid_flag(sep::Ctx& c, const Sep2dParams& P, int myflag) {
+  if (c.tid == 0 && myflag) atomicOr(&P.bar[1], 1u);
+  stm::grid_barrier(P.bar, P.G, c.gen);
+  if (c.tid == 0) c.s.ired[33] = (int)stm::ld_acquire(&P.bar[1]);
+  __syncthreads();
+  const int f = c.s.ired[33];
+  __syncthreads();
+  return f;
+}
+
 // ------------------------------------------------------------ the kernel (solve only)
 template <int E, int MINB>
 __global__ void __launch_bounds__(NT, MINB) fs1_sep2dw_kernel(const __grid_constant__ Sep2dParams P) {
@@ -476,7 +488,9 @@ __global__ void __launch_bounds__(NT, MINB) fs1_sep2dw_kernel(const __grid_const
                                    (P.tdbg && l == 5) ? P.tdbg : nullptr);
     bad = __syncthreads_or(bad);
     int f;
-    const double e = sep::grid_sum(c, P, es, 0, f, bad);
+    double e = 0.0;
+    if (check) e = sep::grid_sum(c, P, es, 0, f, bad);
+    else f = grid_flag(c, P, bad);
     if (P.tdbg && l == 5 && c.tid == 0) P.tdbg[(size_t)G * W * 16 + c.r] = stm::gtimer();
     if (check) {
       errv = e;
@@ -492,7 +506,7 @@ __global__ void __launch_bounds__(NT, MINB) fs1_sep2dw_kernel(const __grid_const
     if (keep) fused_pass<E, UPD | WR | FUSE>(c, io, T1, Z2, LA, nullptr, Fp, Z1, m, n, G, es, bad);
     else fused_pass<E, UPD | FUSE>(c, io, T1, Z2, LA, nullptr, Fp, Z1, m, n, G, es, bad);
     bad = __syncthreads_or(bad);
-    sep::grid_sum(c, P, 0.0, 1, f, bad);
+    f = grid_flag(c, P, bad);
     ++l;  // line 13
     if (f) { flag = 2; break; }
   }
