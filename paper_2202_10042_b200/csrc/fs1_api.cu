@@ -154,7 +154,7 @@ StreamParams stream_params(const fs1_plan_s* p, void* ws) {
 // K3 / K3w workspace: log a, (log b)^T, G ping-pong, two pass scratches, F (K3w), fp32
 // arrays of max(n m, lines x LP) floats each, + per-CTA partials and the barrier
 struct SepWs {
-  size_t LA, LBt, Gt0, Gt1, Z, Z2, Fp, part, flagp, bar, total;
+  size_t LA, LBt, Gt0, Gt1, Z, Z2, Fp, AM, BM, AX, BX, part, flagp, bar, total;
 };
 SepWs sep_ws(size_t nm, size_t nperm, int G) {
   SepWs w;
@@ -167,6 +167,11 @@ SepWs sep_ws(size_t nm, size_t nperm, int G) {
   w.Z = o; o += v;
   w.Z2 = o; o += nperm ? v : 0;
   w.Fp = o; o += nperm ? v : 0;
+  w.AM = o; o += nperm ? v : 0;
+  w.BM = o; o += nperm ? v : 0;
+  const size_t vx = nperm ? al256(nperm / 2) : 0;  // >= [lines][32] ints (nperm = lines x 32 E, E >= 8)
+  w.AX = o; o += vx;
+  w.BX = o; o += vx;
   w.part = o; o += al256((size_t)3 * G * 8);
   w.flagp = o; o += al256((size_t)3 * G * 4);
   w.bar = o; o += 256;
@@ -278,6 +283,10 @@ Sep2dParams sep_params(const fs1_plan_s* p, void* ws) {
   P.Z = (float*)(b + w.Z);
   P.Z2 = P.wE ? (float*)(b + w.Z2) : nullptr;
   P.Fp = P.wE ? (float*)(b + w.Fp) : nullptr;
+  P.AMp = P.wE ? (float*)(b + w.AM) : nullptr;
+  P.BMp = P.wE ? (float*)(b + w.BM) : nullptr;
+  P.AXe = P.wE ? (int*)(b + w.AX) : nullptr;
+  P.BXe = P.wE ? (int*)(b + w.BX) : nullptr;
   P.part = (double*)(b + w.part);
   P.flagp = (int*)(b + w.flagp);
   P.bar = (unsigned*)(b + w.bar);

@@ -111,6 +111,10 @@ struct Sep2dParams {
   float* Z;           // [n*m] pass scratch
   float* Z2;          // K3w: [m][LP] second transposed scratch (permuted lines)
   float* Fp;          // K3w: [m][LP] F state (permuted lines)
+  float* AMp;         // K3w: [m][LP] a as mantissas per lane chunk (permuted lines)
+  float* BMp;         // K3w: [n][LP] b (row lines)
+  int* AXe;           // K3w: [m][32] exponents of the lane chunks of a
+  int* BXe;           // K3w: [n][32]
   double* part;       // [3][G] per-CTA partial sums
   int* flagp;         // [3][G]
   unsigned* bar;

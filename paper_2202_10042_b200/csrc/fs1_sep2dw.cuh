@@ -123,11 +123,10 @@ __device__ __forceinline__ ERf erm(ERf a, float bm, int be) { return ern(a.m * b
 using AxT = Sep2dParams::WAx;
 
 // ------------------------------------------------------------ one line apply
-// A: this lane's chunk of natural logs X (padding -inf).  On return A[e] = (K e^X)_e
-// relative to 2^R (linear fp32), R returned.
+// Natural logs X of this lane's chunk -> mantissas relative to 2^oe, oe = floor(max X
+// log2 e) (one MUFU ex2 per point); an all -inf chunk gives zeros and oe = ZE.
 template <int E>
-__device__ __forceinline__ int line_apply(float (&A)[E], const AxT& T, int lane) {
-  constexpr int H = E / 2;
+__device__ __forceinline__ int prep_log(float (&A)[E]) {
   float M = -INFINITY;
 #pragma unroll
   for (int e = 0; e < E; ++e) M = fmaxf(M, A[e]);
@@ -146,6 +145,14 @@ __device__ __forceinline__ int line_apply(float (&A)[E], const AxT& T, int lane)
 #pragma unroll
     for (int e = 0; e < E; ++e) A[e] = sep::ex2f(fmaf(A[e], LOG2E, -o));
   }
+  return oe;
+}
+
+// A: this lane's chunk as linear mantissas relative to 2^oe (oe = ZE: zero chunk).
+// On return A[e] = (K x)_e relative to 2^R (linear fp32), R returned.
+template <int E>
+__device__ __forceinline__ int line_apply_lin(float (&A)[E], int oe, const AxT& T, int lane) {
+  constexpr int H = E / 2;
   // chunk aggregates (Horner, zero carries), 4 independent chains over the halves
   const float lam = T.lam, lH = T.lamH;
   float f0 = 0.f, f1 = 0.f, g0 = 0.f, g1 = 0.f;
@@ -211,6 +218,13 @@ __device__ __forceinline__ int line_apply(float (&A)[E], const AxT& T, int lane)
   return R;
 }
 
+// A: natural logs of this lane's chunk (padding -inf) -> (K e^X)_e relative to 2^R.
+template <int E>
+__device__ __forceinline__ int line_apply(float (&A)[E], const AxT& T, int lane) {
+  const int oe = prep_log<E>(A);
+  return line_apply_lin<E>(A, oe, T, lane);
+}
+
 template <int E>
 __device__ __forceinline__ void load_line(const float* line, int lane, float (&A)[E]) {
 #pragma unroll
@@ -233,16 +247,23 @@ struct WarpIO {
 };
 
 // One fused pass over `nlines` lines of length `len` (axis tables T):
-//   UPD:  Y = log K e^{X}, values = LT - Y (the update), [CHK] error vs Yold, [WR] -> Yout
-//   FUSE: Z = log K e^{values} (values = X when !UPD), written transposed into Zout
-//         (lines = positions 0..len-1, points = this pass's line indices).
-// Inputs arrive by 1D TMA bulk copies (cp.async.bulk, mbarrier complete_tx) issued by
-// lane 0 when the warp takes the line: the target line lands while the first apply
-// runs, so the update reads it from shared memory without a global-latency stall.
+//   UPD:  k = K e^{X} (linear, relative to 2^R); the update y = tgt / k (PAPER.md:154 /
+//         160) as linear mantissas  s = tm * rcp(k) with chunk exponent tx - R, where
+//         (tm, tx) are the target's mantissas and per-lane-chunk exponents; [CHK] the
+//         marginal error sum |e^{Yold + log k} - e^{LT}|; [WR] the state
+//         y = LT - log k stored as logs into Yout (only where a loop top may stop on it).
+//   FUSE: Z = log K y (y = X when !UPD), written transposed into Zout (lines =
+//         positions 0..len-1, points = this pass's line indices).
+// The target mantissa line arrives by a 1D TMA bulk copy issued when the warp takes
+// the line, so the update reads it from shared memory.  Target entries below 2^-126 of
+// their chunk's largest flush to 0 in s; within the chunk span (c E <= 40 nats) their
+// contribution to every K y is below fp32 resolution, and the stored state (WR) comes
+// from the exact log form.
 template <int E, int MODE>
 __device__ __forceinline__ void fused_pass(sep::Ctx& c, WarpIO& io, const AxT& T, const float* X,
-                                           const float* LT, const float* Yold, float* Yout, float* Zout,
-                                           int nlines, int len, int G, double& errsum, int& bad,
+                                           const float* TM, const int* TX, const float* LT,
+                                           const float* Yold, float* Yout, float* Zout, int nlines,
+                                           int len, int G, double& errsum, int& bad,
                                            unsigned long long* td = nullptr) {
   using C = Cfg<E>;
   const int lane = c.lane, w = c.warp;
@@ -259,42 +280,51 @@ __device__ __forceinline__ void fused_pass(sep::Ctx& c, WarpIO& io, const AxT& T
       if ((MODE & UPD) && lane == 0) {
         stm::fence_async_smem();
         stm::mbar_expect_tx(&io.mb[1], (unsigned)C::LINEB);
-        stm::bulk_g2s(io.ts, LT + off, (unsigned)C::LINEB, &io.mb[1]);
+        stm::bulk_g2s(io.ts, TM + off, (unsigned)C::LINEB, &io.mb[1]);
       }
-      load_line<E>(X + off, lane, A);  // E/4 coalesced LDG.128, all in flight at once
+      load_line<E>(X + off, lane, A);  // E/8 coalesced 256-bit loads, all in flight at once
       if (t) t[1] = stm::gtimer() + (A[0] == 12345.f);
+      int oe2 = 0;
       if (MODE & UPD) {
         const int R = line_apply<E>(A, T, lane);
         if (t) t[2] = stm::gtimer() + (R == 12345);
+        const int tx = TX[(size_t)line * 32 + lane];
+        oe2 = (tx == ZE) ? ZE : tx - R;
         const float Rl = (float)R * LN2;
         double ep = 0.0;
         stm::mbar_wait(&io.mb[1], io.ph1);
         io.ph1 ^= 1u;
         if (t) t[3] = stm::gtimer();
-        const float4* lt4 = reinterpret_cast<const float4*>(io.ts);
+        const float4* tm4 = reinterpret_cast<const float4*>(io.ts);
         int b = 0;
 #pragma unroll
         for (int j = 0; j < E / 8; ++j) {
           if ((j & 1) == 0) __syncwarp();  // bounds the hoisting of the shared loads (registers)
-          const float4 t0 = lt4[(j * 32 + lane) * 2], t1 = lt4[(j * 32 + lane) * 2 + 1];
-          float yo[8];
-          if (MODE & CHK) ldg8(Yold + off + (j * 32 + lane) * 8, yo);  // check passes only
-          const float tl[8] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w};
+          const float4 m0 = tm4[(j * 32 + lane) * 2], m1 = tm4[(j * 32 + lane) * 2 + 1];
+          const float tmv[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
+          float lt[8], yo[8], ys[8];
+          if (MODE & (CHK | WR)) ldg8(LT + off + (j * 32 + lane) * 8, lt);  // rare passes only
+          if (MODE & CHK) ldg8(Yold + off + (j * 32 + lane) * 8, yo);
 #pragma unroll
           for (int r = 0; r < 8; ++r) {
             const int e = 8 * j + r;
-            const float Y = fmaf(sep::lg2f(A[e]), LN2, Rl);
-            if (MODE & CHK) {
-              const float ea = sep::ex2f((yo[r] + Y) * LOG2E);
-              const float eb = (tl[r] == -INFINITY) ? 0.f : sep::ex2f(tl[r] * LOG2E);
-              ep += fabs((double)ea - (double)eb);
+            const float k = A[e];
+            if (MODE & (CHK | WR)) {
+              const float Y = fmaf(sep::lg2f(k), LN2, Rl);
+              if (MODE & CHK) {
+                const float ea = sep::ex2f((yo[r] + Y) * LOG2E);
+                const float eb = (lt[r] == -INFINITY) ? 0.f : sep::ex2f(lt[r] * LOG2E);
+                ep += fabs((double)ea - (double)eb);
+              }
+              ys[r] = (lt[r] == -INFINITY) ? -INFINITY : lt[r] - Y;
+              if (MODE & WR) b |= (ys[r] != ys[r]) | (ys[r] == INFINITY);
             }
-            const float v = (tl[r] == -INFINITY) ? -INFINITY : tl[r] - Y;
+            const float v = tmv[r] * Tr<float>::rcp(k);
             b |= (v != v) | (v == INFINITY);
             A[e] = v;
           }
+          if (MODE & WR) stg8(Yout + off + (j * 32 + lane) * 8, ys);
         }
-        if (MODE & WR) store_line<E>(Yout + off, lane, A);
         if (b) bad = 1;
         if (MODE & CHK) {
           ep = warp_sum(ep);
@@ -303,7 +333,7 @@ __device__ __forceinline__ void fused_pass(sep::Ctx& c, WarpIO& io, const AxT& T
       }
       if (t) t[4] = stm::gtimer() + (A[1] == 12345.f);
       if (MODE & FUSE) {
-        const int R2 = line_apply<E>(A, T, lane);
+        const int R2 = (MODE & UPD) ? line_apply_lin<E>(A, oe2, T, lane) : line_apply<E>(A, T, lane);
         if (t) t[5] = stm::gtimer() + (R2 == 12345);
         const float Rl2 = (float)R2 * LN2;
         __syncwarp();  // every lane has read its target chunk (the stage aliases it)
@@ -347,6 +377,21 @@ __device__ __forceinline__ void fused_pass(sep::Ctx& c, WarpIO& io, const AxT& T
     }
     __syncthreads();
     if (t) t[7] = stm::gtimer();
+  }
+}
+
+// Prologue: target logs (permuted lines) -> linear mantissas relative to one exponent
+// per lane chunk (the update's numerator), exponents to X[line * 32 + lane].
+template <int E>
+__device__ __forceinline__ void to_mantissa(const sep::Ctx& c, const float* Lg, int nlines, float* M, int* X,
+                                            int G) {
+  using C = Cfg<E>;
+  for (int line = c.r * W + c.warp; line < nlines; line += G * W) {
+    float A[E];
+    load_line<E>(Lg + (size_t)line * C::LP, c.lane, A);
+    const int oe = prep_log<E>(A);
+    store_line<E>(M + (size_t)line * C::LP, c.lane, A);
+    X[(size_t)line * 32 + c.lane] = oe;
   }
 }
 
@@ -457,10 +502,17 @@ __global__ void __launch_bounds__(NT, MINB) fs1_sep2dw_kernel(const __grid_const
   fill(c, Z1, (size_t)n * C::LP, -INFINITY, G);
   fill(c, Z2, (size_t)m * C::LP, -INFINITY, G);
   stm::grid_barrier(P.bar, G, c.gen);
+  // the update's numerators a, b as mantissas + per-lane-chunk exponents
+  float* AM = P.AMp;
+  float* BM = P.BMp;
+  int* AX = P.AXe;
+  int* BX = P.BXe;
+  to_mantissa<E>(c, LA, m, AM, AX, G);
+  to_mantissa<E>(c, LBt, n, BM, BX, G);
   double dummy = 0.0;
   int bad = 0;
   // Z1 = K1 on the columns of F, transposed
-  fused_pass<E, FUSE>(c, io, T1, Fp, nullptr, nullptr, nullptr, Z1, m, n, G, dummy, bad);
+  fused_pass<E, FUSE>(c, io, T1, Fp, nullptr, nullptr, nullptr, nullptr, nullptr, Z1, m, n, G, dummy, bad);
   stm::grid_barrier(P.bar, G, c.gen);
 
   int l = 0, qi = 0, flag = 0;
@@ -480,11 +532,12 @@ __global__ void __launch_bounds__(NT, MINB) fs1_sep2dw_kernel(const __grid_const
     double es = 0.0;
     bad = 0;
     // ---- pass R: psi half-step (Alg. 2 lines 3-7) + first pass of the phi half-step
-    if (last) fused_pass<E, UPD | CHK>(c, io, T2, Z1, LBt, Gi, Go, Z2, n, m, G, es, bad);
-    else if (check && keep) fused_pass<E, UPD | WR | CHK | FUSE>(c, io, T2, Z1, LBt, Gi, Go, Z2, n, m, G, es, bad);
-    else if (check) fused_pass<E, UPD | CHK | FUSE>(c, io, T2, Z1, LBt, Gi, Go, Z2, n, m, G, es, bad);
-    else if (keep) fused_pass<E, UPD | WR | FUSE>(c, io, T2, Z1, LBt, nullptr, Go, Z2, n, m, G, es, bad);
-    else fused_pass<E, UPD | FUSE>(c, io, T2, Z1, LBt, nullptr, Go, Z2, n, m, G, es, bad,
+    if (last) fused_pass<E, UPD | CHK>(c, io, T2, Z1, BM, BX, LBt, Gi, Go, Z2, n, m, G, es, bad);
+    else if (check && keep)
+      fused_pass<E, UPD | WR | CHK | FUSE>(c, io, T2, Z1, BM, BX, LBt, Gi, Go, Z2, n, m, G, es, bad);
+    else if (check) fused_pass<E, UPD | CHK | FUSE>(c, io, T2, Z1, BM, BX, LBt, Gi, Go, Z2, n, m, G, es, bad);
+    else if (keep) fused_pass<E, UPD | WR | FUSE>(c, io, T2, Z1, BM, BX, LBt, nullptr, Go, Z2, n, m, G, es, bad);
+    else fused_pass<E, UPD | FUSE>(c, io, T2, Z1, BM, BX, LBt, nullptr, Go, Z2, n, m, G, es, bad,
                                    (P.tdbg && l == 5) ? P.tdbg : nullptr);
     bad = __syncthreads_or(bad);
     int f;
@@ -503,8 +556,8 @@ __global__ void __launch_bounds__(NT, MINB) fs1_sep2dw_kernel(const __grid_const
     if (f) { ++l; flag = 2; break; }
     // ---- pass C: phi half-step (lines 8-12) + first pass of the next psi half-step
     bad = 0;
-    if (keep) fused_pass<E, UPD | WR | FUSE>(c, io, T1, Z2, LA, nullptr, Fp, Z1, m, n, G, es, bad);
-    else fused_pass<E, UPD | FUSE>(c, io, T1, Z2, LA, nullptr, Fp, Z1, m, n, G, es, bad);
+    if (keep) fused_pass<E, UPD | WR | FUSE>(c, io, T1, Z2, AM, AX, LA, nullptr, Fp, Z1, m, n, G, es, bad);
+    else fused_pass<E, UPD | FUSE>(c, io, T1, Z2, AM, AX, LA, nullptr, Fp, Z1, m, n, G, es, bad);
     bad = __syncthreads_or(bad);
     f = grid_flag(c, P, bad);
     ++l;  // line 13
