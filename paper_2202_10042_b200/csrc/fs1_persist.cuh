@@ -556,8 +556,15 @@ __device__ double cost_pass(const PersistParams& P, const typename Tr<T>::V* sx,
 }
 
 // ---------------------------------------------------------------------------------------
+// resident CTAs the register budget is sized for: 16 warps per SM, 8 when the chunk
+// state (2 E values of T per thread) needs more than 128 registers
+template <class T, int E, int WARPS> constexpr int persist_minb() {
+  const int warps = (sizeof(T) * E >= 256) ? 8 : 16;
+  return warps / WARPS > 0 ? warps / WARPS : 1;
+}
+
 template <class T, int E, int WARPS, bool LOGD>
-__global__ void __launch_bounds__(32 * WARPS, (16 / WARPS > 0 ? 16 / WARPS : 1)) fs1_persist_solve(const PersistParams P) {
+__global__ void __launch_bounds__(32 * WARPS, (persist_minb<T, E, WARPS>())) fs1_persist_solve(const PersistParams P) {
   using PS = Persist<T, E, WARPS, LOGD>;
   using H = Half<T, E, WARPS, LOGD>;
   using Vt = typename PS::Vt;
