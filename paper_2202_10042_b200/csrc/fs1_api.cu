@@ -424,12 +424,12 @@ static fs1_status plan_impl(const fs1_desc* desc, int device, int force, fs1_pla
   const bool logd = d.domain == FS1_LOG;
   const double c = d.h1 / d.eps;
 
-  if (d.ndim == 1 && (force == 2 || force >= 10)) {
+  if (d.ndim == 1 && (force == 2 || (force >= 10 && force < 20))) {
     std::lock_guard<std::mutex> lk(g_attr_mu);
     int cur = 0;
     if (cudaGetDevice(&cur) != cudaSuccess) { delete p; return FS1_ERR_CUDA; }
     if (cur != device && cudaSetDevice(device) != cudaSuccess) { delete p; return FS1_ERR_CUDA; }
-    const fs1_status st = plan_stream(p, device, force >= 10 ? force - 10 : -1);
+    const fs1_status st = plan_stream(p, device, (force >= 10 && force < 20) ? force - 10 : -1);
     if (cur != device) cudaSetDevice(cur);
     if (st != FS1_OK) { delete p; return st; }
   } else if (d.ndim == 1) {
@@ -448,6 +448,7 @@ static fs1_status plan_impl(const fs1_desc* desc, int device, int force, fs1_pla
      for (int i = 0; i < cnt; ++i) {
       const PersistEntry& e = tab[i];
       if (e.logd != logd) continue;
+      if (force >= 30 && e.W != force - 30) continue;  // test-only: warps per CTA
       const long long cap = 32LL * e.W * e.E;
       if (cap < d.n) continue;
       if (logd) {
