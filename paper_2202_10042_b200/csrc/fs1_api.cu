@@ -448,7 +448,8 @@ static fs1_status plan_impl(const fs1_desc* desc, int device, int force, fs1_pla
      for (int i = 0; i < cnt; ++i) {
       const PersistEntry& e = tab[i];
       if (e.logd != logd) continue;
-      if (force >= 30 && e.W != force - 30) continue;  // test-only: warps per CTA
+      if (force >= 30 && force < 100 && e.W != force - 30) continue;  // test-only: warps per CTA
+      if (force >= 100 && force < 200 && e.E != force - 100) continue;  // test-only: chunk E
       const long long cap = 32LL * e.W * e.E;
       if (cap < d.n) continue;
       if (logd) {

@@ -6,6 +6,9 @@ static const PersistEntry kTable[] = {
     FS1_PERSIST_ENTRY(float, 0, 8, 1, true),
     FS1_PERSIST_ENTRY(float, 0, 16, 1, true),
     FS1_PERSIST_ENTRY(float, 0, 32, 1, true),
+    FS1_PERSIST_ENTRY(float, 0, 64, 1, true),
+    FS1_PERSIST_ENTRY(float, 0, 64, 2, true),
+    FS1_PERSIST_ENTRY(float, 0, 64, 4, true),
     FS1_PERSIST_ENTRY(float, 0, 32, 2, true),
     FS1_PERSIST_ENTRY(float, 0, 32, 4, true),
     FS1_PERSIST_ENTRY(float, 0, 32, 8, true),
