@@ -540,14 +540,6 @@ fs1_status fs1__plan_kind(const fs1_desc* desc, int device, int kind, fs1_plan_t
   return plan_impl(desc, device, kind, out, workspace_bytes);
 }
 
-// test-only (not in include/fs1.h): per-half-step trace of CTA 0 into buf
-// [2*itr_max+2][threads][10] doubles.
-fs1_status fs1__set_debug(fs1_plan_t* plan, double* buf) {
-  if (!plan) return FS1_ERR_ARG;
-  plan->base.dbg = buf;
-  return FS1_OK;
-}
-
 // test-only (not in include/fs1.h): phase timestamps of the streaming kernel,
 // buf = [grid][64][4] u64 (globaltimer ns at: barrier exit, carries ready, stream
 // done, totals published) for the first 64 psi half-steps.

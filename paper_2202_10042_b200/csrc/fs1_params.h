@@ -28,7 +28,6 @@ struct PersistParams {
   int warm;          // u, v hold the initial state
   int input_is_log;  // a, b hold log-weights
   int write_uv;      // write the final state back to u, v
-  double* dbg;       // optional per-half-step trace (debug builds of the tests only)
   // scaling domain: lambda^{E 2^k} = lvA[k] * lvB[k] (two factors: an underflow of the
   // power alone cannot zero a carry that is still representable, Remark 3.3)
   double lvA[5], lvB[5];

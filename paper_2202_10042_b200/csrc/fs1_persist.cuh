@@ -198,7 +198,7 @@ template <class T, int E, int WARPS, bool LOGD> struct Half {
   using Vt = typename Tt::V;
 
   struct Ctx {
-    int tid, lane, warp, nv, slot;
+    int tid, lane, warp, nv;
     T lam, lamS;  // lambda, lambda^S (S = E / NCH: one sub-chain run)
     T lA, lB, rA, rB;        // scaling: lane powers
     ER<double> lP, rP;       // log: lane powers
@@ -352,11 +352,6 @@ template <class T, int E, int WARPS, bool LOGD> struct Half {
     }
     R_out = R;
     k_out = kexp;
-    if (P.dbg && blockIdx.x == 0) {
-      double* r = P.dbg + ((size_t)c.slot * PS::NT + c.tid) * 10;
-      r[0] = xe; r[1] = R; r[2] = kexp; r[3] = ye; r[4] = slow; r[5] = f; r[6] = cf; r[7] = cb;
-      r[8] = y[0]; r[9] = x[0];
-    }
     return errp;
   }
 
@@ -641,7 +636,6 @@ __global__ void __launch_bounds__(32 * WARPS, (persist_minb<T, E, WARPS>())) fs1
     const bool check = (l >= itr_max) || (use_tol && (l % P.check_interval) == 0);
     T accx = T(0), accy = T(0);
     int R, kx;
-    c.slot = 2 * l;
     if (check) {
       // line 2: err = sum |psi (K^T phi) - b| with phi^(l), psi^(l)
       double ep = full ? H::template run<true, false>(c, P, phi, pe, psi, qe, sB, be, sK, par, accx, R, kx)
@@ -667,7 +661,6 @@ __global__ void __launch_bounds__(32 * WARPS, (persist_minb<T, E, WARPS>())) fs1
       par ^= 1;
     }
     // lines 8-12: phi = a ./ (K psi)
-    c.slot = 2 * l + 1;
     if (full) H::template run<false, false>(c, P, psi, qe, phi, pe, sA, ae, sK, par, accy, R, kx);
     else H::template run<false, true>(c, P, psi, qe, phi, pe, sA, ae, sK, par, accy, R, kx);
     par ^= 1;
