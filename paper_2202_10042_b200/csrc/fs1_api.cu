@@ -84,7 +84,7 @@ fs1_status plan_stream(fs1_plan_s* p, int device, int variant) {
   const long long ntiles = (d.n + TILE - 1) / TILE;
   if (ntiles > (1LL << 30)) return FS1_ERR_UNSUPPORTED;
 
-  const int G = (int)std::min<long long>(sms, ntiles);
+  const int G = (int)std::min<long long>(std::min(sms, 256), ntiles);  // <= 32 x GLANE ranges
   const int ntmax = (int)((ntiles + G - 1) / G);
   int cnt = 0;
   const StreamEntry* tab = stream_table(&cnt);

@@ -476,15 +476,31 @@ __device__ __forceinline__ ER<double> block_er_sum(Ctx& c, const double* vm, con
 // ---------------------------------------------------------------- external carries
 // Warp 0: the other ranges' totals (slot par), each decayed by the precomputed
 // lambda^{256 d_k} to this range's boundary, summed in a fixed order.
+constexpr int GLANE = 8;  // ranges per lane in the warp-0 folds (G <= 256, checked by the plan)
 __device__ __forceinline__ void ext_carries(Ctx& c, const StreamParams& P, int par, ER<double>& CFx, ER<double>& CBx) {
   const double* gt = P.gtot + (size_t)par * P.G * 4;
   const int* ge = P.gtote + (size_t)par * P.G * 4;
+  // all loads first (one L2 round trip), then the fixed-order fold
+  double fm[GLANE], bm[GLANE];
+  int fe[GLANE], be[GLANE];
+#pragma unroll
+  for (int j = 0; j < GLANE; ++j) {
+    const int k = c.lane + 32 * j;
+    fm[j] = bm[j] = 0.0;
+    fe[j] = be[j] = ZE;
+    if (k < P.G) {
+      fm[j] = __ldcg(gt + 4 * k); fe[j] = __ldcg(ge + 4 * k);
+      bm[j] = __ldcg(gt + 4 * k + 1); be[j] = __ldcg(ge + 4 * k + 1);
+    }
+  }
   ER<double> f = er_zero<double>(), b = er_zero<double>();
-  for (int k = c.lane; k < P.G; k += 32) {
-    if (k == c.r) continue;
+#pragma unroll
+  for (int j = 0; j < GLANE; ++j) {
+    const int k = c.lane + 32 * j;
+    if (k >= P.G || k == c.r) continue;
     const ER<double> dp{c.dpm[k], c.dpe[k]};
-    if (k < c.r) f = er_add(f, er_mul(dp, ER<double>{__ldcg(gt + 4 * k), __ldcg(ge + 4 * k)}));
-    else b = er_add(b, er_mul(dp, ER<double>{__ldcg(gt + 4 * k + 1), __ldcg(ge + 4 * k + 1)}));
+    if (k < c.r) f = er_add(f, er_mul(dp, ER<double>{fm[j], fe[j]}));
+    else b = er_add(b, er_mul(dp, ER<double>{bm[j], be[j]}));
   }
   CFx = warp_er_sum(f);
   CBx = warp_er_sum(b);
@@ -1043,11 +1059,24 @@ __device__ __forceinline__ void publish(Ctx& c, const StreamParams& P, int slot,
 // broadcast through shared memory)
 __device__ __forceinline__ void read_slot(Ctx& c, const StreamParams& P, int slot, double& err, int& flag) {
   if (c.warp == 0) {
+    double v[GLANE];
+    int fl[GLANE];
+#pragma unroll
+    for (int j = 0; j < GLANE; ++j) {  // all loads first, then the fixed-order sum
+      const int k = c.lane + 32 * j;
+      v[j] = 0.0;
+      fl[j] = 0;
+      if (k < P.G) {
+        v[j] = __ldcg(P.gtot + ((size_t)slot * P.G + k) * 4 + 2);
+        fl[j] = __ldcg(P.gtote + ((size_t)slot * P.G + k) * 4 + 2);
+      }
+    }
     double s = 0.0;
     int f = 0;
-    for (int k = c.lane; k < P.G; k += 32) {
-      s += __ldcg(P.gtot + ((size_t)slot * P.G + k) * 4 + 2);
-      f |= __ldcg(P.gtote + ((size_t)slot * P.G + k) * 4 + 2);
+#pragma unroll
+    for (int j = 0; j < GLANE; ++j) {
+      s += v[j];
+      f |= fl[j];
     }
     s = warp_sum(s);
     f = __reduce_or_sync(FULL, (unsigned)f);
