@@ -84,7 +84,7 @@ fs1_status plan_stream(fs1_plan_s* p, int device, int variant) {
   const long long ntiles = (d.n + TILE - 1) / TILE;
   if (ntiles > (1LL << 30)) return FS1_ERR_UNSUPPORTED;
 
-  const int G = (int)std::min<long long>(std::min(sms, 256), ntiles);  // <= 32 x GLANE ranges
+  const int G = (int)std::min<long long>(std::min(sms, 256), ntiles);  // one range per thread in the folds
   const int ntmax = (int)((ntiles + G - 1) / G);
   int cnt = 0;
   const StreamEntry* tab = stream_table(&cnt);
@@ -92,6 +92,7 @@ fs1_status plan_stream(fs1_plan_s* p, int device, int variant) {
   size_t smem = 0;
   for (int i = 0; i < cnt; ++i) {
     if (variant >= 0 && i != variant) continue;
+    if (32 * tab[i].NW < G) continue;  // ext_carries_cta: one range per thread
     const size_t need = stream_smem(tab[i].NW, tab[i].S, ntmax, G);
     if (need <= (size_t)optin) { best = &tab[i]; smem = need; break; }
   }

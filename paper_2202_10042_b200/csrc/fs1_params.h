@@ -68,7 +68,7 @@ struct StreamParams {
   double* gtot2;     // [G][8] cost-phase range totals (p, P', t, Q') m
   int* gtot2e;       // [G][8]
   unsigned* bar;     // grid barrier {count, generation}
-  unsigned long long* tdbg;  // optional phase timestamps (test-only), [G][64 half-steps][4]
+  unsigned long long* tdbg;  // optional phase timestamps (test-only), [G][64 half-steps][8]
   long long n;
   long long npad;    // ntiles * 256
   int ntiles;

@@ -477,33 +477,24 @@ __device__ __forceinline__ ER<double> block_er_sum(Ctx& c, const double* vm, con
 // Warp 0: the other ranges' totals (slot par), each decayed by the precomputed
 // lambda^{256 d_k} to this range's boundary, summed in a fixed order.
 constexpr int GLANE = 8;  // ranges per lane in the warp-0 folds (G <= 256, checked by the plan)
-__device__ __forceinline__ void ext_carries(Ctx& c, const StreamParams& P, int par, ER<double>& CFx, ER<double>& CBx) {
+// Every thread decays at most one other range's totals (range k = tid, G <= NT); the
+// per-warp sums are folded by warp 0 in warp order (fixed order: deterministic).
+__device__ __forceinline__ void ext_carries_cta(Ctx& c, const StreamParams& P, int par, double* wm, int* we) {
   const double* gt = P.gtot + (size_t)par * P.G * 4;
   const int* ge = P.gtote + (size_t)par * P.G * 4;
-  // all loads first (one L2 round trip), then the fixed-order fold
-  double fm[GLANE], bm[GLANE];
-  int fe[GLANE], be[GLANE];
-#pragma unroll
-  for (int j = 0; j < GLANE; ++j) {
-    const int k = c.lane + 32 * j;
-    fm[j] = bm[j] = 0.0;
-    fe[j] = be[j] = ZE;
-    if (k < P.G) {
-      fm[j] = __ldcg(gt + 4 * k); fe[j] = __ldcg(ge + 4 * k);
-      bm[j] = __ldcg(gt + 4 * k + 1); be[j] = __ldcg(ge + 4 * k + 1);
-    }
-  }
   ER<double> f = er_zero<double>(), b = er_zero<double>();
-#pragma unroll
-  for (int j = 0; j < GLANE; ++j) {
-    const int k = c.lane + 32 * j;
-    if (k >= P.G || k == c.r) continue;
+  const int k = c.tid;
+  if (k < P.G && k != c.r) {
     const ER<double> dp{c.dpm[k], c.dpe[k]};
-    if (k < c.r) f = er_add(f, er_mul(dp, ER<double>{fm[j], fe[j]}));
-    else b = er_add(b, er_mul(dp, ER<double>{bm[j], be[j]}));
+    if (k < c.r) f = er_mul(dp, ER<double>{__ldcg(gt + 4 * k), __ldcg(ge + 4 * k)});
+    else b = er_mul(dp, ER<double>{__ldcg(gt + 4 * k + 1), __ldcg(ge + 4 * k + 1)});
   }
-  CFx = warp_er_sum(f);
-  CBx = warp_er_sum(b);
+  f = warp_er_sum(f);
+  b = warp_er_sum(b);
+  if (c.lane == 0) {
+    wm[2 * c.warp] = f.m; we[2 * c.warp] = f.e;
+    wm[2 * c.warp + 1] = b.m; we[2 * c.warp + 1] = b.e;
+  }
 }
 // tiles between range k and this range r (the decay distance of k's total)
 __device__ __forceinline__ long long range_gap(const StreamParams& P, int k, int r) {
@@ -512,16 +503,25 @@ __device__ __forceinline__ long long range_gap(const StreamParams& P, int k, int
 
 // [A]: full per-tile carries of the consumed vector x (tables F/B, exponents Xx).
 __device__ __forceinline__ void tile_carries(Ctx& c, const StreamParams& P, int par, const double* Fm, const int* Fe,
-                             const double* Bm, const int* Be, const int* Xx) {
+                             const double* Bm, const int* Be, const int* Xx, unsigned long long* td = nullptr) {
+  ext_carries_cta(c, P, par, c.redm + 64, c.rede + 64);
+  __syncthreads();
+  if (td) td[4] = gtimer();
   if (c.warp == 0) {
-    ER<double> CFx, CBx;
-    ext_carries(c, P, par, CFx, CBx);
+    ER<double> F = er_zero<double>(), B = er_zero<double>();
+    if (c.lane < c.NW) {
+      F = ER<double>{c.redm[64 + 2 * c.lane], c.rede[64 + 2 * c.lane]};
+      B = ER<double>{c.redm[64 + 2 * c.lane + 1], c.rede[64 + 2 * c.lane + 1]};
+    }
+    F = warp_er_sum(F);
+    B = warp_er_sum(B);
     if (c.lane == 0) {
-      c.redm[0] = CFx.m; c.rede[0] = CFx.e;
-      c.redm[1] = CBx.m; c.rede[1] = CBx.e;
+      c.redm[0] = F.m; c.rede[0] = F.e;
+      c.redm[1] = B.m; c.rede[1] = B.e;
     }
   }
   __syncthreads();
+  if (td) td[5] = gtimer();
   const ER<double> CFx{c.redm[0], c.rede[0]}, CBx{c.redm[1], c.rede[1]};
   for (int i = c.tid; i < c.nt; i += c.NT) {
     const ER<double> CF = er_fma(pw(c, i), CFx, ER<double>{Fm[i], Fe[i]});
@@ -1208,9 +1208,9 @@ __global__ void __launch_bounds__(32 * NW, 1) fs1_stream_kernel(const __grid_con
     const bool check = (l >= P.itr_max) || (use_tol && (l % P.check_interval) == 0);
     const bool last = l >= P.itr_max;
     // ---- lines 2-7: psi = b ./ (K^T phi), with the marginal error on check iterations
-    unsigned long long* td = (P.tdbg && c.tid == 0 && l < 64) ? P.tdbg + ((size_t)c.r * 64 + l) * 4 : nullptr;
+    unsigned long long* td = (P.tdbg && c.tid == 0 && l < 64) ? P.tdbg + ((size_t)c.r * 64 + l) * 8 : nullptr;
     if (td) td[0] = gtimer();
-    tile_carries(c, P, par, c.PFm, c.PFe, c.PBm, c.PBe, c.PX);
+    tile_carries(c, P, par, c.PFm, c.PFe, c.PBm, c.PBe, c.PX, td);
     if (td) td[1] = gtimer();
     const int qo = check ? (qi ^ 1) : qi;  // a checking step keeps psi^(l) in Qm[qi]
     double* Qi = qi ? P.Qm1 : P.Qm0;

@@ -14,12 +14,12 @@ spec = fs1.Spec(ndim=1, n=cfg.n, m=1, h1=cfg.h1, h2=0.0, eps=cfg.eps, batch=1, d
                 domain="log", input_is_log=True, itr_max=60, kernel=kern)
 p = fs1.plan(spec, 0)
 G = p.info()["grid"]
-buf = torch.zeros(G * 64 * 4, dtype=torch.int64, device="cuda")
+buf = torch.zeros(G * 64 * 8, dtype=torch.int64, device="cuda")
 lib = _lib.lib()
 lib.fs1__set_stream_timers.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
 lib.fs1__set_stream_timers(p._h, ctypes.c_void_p(buf.data_ptr()))
 o = fs1.solve(A, B, **kw); torch.cuda.synchronize()
-t = buf.cpu().numpy().reshape(G, 64, 4).astype(np.float64)
+t = buf.cpu().numpy().reshape(G, 64, 8).astype(np.float64)
 t = t[:, 5:59]  # steady state
 carries = t[:, :, 1] - t[:, :, 0]
 stream = t[:, :, 2] - t[:, :, 1]
@@ -30,3 +30,7 @@ waitb = t[:, :, 0] - 0
 print(f"CTAs {G}; per psi half-step (us): carries {np.median(carries)/1e3:.2f}  stream med {np.median(stream)/1e3:.2f} "
       f"max {np.median(stream.max(0))/1e3:.2f} min {np.median(stream.min(0))/1e3:.2f}  scan+publish {np.median(scan)/1e3:.2f}  "
       f"iteration {np.median(step)/1e3:.2f}")
+ext = t[:, :, 4] - t[:, :, 0]
+sync1 = t[:, :, 5] - t[:, :, 4]
+tiles = t[:, :, 1] - t[:, :, 5]
+print(f"  carries split (us): ext fold {np.median(ext)/1e3:.2f}  first sync {np.median(sync1)/1e3:.2f}  per-tile {np.median(tiles)/1e3:.2f}")
