@@ -221,24 +221,26 @@ __global__ void __launch_bounds__(SCAN_NT) k_scan(const ShardParams P, double* F
   if (tid == 0) { tot[2] = cb.m; tot[3] = (double)cb.e; }
 }
 
-// Decay of the other ranks' totals to this segment (fixed fold order): forward from
-// ranks k < r over the tiles between k's end and this segment's start; backward from
-// ranks k > r.  allT = [world][4] {F m, F e, B m, B e}.
-__device__ __forceinline__ void ext_carries(const ShardParams& P, const double* allT, ER<double>& EF,
+// Decay of the other ranks' totals to this segment: lane k of warp 0 takes rank k
+// (forward from ranks k < r over the tiles between k's end and this segment's start,
+// backward from ranks k > r), then a fixed-order warp sum.  allT = [world][4]
+// {F m, F e, B m, B e}; world <= 32 per pass of the lane loop.
+__device__ __forceinline__ void ext_carries(const ShardParams& P, const double* allT, int lane, ER<double>& EF,
                                             ER<double>& EB) {
-  EF = er_zero<double>();
-  EB = er_zero<double>();
-  for (int k = 0; k < P.world; ++k) {
+  ER<double> f = er_zero<double>(), b = er_zero<double>();
+  for (int k = lane; k < P.world; k += 32) {
     if (k == P.rank) continue;
     const long long T0k = (long long)k * P.Ttot / P.world, T1k = (long long)(k + 1) * P.Ttot / P.world;
     if (k < P.rank) {
       const ER<double> t{allT[4 * k], (int)allT[4 * k + 1]};
-      EF = er_add(EF, er_mul(powt(P, P.T0 - T1k), t));
+      f = er_add(f, er_mul(powt(P, P.T0 - T1k), t));
     } else {
       const ER<double> t{allT[4 * k + 2], (int)allT[4 * k + 3]};
-      EB = er_add(EB, er_mul(powt(P, T0k - (P.T0 + P.T)), t));
+      b = er_add(b, er_mul(powt(P, T0k - (P.T0 + P.T)), t));
     }
   }
+  EF = stm::warp_er_sum(f);
+  EB = stm::warp_er_sum(b);
 }
 
 // ------------------------------------------------------------------ k_half
@@ -264,10 +266,8 @@ __global__ void __launch_bounds__(32 * NW) k_half(const ShardParams P, const Hal
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (warp == 0) {
     ER<double> EF, EB;
-    if (lane == 0) {
-      ext_carries(P, io.allT, EF, EB);
-      sEm[0] = EF.m; sEe[0] = EF.e; sEm[1] = EB.m; sEe[1] = EB.e;
-    }
+    ext_carries(P, io.allT, lane, EF, EB);
+    if (lane == 0) { sEm[0] = EF.m; sEe[0] = EF.e; sEm[1] = EB.m; sEe[1] = EB.e; }
   }
   __syncthreads();
   const ER<double> EF{sEm[0], sEe[0]}, EB{sEm[1], sEe[1]};
