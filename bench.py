@@ -177,9 +177,9 @@ def sample_plan(cfg):
         return list(range(8)), 200, "8 pairs, 200 of 1000 iterations, dense fp64 (BLAS)"
     if cfg.name == "c1":
         return [0], 700, "1 pair, 700 iterations, dense fp64"
-    if cfg.name.startswith("e1_"):
+    if cfg.name.startswith(("e1_", "e2_")):
         it = {500: 500, 2000: 50, 8000: 20}.get(cfg.n, 20)
-        return [0], it, f"1 of 100 pairs, {it} of 1000 iterations, dense fp64"
+        return [0], it, f"1 of 100 pairs, {it} of {cfg.itr_max} iterations, dense fp64"
     return [0], 1, "1 pair, 1 iteration, plain-C LSE recursion"
 
 
@@ -354,10 +354,11 @@ def run_fs1(args, cfg):
         if cfg.name in gi.PAPER_TABLE1_SECONDS:
             # the paper's own FS-1 number for this exact workload (Table 1, PAPER.md:371-373:
             # seconds per 1000-iteration trial on a 14-core Xeon Gold 5117, CPU): context
-            paper_ups = cfg.n * 1000 / gi.PAPER_TABLE1_SECONDS[cfg.name]
+            paper_ups = cfg.n * cfg.itr_max / gi.PAPER_TABLE1_SECONDS[cfg.name]
             line["vs_baseline"] = value / paper_ups
-            line["baseline"] = {"value": paper_ups, "unit": UNIT, "source": "PAPER.md Table 1 (CPU, "
-                                "Xeon Gold 5117), N x 1000 / seconds per trial", "hardware": "CPU"}
+            table = "Table 1" if cfg.name.startswith("e1") else "Table 2"
+            line["baseline"] = {"value": paper_ups, "unit": UNIT, "source": f"PAPER.md {table} (CPU, "
+                                "Xeon Gold 5117), N x iterations / seconds per trial", "hardware": "CPU"}
         if info["kernel"].startswith("persist"):
             clk_mhz = peaks.get("sm_max_mhz", 1965.0)
             peak = alu_peak_updates(props.multi_processor_count, clk_mhz) / 1e9

@@ -88,9 +88,23 @@ for _k, _n in enumerate((500, 2000, 8000)):
         f"paper E1 (Table 1): 100 trials, 1D N={_n} on [-3,3], dx=6/(N-1), u,v iid U[0,1] "
         f"normalised, eps=1e-3, 1000 iters, fp64 scaling domain", h=6.0 / (_n - 1), seed_index=11 + _k)
 
-# the paper's FS-1 time per trial on its CPU (Table 1; Xeon Gold 5117):
-# context for the E1 bench lines (updates/s = N x 1000 / time)
-PAPER_TABLE1_SECONDS = {"e1_500": 8.70e-3, "e1_2000": 4.25e-2, "e1_8000": 1.53e-1}
+# The paper's Ricker-wavelet experiment (Table 2 :412-429): f = R(t),
+# g = R(t - s), R(t) = (1 - 2 pi^2 t^2) exp(-pi^2 t^2) (f0 = A = 1), s = -1.2032, squared and
+# normalised by Eq. (ricker) with delta = 1e-3 (L = N so that each sums to 1); eps = 1e-2,
+# 500 iterations, repeated 100 times (one batch of 100 identical pairs).  The time interval
+# is unstated: [-4, 4] (SPEC.md's reading, R28), dt = 8/(N-1).  fp64 scaling domain.
+for _k, _n in enumerate((500, 2000, 8000)):
+    CONFIGS[f"e2_{_n}"] = Config(
+        f"e2_{_n}", 1, _n, 1, 100, "f64", "scaling", 1e-2, 500, 0.0, False,
+        f"paper E2 (Table 2): Ricker wavelet R(t) vs R(t+1.2032) on [-4,4], N={_n}, squared, "
+        f"normalised with delta=1e-3, eps=1e-2, 500 iters, 100 repetitions, fp64 scaling domain",
+        h=8.0 / (_n - 1), seed_index=21 + _k)
+
+# the paper's FS-1 time per trial on its CPU (Xeon Gold 5117): Table 1 (PAPER.md:371-373,
+# 1000 iterations) and Table 2 (PAPER.md:422-424, 500 iterations); context for the paper
+# workload bench lines (updates/s = N x iterations / time)
+PAPER_TABLE1_SECONDS = {"e1_500": 8.70e-3, "e1_2000": 4.25e-2, "e1_8000": 1.53e-1,
+                        "e2_500": 4.90e-3, "e2_2000": 1.52e-2, "e2_8000": 5.96e-2}
 
 
 def pair_rng(cfg_index: int, pair: int) -> np.random.Generator:
@@ -173,6 +187,26 @@ def _e1_hist(rng, n):
     return w / w.sum()
 
 
+RICKER_SHIFT = -1.2032
+RICKER_DELTA = 1e-3
+
+
+def ricker(t):
+    """R(t) = A (1 - 2 pi^2 f0^2 t^2) exp(-pi^2 f0^2 t^2), f0 = A = 1."""
+    x = (math.pi * t) ** 2
+    return (1.0 - 2.0 * x) * np.exp(-x)
+
+
+def ricker_pair(n, lo=-4.0, hi=4.0, shift=RICKER_SHIFT, delta=RICKER_DELTA):
+    """(u, v) of Eq. (ricker): (f^2/||f^2||_1 + delta) / (1 + N delta), f = R(t), g = R(t - s)."""
+    t = np.linspace(lo, hi, n)
+    out = []
+    for f in (ricker(t), ricker(t - shift)):
+        f2 = f * f
+        out.append((f2 / f2.sum() + delta) / (1.0 + n * delta))
+    return out[0], out[1]
+
+
 _DRAW = {
     "c1": lambda rng, cfg: _c1_hist(rng, cfg.n),
     "c2": lambda rng, cfg: _c2_hist(rng, cfg.n),
@@ -194,6 +228,8 @@ def pair(cfg: Config | str, p: int, n: int | None = None):
                                   h=(6.0 / (n - 1) if cfg.h and n > 1 else cfg.h))
     idx = cfg.seed_index or int(cfg.name[1:])
     rng = pair_rng(idx, p)
+    if cfg.name.startswith("e2"):  # deterministic signals: every repetition is the same pair
+        return ricker_pair(cfg.n)
     draw = _DRAW[cfg.name.split("_")[0]]
     a = draw(rng, cfg)
     b = draw(rng, cfg)
