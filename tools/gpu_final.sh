@@ -6,7 +6,7 @@ mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $O/smi.txt 2>&1
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/smoke.log
 timeout 300 python bench.py > $O/bench_c2.json 2> $O/bench_c2.err
-for c in c1 c3 c4 c5 e1_8000; do
+for c in c1 c3 c4 c5 e1_8000 e2_8000; do
   timeout 400 python bench.py --config $c --steps 5 --warmup 3 > $O/bench_$c.json 2> $O/bench_$c.err
 done
 timeout 300 python bench.py --impl reference --steps 2 --warmup 3 > $O/bench_ref.json 2> $O/bench_ref.err
