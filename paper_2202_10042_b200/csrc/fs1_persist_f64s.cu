@@ -8,6 +8,7 @@ static const PersistEntry kTable[] = {
     FS1_PERSIST_ENTRY(double, 1, 4, 4, false),
     FS1_PERSIST_ENTRY(double, 1, 4, 8, false),
     FS1_PERSIST_ENTRY(double, 1, 4, 16, false),
+    FS1_PERSIST_ENTRY(double, 1, 8, 4, false),
     FS1_PERSIST_ENTRY(double, 1, 8, 16, false),
     FS1_PERSIST_ENTRY(double, 1, 16, 16, false),
 };
