@@ -129,6 +129,31 @@ def test_sep2d_linear_weights_and_tolerance_stop():
     assert_solve_parity(o2, r2, "log", "f32", tol=TOL32, check_err=False)
 
 
+@pytest.mark.parametrize("ci", [2, 5])
+def test_sep2d_check_interval(ci):
+    """Checks every ci iterations (the solve keeps F, G only ahead of check iterations,
+    DESIGN.md R26): the stop lands within ci of the oracle's, and the replay at the
+    oracle's own stop is its state."""
+    n, m = 96, 80
+    la, lb = _pair2d(n, m, 13)
+    A, B = la.astype(np.float32), lb.astype(np.float32)
+    kw = dict(h=1 / n, h2=1 / m, eps=0.02, domain="log", input_is_log=True, shape=(n, m))
+    out = fs1.solve(_cuda(A[None]), _cuda(B[None]), itr_max=4000, tol=1e-5, check_interval=ci, **kw)
+    ref = sinkhorn.solve(A.astype(np.float64), B.astype(np.float64), n=n, m=m, h1=1 / n, h2=1 / m, eps=0.02,
+                         itr_max=4000, tol=1e-5, check_interval=ci, domain="log", input_is_log=True, apply="recur")
+    assert out["flags"].item() == 1 and out["err"].item() <= 1e-5
+    assert out["iters"].item() % ci == 0
+    assert abs(int(out["iters"].item()) - int(ref["iters"][0])) <= ci
+    it = int(out["iters"].item())
+    r2 = sinkhorn.solve(A.astype(np.float64), B.astype(np.float64), n=n, m=m, h1=1 / n, h2=1 / m, eps=0.02,
+                        itr_max=it, domain="log", input_is_log=True, apply="recur")
+    o2 = fs1.solve(_cuda(A[None]), _cuda(B[None]), itr_max=it, **kw)
+    assert_solve_parity(o2, r2, "log", "f32", tol=TOL32, check_err=False)
+    # the tol-stopped state is the fixed-iteration state at the same iteration
+    assert rel_norm(out["u"].double().cpu().numpy()[0], o2["u"].double().cpu().numpy()[0]) <= 1e-6
+    assert rel_norm(out["v"].double().cpu().numpy()[0], o2["v"].double().cpu().numpy()[0]) <= 1e-6
+
+
 def test_sep2d_cost_entry_point():
     n, m = 30, 45
     F = _field(n, m, 3, 2.0) - 9
