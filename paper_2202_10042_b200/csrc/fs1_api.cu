@@ -533,9 +533,11 @@ fs1_status fs1_plan(const fs1_desc* desc, int device, fs1_plan_t** out, size_t* 
   return plan_impl(desc, device, 0, out, workspace_bytes);
 }
 
-// test-only (not in include/fs1.h): plan with a forced kernel family
-// (kind 1 persistent, 2 streaming, 10 + i streaming instantiation i) so the parity
-// tests reach K2 at small n and the benchmarks can compare instantiations.
+// test-only (not in include/fs1.h): plan with a forced kernel family so the parity
+// tests reach every kernel at small sizes and the benchmarks can compare
+// instantiations.  kind: 1 persistent (K1); 2 streaming (K2); 10 + i streaming
+// instantiation i; 3 2D CTA-line kernel (K3); 20 + i 2D warp-line instantiation i
+// (K3w); 30 + W persistent with W warps per CTA; 100 + E persistent with chunk E.
 fs1_status fs1__plan_kind(const fs1_desc* desc, int device, int kind, fs1_plan_t** out,
                           size_t* workspace_bytes) {
   return plan_impl(desc, device, kind, out, workspace_bytes);

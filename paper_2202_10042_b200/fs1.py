@@ -40,7 +40,7 @@ class Spec:
     tol: float = 0.0
     check_interval: int = 1
     warm_start: bool = False
-    kernel: int = 0          # 0 auto; test-only overrides: 1 persistent, 2 streaming, 3 2D CTA-line (K3)
+    kernel: int = 0          # 0 auto; test-only overrides (fs1__plan_kind in fs1_api.cu)
 
     def desc(self) -> L.Desc:
         return L.Desc(ndim=self.ndim, n=self.n, m=self.m, h1=self.h1, h2=self.h2, eps=self.eps,
