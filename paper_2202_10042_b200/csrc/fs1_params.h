@@ -140,6 +140,7 @@ struct ShardParams {
   long long T0;      // global index of the first tile
   long long Ttot;    // global tiles
   int T;             // tiles of this segment
+  int TB, nblk;      // tiles per block (one CTA of the tile kernels), blocks
   int world, rank;
   double lam, h;
   double lvd[5];       // lambda^{8 2^k}

@@ -33,7 +33,8 @@ void er_pow_l(long double c, long double L, double* m, int* e) {
 // workspace layout of one rank
 struct Ws {
   size_t Am, Bm, Pm, Q0, Q1, AX, BX, PX, QX0, QX1, tzA, tzB;
-  size_t Fm[2], Bmt[2], Fe[2], Be[2];
+  size_t Fm[2], Bmt[2], Fe[2], Be[2];     // tile totals / in-block carries, two sets
+  size_t BFm[2], BBm[2], BFe[2], BBe[2];  // block totals / block carries, two sets
   size_t Jm, Je, part, parte, flag, total;
 };
 Ws ws_layout(long long T, int grid) {
@@ -45,6 +46,10 @@ Ws ws_layout(long long T, int grid) {
   w.tzA = o; o += al256((size_t)T); w.tzB = o; o += al256((size_t)T);
   for (int k = 0; k < 2; ++k) {
     w.Fm[k] = o; o += td; w.Bmt[k] = o; o += td; w.Fe[k] = o; o += ti; w.Be[k] = o; o += ti;
+  }
+  const size_t bd = al256((size_t)grid * 8), bi = al256((size_t)grid * 4);
+  for (int k = 0; k < 2; ++k) {
+    w.BFm[k] = o; o += bd; w.BBm[k] = o; o += bd; w.BFe[k] = o; o += bi; w.BBe[k] = o; o += bi;
   }
   w.Jm = o; o += 4 * td; w.Je = o; o += 4 * ti;
   w.part = o; o += al256((size_t)grid * 8);
@@ -65,6 +70,15 @@ struct fs1_shard_s {
 };
 
 template <class T> static T* at(void* ws, size_t off) { return reinterpret_cast<T*>((char*)ws + off); }
+
+static shd::BlockIO block_io(const Ws& w, void* ws, int set) {
+  shd::BlockIO b;
+  b.Fm = at<double>(ws, w.Fm[set]); b.Fe = at<int>(ws, w.Fe[set]);
+  b.Bm = at<double>(ws, w.Bmt[set]); b.Be = at<int>(ws, w.Be[set]);
+  b.BFm = at<double>(ws, w.BFm[set]); b.BFe = at<int>(ws, w.BFe[set]);
+  b.BBm = at<double>(ws, w.BBm[set]); b.BBe = at<int>(ws, w.BBe[set]);
+  return b;
+}
 
 extern "C" {
 
@@ -107,7 +121,11 @@ fs1_status fs1_shard_plan(const fs1_desc* desc, int world, int rank, int device,
   }
   for (int l = 0; l < 32; ++l) P.lanepow[l] = (double)expl(-C * (long double)(8 * l));
   for (int j = 0; j < 40; ++j) er_pow_l(C, (long double)shd::TILE * ldexpl(1.0L, j), &P.t2m[j], &P.t2e[j]);
-  s->grid = (int)std::min<long long>((long long)sms * 4, std::max<long long>(1, (P.T + shd::NW - 1) / shd::NW));
+  // blocks of TB tiles, one CTA each (about 4 per SM): the tile kernels' work units and
+  // the first level of the two-level tile scan
+  P.TB = std::max(shd::NW, (int)((P.T + 4LL * sms - 1) / (4LL * sms)));
+  P.nblk = (P.T + P.TB - 1) / P.TB;
+  s->grid = P.nblk;
   s->w = ws_layout(P.T, s->grid);
   if (workspace_bytes) *workspace_bytes = s->w.total;
   if (seg_lo) *seg_lo = P.lo;
@@ -135,8 +153,9 @@ fs1_status fs1_shard_init(const fs1_shard_t* s, const void* a_seg, const void* b
                                at<int>(ws, w.Be[0]));
   shd::k_load<<<g, b, 0, st>>>(P, nullptr, 2, init, at<double>(ws, w.Q0), at<int>(ws, w.QX0), nullptr, nullptr,
                                nullptr, nullptr, nullptr);
-  shd::k_scan<<<1, shd::SCAN_NT, 0, st>>>(P, at<double>(ws, w.Fm[0]), at<int>(ws, w.Fe[0]),
-                                          at<double>(ws, w.Bmt[0]), at<int>(ws, w.Be[0]), tot4);
+  const shd::BlockIO b0 = block_io(w, ws, 0);
+  shd::k_block_scan<<<s->grid, 32 * shd::NW, 0, st>>>(P, b0);
+  shd::k_scan_blocks<<<1, shd::SCAN_NT, 0, st>>>(P, b0, tot4);
   return cudaGetLastError() == cudaSuccess ? FS1_OK : FS1_ERR_CUDA;
 }
 
@@ -154,10 +173,10 @@ fs1_status fs1_shard_half(const fs1_shard_t* s, int which, int hs, int check, in
   const size_t Qoff[2] = {w.Q0, w.Q1}, QXoff[2] = {w.QX0, w.QX1};
   shd::HalfIO io;
   memset(&io, 0, sizeof(io));
-  io.CFm = at<double>(ws, w.Fm[si]); io.CFe = at<int>(ws, w.Fe[si]);
-  io.CBm = at<double>(ws, w.Bmt[si]); io.CBe = at<int>(ws, w.Be[si]);
-  io.FAm = at<double>(ws, w.Fm[so]); io.FAe = at<int>(ws, w.Fe[so]);
-  io.BAm = at<double>(ws, w.Bmt[so]); io.BAe = at<int>(ws, w.Be[so]);
+  const shd::BlockIO bx = block_io(w, ws, si);
+  io.CFm = bx.Fm; io.CFe = bx.Fe; io.CBm = bx.Bm; io.CBe = bx.Be;
+  io.BCFm = bx.BFm; io.BCFe = bx.BFe; io.BCBm = bx.BBm; io.BCBe = bx.BBe;
+  io.yb = block_io(w, ws, so);
   io.allT = all_tot;
   io.part = at<double>(ws, w.part);
   io.flag = at<int>(ws, w.flag);
@@ -177,8 +196,7 @@ fs1_status fs1_shard_half(const fs1_shard_t* s, int which, int hs, int check, in
   if (check && write) shd::k_half<true, true><<<g, b, 0, st>>>(P, io);
   else if (check) shd::k_half<true, false><<<g, b, 0, st>>>(P, io);
   else if (write) shd::k_half<false, true><<<g, b, 0, st>>>(P, io);
-  if (write)
-    shd::k_scan<<<1, shd::SCAN_NT, 0, st>>>(P, io.FAm, io.FAe, io.BAm, io.BAe, tot4);
+  if (write) shd::k_scan_blocks<<<1, shd::SCAN_NT, 0, st>>>(P, io.yb, tot4);
   if (check) shd::k_reduce<<<1, 32, 0, st>>>(io.part, s->grid, io.flag, errflag);
   return cudaGetLastError() == cudaSuccess ? FS1_OK : FS1_ERR_CUDA;
 }

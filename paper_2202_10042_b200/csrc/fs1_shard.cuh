@@ -166,19 +166,30 @@ __global__ void __launch_bounds__(32 * NW) k_load(const ShardParams P, const dou
   }
 }
 
-// ------------------------------------------------------------------ k_scan
-// One CTA: exclusive local tile carries CF_i = sum_{i'<i} lam^{256(i-1-i')} F_i',
-// CB_i = sum_{i'>i} lam^{256(i'-i-1)} B_i' (in place over the tile totals) and the
-// segment totals {F at the end, B at the start} -> tot[0..3] (m, e as doubles).
-__global__ void __launch_bounds__(SCAN_NT) k_scan(const ShardParams P, double* Fm, int* Fe, double* Bm, int* Be,
-                                                  double* tot) {
-  __shared__ double wFm[32], wGm[32];
-  __shared__ int wFe[32], wGe[32], wFs[32], wGs[32];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = SCAN_NT / 32;
-  const int T = P.T;
-  const int q = (T + SCAN_NT - 1) / SCAN_NT;
-  const int i0 = min(T, tid * q), i1 = min(T, i0 + q);
-  const ER<double> L1{P.t2m[0], P.t2e[0]};
+// ------------------------------------------------------------------ scans
+// lambda^{256 stride k} for stride = 1 (tiles: host tables) or any stride (blocks)
+__device__ __forceinline__ ER<double> pow_span(const ShardParams& P, long long stride, long long k) {
+  return powt(P, stride * k);
+}
+
+// One CTA (NTH threads): exclusive local carries over n elements in place,
+//   CF_i = sum_{i'<i} lam^{256 s (i-1-i')} F_i',  CB_i = sum_{i'>i} lam^{256 s (i'-i-1)} B_i'
+// (s = tiles per element: 1 for tiles, TB for blocks), and the totals {F at the end,
+// B at the start}.  Only the last element may be shorter (s_last tiles): no carry into
+// an element crosses it, only the forward total does (and the backward total when
+// n = 1), so the warp / CTA combines use the uniform span and the per-element steps
+// the element's own.
+template <int NTH>
+__device__ __forceinline__ void cta_scan(const ShardParams& P, int n, long long s, long long s_last, double* Fm,
+                                         int* Fe, double* Bm, int* Be, ER<double>& totF, ER<double>& totB) {
+  __shared__ double wFm[NTH / 32], wGm[NTH / 32];
+  __shared__ int wFe[NTH / 32], wGe[NTH / 32], wFs[NTH / 32], wGs[NTH / 32];
+  __shared__ double tm[2];
+  __shared__ int te[2];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = NTH / 32;
+  const int q = (n + NTH - 1) / NTH;
+  const int i0 = min(n, tid * q), i1 = min(n, i0 + q);
+  const ER<double> L1 = pow_span(P, s, 1), Ll = pow_span(P, s_last, 1);
   ER<double> f = er_zero<double>(), g = er_zero<double>();
   for (int i = i0; i < i1; ++i) f = er_fma(f, L1, ER<double>{Fm[i], Fe[i]});
   for (int i = i1 - 1; i >= i0; --i) g = er_fma(g, L1, ER<double>{Bm[i], Be[i]});
@@ -190,8 +201,8 @@ __global__ void __launch_bounds__(SCAN_NT) k_scan(const ShardParams P, double* F
     const int us = __shfl_up_sync(FULL, sF, d);
     const ER<double> dg = shfl_down_er(G, d);
     const int ds = __shfl_down_sync(FULL, sG, d);
-    if (lane >= d) { F = er_fma(uf, powt(P, sF), F); sF += us; }
-    if (lane + d < 32) { G = er_fma(dg, powt(P, sG), G); sG += ds; }
+    if (lane >= d) { F = er_fma(uf, pow_span(P, s, sF), F); sF += us; }
+    if (lane + d < 32) { G = er_fma(dg, pow_span(P, s, sG), G); sG += ds; }
   }
   ER<double> eF = shfl_up_er(F, 1);
   int esF = __shfl_up_sync(FULL, sF, 1);
@@ -203,22 +214,59 @@ __global__ void __launch_bounds__(SCAN_NT) k_scan(const ShardParams P, double* F
   if (lane == 0) { wGm[warp] = G.m; wGe[warp] = G.e; wGs[warp] = sG; }
   __syncthreads();
   ER<double> cw = er_zero<double>(), cg = er_zero<double>();
-  for (int w = 0; w < warp; ++w) cw = er_fma(cw, powt(P, wFs[w]), ER<double>{wFm[w], wFe[w]});
-  for (int w = nwarp - 1; w > warp; --w) cg = er_fma(cg, powt(P, wGs[w]), ER<double>{wGm[w], wGe[w]});
-  ER<double> cf = er_fma(cw, powt(P, esF), eF);
-  ER<double> cb = er_fma(cg, powt(P, esG), eG);
+  for (int w = 0; w < warp; ++w) cw = er_fma(cw, pow_span(P, s, wFs[w]), ER<double>{wFm[w], wFe[w]});
+  for (int w = nwarp - 1; w > warp; --w) cg = er_fma(cg, pow_span(P, s, wGs[w]), ER<double>{wGm[w], wGe[w]});
+  ER<double> cf = er_fma(cw, pow_span(P, s, esF), eF);
+  ER<double> cb = er_fma(cg, pow_span(P, s, esG), eG);
   for (int i = i0; i < i1; ++i) {
     const ER<double> t{Fm[i], Fe[i]};
     Fm[i] = cf.m; Fe[i] = cf.e;
-    cf = er_fma(cf, L1, t);
+    cf = er_fma(cf, (i == n - 1) ? Ll : L1, t);
   }
   for (int i = i1 - 1; i >= i0; --i) {
     const ER<double> t{Bm[i], Be[i]};
     Bm[i] = cb.m; Be[i] = cb.e;
-    cb = er_fma(cb, L1, t);
+    cb = er_fma(cb, (i == n - 1) ? Ll : L1, t);
   }
-  if (tid == SCAN_NT - 1) { tot[0] = cf.m; tot[1] = (double)cf.e; }
-  if (tid == 0) { tot[2] = cb.m; tot[3] = (double)cb.e; }
+  if (n == 0) {
+    if (tid == 0) { tm[0] = tm[1] = 0.0; te[0] = te[1] = ZE; }
+  } else {
+    if (i0 < n && i1 == n) { tm[0] = cf.m; te[0] = cf.e; }  // owner of the last element
+    if (tid == 0) { tm[1] = cb.m; te[1] = cb.e; }
+  }
+  __syncthreads();
+  totF = ER<double>{tm[0], te[0]};
+  totB = ER<double>{tm[1], te[1]};
+  __syncthreads();
+}
+
+// Block level: CTA b scans its block's tile totals in place (in-block exclusive
+// carries) and writes the block totals {F end, B start} to BF/BB[b].
+struct BlockIO {
+  double *Fm, *Bm;   // tile totals -> in-block exclusive carries
+  int *Fe, *Be;
+  double *BFm, *BBm; // [nblocks] block totals -> block carries (k_scan_blocks)
+  int *BFe, *BBe;
+};
+__device__ __forceinline__ void block_totals(const ShardParams& P, const BlockIO& bi) {
+  const int b = blockIdx.x;
+  const int t0 = b * P.TB, n = min(P.T, t0 + P.TB) - t0;
+  ER<double> tF, tB;
+  cta_scan<32 * NW>(P, n, 1, 1, bi.Fm + t0, bi.Fe + t0, bi.Bm + t0, bi.Be + t0, tF, tB);
+  if (threadIdx.x == 0) {
+    bi.BFm[b] = tF.m; bi.BFe[b] = tF.e;
+    bi.BBm[b] = tB.m; bi.BBe[b] = tB.e;
+  }
+}
+__global__ void __launch_bounds__(32 * NW) k_block_scan(const ShardParams P, const BlockIO bi) { block_totals(P, bi); }
+
+// One CTA over the blocks: exclusive block carries in place and the rank's totals
+// {F at the segment end, B at its start} -> tot[0..3] (m, e as doubles).
+__global__ void __launch_bounds__(SCAN_NT) k_scan_blocks(const ShardParams P, const BlockIO bi, double* tot) {
+  ER<double> tF, tB;
+  cta_scan<SCAN_NT>(P, P.nblk, P.TB, P.T - (long long)(P.nblk - 1) * P.TB, bi.BFm, bi.BFe, bi.BBm, bi.BBe, tF,
+                    tB);
+  if (threadIdx.x == 0) { tot[0] = tF.m; tot[1] = (double)tF.e; tot[2] = tB.m; tot[3] = (double)tB.e; }
 }
 
 // Decay of the other ranks' totals to this segment: lane k of warp 0 takes rank k
@@ -246,12 +294,14 @@ __device__ __forceinline__ void ext_carries(const ShardParams& P, const double* 
 // ------------------------------------------------------------------ k_half
 struct HalfIO {
   const double* xm; const int* xX;                 // x (consumed): mantissas, tile exponents
-  const double* CFm; const int* CFe;               // x's local exclusive tile carries
+  const double* CFm; const int* CFe;               // x's in-block exclusive tile carries
   const double* CBm; const int* CBe;
+  const double* BCFm; const int* BCFe;             // x's block carries (k_scan_blocks)
+  const double* BCBm; const int* BCBe;
+  BlockIO yb;                                      // y's tile totals -> in-block carries, block totals
   const double* tm; const int* tX; const unsigned char* tz;  // target a or b
   const double* om; const int* oX;                 // psi^(l) (check)
   double* ym; int* yX;                             // y (produced)
-  double* FAm; int* FAe; double* BAm; int* BAe;    // y's tile totals (for the next k_scan)
   const double* allT;                              // [world][4] totals of x
   double* part;                                    // [gridDim] error partials
   int* flag;                                       // [2]: non-finite seen, first iteration
@@ -275,20 +325,24 @@ __global__ void __launch_bounds__(32 * NW) k_half(const ShardParams P, const Hal
   const double lp = P.lanepow[lane], rp = P.lanepow[31 - lane];
   double errw = 0.0;
   int bad = 0;
-  const long long wg = (long long)blockIdx.x * NW + warp;
-  const long long nwarps = (long long)gridDim.x * NW;
-  for (long long i = wg; i < P.T; i += nwarps) {
+  // this CTA's block of tiles [t0, t1): the carries entering it (block carries of this
+  // rank + the other ranks' totals decayed over the tiles before / after the block)
+  const int blk = blockIdx.x;
+  const int t0 = blk * P.TB, t1 = min(P.T, t0 + P.TB);
+  const ER<double> CFb = er_fma(powt(P, t0), EF, ER<double>{io.BCFm[blk], io.BCFe[blk]});
+  const ER<double> CBb = er_fma(powt(P, P.T - t1), EB, ER<double>{io.BCBm[blk], io.BCBe[blk]});
+  for (int i = t0 + warp; i < t1; i += NW) {
     // full carries of tile i relative to its reference exponent R
-    const ER<double> CF = er_fma(powt(P, i), EF, ER<double>{io.CFm[i], io.CFe[i]});
-    const ER<double> CB = er_fma(powt(P, P.T - 1 - i), EB, ER<double>{io.CBm[i], io.CBe[i]});
+    const ER<double> CF = er_fma(powt(P, i - t0), CFb, ER<double>{io.CFm[i], io.CFe[i]});
+    const ER<double> CB = er_fma(powt(P, t1 - 1 - i), CBb, ER<double>{io.CBm[i], io.CBe[i]});
     const int X = io.xX[i];
     int R = X;
     if (X == ZE || CF.e - X > LIM || CB.e - X > LIM) R = max(CF.e, CB.e);
     if (R == ZE) R = 0;
     const double cfr = er_rel(CF, R), cbr = er_rel(CB, R);
     double xv[E], tv[E];
-    ld_tile(io.xm + i * TILE, lane, xv);
-    ld_tile(io.tm + i * TILE, lane, tv);
+    ld_tile(io.xm + (size_t)i * TILE, lane, xv);
+    ld_tile(io.tm + (size_t)i * TILE, lane, tv);
     if (X != R) {
       const double sc = pow2d(max(X - R, -1100));
 #pragma unroll
@@ -306,7 +360,7 @@ __global__ void __launch_bounds__(32 * NW) k_half(const ShardParams P, const Hal
     double ov[E];
     double sce = 0.0;
     if (CHECK) {
-      ld_tile(io.om + i * TILE, lane, ov);
+      ld_tile(io.om + (size_t)i * TILE, lane, ov);
       sce = pow2d(min(max(io.oX[i] + R - io.tX[i], -1100), 1000));
     }
     const int Xt = io.tX[i];
@@ -344,8 +398,8 @@ __global__ void __launch_bounds__(32 * NW) k_half(const ShardParams P, const Hal
       double FiY, GiY;
       lane_scan(P, tv, FiY, GiY);
       if (!isfinite(FiY + GiY)) bad = 1;
-      put_tot(P, lane, FiY, GiY, Y, (int)i, io.FAm, io.FAe, io.BAm, io.BAe);
-      st_tile(io.ym + i * TILE, lane, tv);
+      put_tot(P, lane, FiY, GiY, Y, i, io.yb.Fm, io.yb.Fe, io.yb.Bm, io.yb.Be);
+      st_tile(io.ym + (size_t)i * TILE, lane, tv);
       if (lane == 0) io.yX[i] = Y;
     }
   }
@@ -357,6 +411,10 @@ __global__ void __launch_bounds__(32 * NW) k_half(const ShardParams P, const Hal
       for (int w = 0; w < NW; ++w) s += werr[w];
       io.part[blockIdx.x] = s;
     }
+  }
+  if (WRITE) {  // y's tiles of this block: in-block exclusive carries and block totals
+    __syncthreads();
+    block_totals(P, io.yb);
   }
   if (__any_sync(FULL, bad) && lane == 0) {
     atomicOr(&io.flag[0], 1);

@@ -80,6 +80,19 @@ def test_segments_linear_weights_recursion_oracle():
     _parity(o, ref)
 
 
+@pytest.mark.parametrize("world", [2, 3])
+def test_segments_short_last_block(world):
+    """Segments of 21 / 14 tiles split into blocks of 8 (two-level tile scan): the short
+    last block enters the rank totals the other ranks decay over their segments."""
+    n = 42 * 256
+    a, b = _pair(n, 17)
+    kw = dict(h=1 / n, eps=1e-3, itr_max=20, input_is_log=True)
+    o = shard.solve_segments(_cuda(a), _cuda(b), world, **kw)
+    ref = sinkhorn.solve(a, b, n=n, h1=1 / n, eps=1e-3, itr_max=20, domain="log", input_is_log=True,
+                         apply="recur")
+    _parity(o, ref)
+
+
 def test_segments_independent_of_world_size():
     """Every world size gives the same state to rounding (the split only moves where
     the exchanged totals enter the recursions)."""
