@@ -154,6 +154,27 @@ def test_sep2d_check_interval(ci):
     assert rel_norm(out["v"].double().cpu().numpy()[0], o2["v"].double().cpu().numpy()[0]) <= 1e-6
 
 
+def test_sep2d_batch_of_problems():
+    """Several 2D problems in one fs1_solve (one launch each, shared workspace): each equals
+    its own single-problem solve, and the apply / cost entry points handle batches too."""
+    n, m = 72, 56
+    pairs = [_pair2d(n, m, 30 + k) for k in range(3)]
+    A = np.stack([p[0] for p in pairs]).astype(np.float32)
+    B = np.stack([p[1] for p in pairs]).astype(np.float32)
+    kw = dict(h=1 / n, h2=1 / m, eps=0.01, itr_max=25, domain="log", input_is_log=True, shape=(n, m))
+    out = fs1.solve(_cuda(A), _cuda(B), **kw)
+    for k in range(3):
+        one = fs1.solve(_cuda(A[k:k + 1]), _cuda(B[k:k + 1]), **kw)
+        assert np.array_equal(out["u"][k].cpu().numpy(), one["u"][0].cpu().numpy())
+        assert np.array_equal(out["v"][k].cpu().numpy(), one["v"][0].cpu().numpy())
+        assert out["cost"][k].item() == one["cost"].item()
+    cb = fs1.cost(out["u"], out["v"], h=1 / n, h2=1 / m, eps=0.01, domain="log", shape=(n, m))
+    assert np.allclose(cb.cpu().numpy(), out["cost"].cpu().numpy(), rtol=1e-5)
+    ref = sinkhorn.solve(A.astype(np.float64), B.astype(np.float64), n=n, m=m, h1=1 / n, h2=1 / m, eps=0.01,
+                         itr_max=25, domain="log", input_is_log=True, apply="recur")
+    assert_solve_parity(out, ref, "log", "f32", tol=TOL32)
+
+
 def test_sep2d_cost_entry_point():
     n, m = 30, 45
     F = _field(n, m, 3, 2.0) - 9
