@@ -12,6 +12,7 @@
 //      multipliers lambda^{E 2^k}; CTA: warp totals through shared memory;
 //   3. per thread: the two recursions again from the exact carries, fused with
 //      the update psi = b ./ (p + q) (q_k = lam t_{k+1}).
+// Steps 1 and 3 run as NCH interleaved sub-chains per thread chunk (ILP).
 // The marginal error and the return-line cost (PAPER.md:163,
 // O(N) Jordan-block scan, R7) are fused into the same passes.
 //

@@ -17,21 +17,24 @@
 // hold -inf.
 //
 // Passes.  Two fused passes per iteration, each one grid barrier:
-//   R (lines = rows i, along axis 2):  Y = log K2 e^{Z1_i}  (Z1 = K1 phi, transposed)
-//       [check: err += sum |e^{G_old + Y} - b|]
-//       G_i = log b_i - Y                        (psi update)
-//       Z2 = log K2 e^{G_i}, written transposed  (first pass of the phi half-step)
-//   C (lines = columns j, along axis 1):  F_j = log a_j - log K1 e^{Z2_j}
-//       Z1 = log K1 e^{F_j}, written transposed  (first pass of the next psi half-step)
+//   R (lines = rows i, along axis 2):  k = K2 e^{Z1_i}  (Z1 = log K1 phi, transposed)
+//       [check: err += sum |e^{G_old + log k} - b|]
+//       psi_i = b_i / k as linear mantissas          (psi update)
+//       [G_i = log b_i - log k stored only where a loop top may stop on it]
+//       Z2 = log K2 psi_i, written transposed        (first pass of the phi half-step)
+//   C (lines = columns j, along axis 1):  phi_j = a_j / K1 e^{Z2_j}
+//       Z1 = log K1 phi_j, written transposed        (first pass of the next psi half-step)
 // The fused second apply reuses the freshly updated line from registers, so each
 // point is read and written twice per iteration instead of four times, and there
 // are 2 grid barriers per iteration instead of 4.  Transposed writes go through a
 // per-CTA shared stage of W = 8 lines so that each position leaves as one sector.
 //
-// Arithmetic (the chunk-relative log scheme): a lane converts its
-// chunk once per apply, m_e = 2^(X_e log2 e - oe) with oe = floor(max X log2 e)
-// (one MUFU ex2 per point), runs the recursions linearly in fp32 relative to 2^oe,
-// and leaves through one MUFU lg2 per point.  Chunk totals cross lanes as
+// Arithmetic (the chunk-relative log scheme): the first apply of a
+// pass converts the lane's chunk, m_e = 2^(X_e log2 e - oe) with oe = floor(max X
+// log2 e) (one MUFU ex2 per point), the recursions run linearly in fp32 relative to
+// 2^oe, the update is one MUFU rcp per point against the target's mantissas, the
+// second apply runs on those linear values directly, and the pass leaves through one
+// MUFU lg2 per point (3 MUFU per point per pass).  Chunk totals cross lanes as
 // extended-range fp32 numbers (mantissa in [1,2), int exponent) in a 5-level warp
 // shuffle scan with multipliers lambda^{E 2^k} formed on the host (Remark 3.3).
 // In-lane work runs as 2-4 independent chains (ILP): the chunk halves get their own

@@ -8,8 +8,9 @@
 // shared memory; only 2 extended-range words per CTA cross the grid per
 // half-step.  One half-step x -> y = tgt ./ (K x) (Alg. 1 lines 3-7 / 8-12):
 //
-//  [A] after the grid barrier: warp 0 folds the other CTAs' range totals of x
-//      into this range's external forward/backward carries; every tile's full
+//  [A] after the grid barrier: the other CTAs' range totals of x, one per thread,
+//      decayed and summed (fixed order) into this range's external forward /
+//      backward carries; every tile's full
 //      carries = local exclusive carries (made by this CTA when it produced x)
 //      + lambda^{256 i} x external carry;
 //  [B] each warp streams its tiles: 1D TMA bulk copies (cp.async.bulk, mbarrier
