@@ -55,7 +55,9 @@ fs1_status fs1_shard_init(const fs1_shard_t* s, const void* a_seg, const void* b
  *   check   : also compute this rank's part of the marginal error
  *             sum_i |psi_i (K^T phi)_i - b_i| with psi = buffer psi_in.
  *   write   : produce y (0 only for the final check at l = itr_max).
- *   l1      : iteration recorded if y becomes non-finite (l + 1).
+ *   l1      : iteration recorded if y becomes non-finite (l + 1); -1 = use the
+ *             plan's device counter (starts at 1, advanced after every phi half-step
+ *             called with -1), for replays of a captured CUDA graph.
  *   psi_in, psi_out : psi buffers (0/1): which=0 reads psi_in (check) and writes
  *             psi_out; which=1 reads psi_in.
  *   all_tot : device [world][4] totals of x from every rank (the all-gather).

@@ -197,6 +197,7 @@ fs1_status fs1_shard_half(const fs1_shard_t* s, int which, int hs, int check, in
   else if (check) shd::k_half<true, false><<<g, b, 0, st>>>(P, io);
   else if (write) shd::k_half<false, true><<<g, b, 0, st>>>(P, io);
   if (write) shd::k_scan_blocks<<<1, shd::SCAN_NT, 0, st>>>(P, io.yb, tot4);
+  if (l1 < 0 && which == 1) shd::k_tick<<<1, 1, 0, st>>>(io.flag);  // device counter mode
   if (check) shd::k_reduce<<<1, 32, 0, st>>>(io.part, s->grid, io.flag, errflag);
   return cudaGetLastError() == cudaSuccess ? FS1_OK : FS1_ERR_CUDA;
 }

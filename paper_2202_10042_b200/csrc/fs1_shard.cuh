@@ -49,12 +49,14 @@ __device__ __forceinline__ ER<double> er_fma(ER<double> a, ER<double> b, ER<doub
   return er_add(er_mul(a, b), d);
 }
 
-// Natural-order tile access: lane l holds points [8l, 8l+8) of the tile.
+// Natural-order tile access: lane l holds points [8l, 8l+8) of the tile.  Loads go
+// through L1 (each lane's 64-byte chunk is two sectors read by four 16-byte loads:
+// L1 keeps the second load of each sector from going to L2 again).
 __device__ __forceinline__ void ld_tile(const double* g, int lane, double (&v)[E]) {
   const double2* p = reinterpret_cast<const double2*>(g + lane * E);
 #pragma unroll
   for (int j = 0; j < E / 2; ++j) {
-    const double2 t = __ldcg(p + j);
+    const double2 t = __ldca(p + j);
     v[2 * j] = t.x;
     v[2 * j + 1] = t.y;
   }
@@ -167,43 +169,60 @@ __global__ void __launch_bounds__(32 * NW) k_load(const ShardParams P, const dou
 }
 
 // ------------------------------------------------------------------ scans
-// lambda^{256 stride k} for stride = 1 (tiles: host tables) or any stride (blocks)
-__device__ __forceinline__ ER<double> pow_span(const ShardParams& P, long long stride, long long k) {
-  return powt(P, stride * k);
+// Powers of the per-element multiplier L = lambda^{256 s}: table pw[j] = L^{2^j}
+// (j < 32), powers by binary decomposition.
+struct PowTab {
+  const double* m;
+  const int* e;
+};
+__device__ __forceinline__ ER<double> tpow(PowTab t, long long k) {
+  ER<double> r{1.0, 0};
+  for (int j = 0; j < 32 && k; ++j, k >>= 1)
+    if (k & 1) r = er_mul(r, ER<double>{t.m[j], t.e[j]});
+  return r;
 }
 
-// One CTA (NTH threads): exclusive local carries over n elements in place,
-//   CF_i = sum_{i'<i} lam^{256 s (i-1-i')} F_i',  CB_i = sum_{i'>i} lam^{256 s (i'-i-1)} B_i'
-// (s = tiles per element: 1 for tiles, TB for blocks), and the totals {F at the end,
-// B at the start}.  Only the last element may be shorter (s_last tiles): no carry into
-// an element crosses it, only the forward total does (and the backward total when
-// n = 1), so the warp / CTA combines use the uniform span and the per-element steps
-// the element's own.
-template <int NTH>
-__device__ __forceinline__ void cta_scan(const ShardParams& P, int n, long long s, long long s_last, double* Fm,
-                                         int* Fe, double* Bm, int* Be, ER<double>& totF, ER<double>& totB) {
-  __shared__ double wFm[NTH / 32], wGm[NTH / 32];
-  __shared__ int wFe[NTH / 32], wGe[NTH / 32], wFs[NTH / 32], wGs[NTH / 32];
-  __shared__ double tm[2];
-  __shared__ int te[2];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = NTH / 32;
-  const int q = (n + NTH - 1) / NTH;
-  const int i0 = min(n, tid * q), i1 = min(n, i0 + q);
-  const ER<double> L1 = pow_span(P, s, 1), Ll = pow_span(P, s_last, 1);
-  ER<double> f = er_zero<double>(), g = er_zero<double>();
-  for (int i = i0; i < i1; ++i) f = er_fma(f, L1, ER<double>{Fm[i], Fe[i]});
-  for (int i = i1 - 1; i >= i0; --i) g = er_fma(g, L1, ER<double>{Bm[i], Be[i]});
-  int sF = i1 - i0, sG = i1 - i0;
-  ER<double> F = f, G = g;
+// Warp-level inclusive scans of (F, span) forward and (G, span) backward with
+// multipliers tpow(span) (Hillis-Steele, 5 levels).
+__device__ __forceinline__ void warp_pair_scan(PowTab t, int lane, ER<double>& F, int& sF, ER<double>& G,
+                                               int& sG) {
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
     const ER<double> uf = shfl_up_er(F, d);
     const int us = __shfl_up_sync(FULL, sF, d);
     const ER<double> dg = shfl_down_er(G, d);
     const int ds = __shfl_down_sync(FULL, sG, d);
-    if (lane >= d) { F = er_fma(uf, pow_span(P, s, sF), F); sF += us; }
-    if (lane + d < 32) { G = er_fma(dg, pow_span(P, s, sG), G); sG += ds; }
+    if (lane >= d) { F = er_fma(uf, tpow(t, sF), F); sF += us; }
+    if (lane + d < 32) { G = er_fma(dg, tpow(t, sG), G); sG += ds; }
   }
+}
+
+// One CTA (NTH threads): exclusive local carries over n elements in place,
+//   CF_i = sum_{i'<i} L^{i-1-i'} F_i',  CB_i = sum_{i'>i} L^{i'-i-1} B_i'
+// (L = lambda^{256 s}, s = tiles per element: 1 for tiles, TB for blocks), and the
+// totals {F at the end, B at the start}.  Only the last element may be shorter
+// (s_last tiles): no carry into an element crosses it, only the forward total does
+// (and the backward total when n = 1), so the lane / warp combines use the uniform
+// span and the per-element steps the element's own.  The per-warp totals are scanned
+// by warp 0 (5 levels), not folded serially.
+template <int NTH>
+__device__ __forceinline__ void cta_scan(PowTab t, ER<double> Ll, int n, double* Fm, int* Fe, double* Bm, int* Be,
+                                         ER<double>& totF, ER<double>& totB) {
+  constexpr int NWP = NTH / 32;
+  __shared__ double wFm[NWP], wGm[NWP];
+  __shared__ int wFe[NWP], wGe[NWP], wFs[NWP], wGs[NWP];
+  __shared__ double tm[2];
+  __shared__ int te[2];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int q = (n + NTH - 1) / NTH;
+  const int i0 = min(n, tid * q), i1 = min(n, i0 + q);
+  const ER<double> L1{t.m[0], t.e[0]};
+  ER<double> f = er_zero<double>(), g = er_zero<double>();
+  for (int i = i0; i < i1; ++i) f = er_fma(f, L1, ER<double>{Fm[i], Fe[i]});
+  for (int i = i1 - 1; i >= i0; --i) g = er_fma(g, L1, ER<double>{Bm[i], Be[i]});
+  int sF = i1 - i0, sG = i1 - i0;
+  ER<double> F = f, G = g;
+  warp_pair_scan(t, lane, F, sF, G, sG);
   ER<double> eF = shfl_up_er(F, 1);
   int esF = __shfl_up_sync(FULL, sF, 1);
   ER<double> eG = shfl_down_er(G, 1);
@@ -213,20 +232,35 @@ __device__ __forceinline__ void cta_scan(const ShardParams& P, int n, long long 
   if (lane == 31) { wFm[warp] = F.m; wFe[warp] = F.e; wFs[warp] = sF; }
   if (lane == 0) { wGm[warp] = G.m; wGe[warp] = G.e; wGs[warp] = sG; }
   __syncthreads();
-  ER<double> cw = er_zero<double>(), cg = er_zero<double>();
-  for (int w = 0; w < warp; ++w) cw = er_fma(cw, pow_span(P, s, wFs[w]), ER<double>{wFm[w], wFe[w]});
-  for (int w = nwarp - 1; w > warp; --w) cg = er_fma(cg, pow_span(P, s, wGs[w]), ER<double>{wGm[w], wGe[w]});
-  ER<double> cf = er_fma(cw, pow_span(P, s, esF), eF);
-  ER<double> cb = er_fma(cg, pow_span(P, s, esG), eG);
+  if (warp == 0) {  // exclusive scan of the warp totals
+    ER<double> A = er_zero<double>(), C = er_zero<double>();
+    int sa = 0, sc = 0;
+    if (lane < NWP) {
+      A = ER<double>{wFm[lane], wFe[lane]}; sa = wFs[lane];
+      C = ER<double>{wGm[lane], wGe[lane]}; sc = wGs[lane];
+    }
+    warp_pair_scan(t, lane, A, sa, C, sc);
+    ER<double> xa = shfl_up_er(A, 1), xc = shfl_down_er(C, 1);
+    if (lane == 0) xa = er_zero<double>();
+    if (lane == 31 || lane + 1 >= NWP) xc = er_zero<double>();
+    __syncwarp();
+    if (lane < NWP) {
+      wFm[lane] = xa.m; wFe[lane] = xa.e;
+      wGm[lane] = xc.m; wGe[lane] = xc.e;
+    }
+  }
+  __syncthreads();
+  ER<double> cf = er_fma(ER<double>{wFm[warp], wFe[warp]}, tpow(t, esF), eF);
+  ER<double> cb = er_fma(ER<double>{wGm[warp], wGe[warp]}, tpow(t, esG), eG);
   for (int i = i0; i < i1; ++i) {
-    const ER<double> t{Fm[i], Fe[i]};
+    const ER<double> v{Fm[i], Fe[i]};
     Fm[i] = cf.m; Fe[i] = cf.e;
-    cf = er_fma(cf, (i == n - 1) ? Ll : L1, t);
+    cf = er_fma(cf, (i == n - 1) ? Ll : L1, v);
   }
   for (int i = i1 - 1; i >= i0; --i) {
-    const ER<double> t{Bm[i], Be[i]};
+    const ER<double> v{Bm[i], Be[i]};
     Bm[i] = cb.m; Be[i] = cb.e;
-    cb = er_fma(cb, (i == n - 1) ? Ll : L1, t);
+    cb = er_fma(cb, (i == n - 1) ? Ll : L1, v);
   }
   if (n == 0) {
     if (tid == 0) { tm[0] = tm[1] = 0.0; te[0] = te[1] = ZE; }
@@ -252,7 +286,8 @@ __device__ __forceinline__ void block_totals(const ShardParams& P, const BlockIO
   const int b = blockIdx.x;
   const int t0 = b * P.TB, n = min(P.T, t0 + P.TB) - t0;
   ER<double> tF, tB;
-  cta_scan<32 * NW>(P, n, 1, 1, bi.Fm + t0, bi.Fe + t0, bi.Bm + t0, bi.Be + t0, tF, tB);
+  const PowTab tiles{P.t2m, P.t2e};  // lambda^{256 2^j}
+  cta_scan<32 * NW>(tiles, ER<double>{P.t2m[0], P.t2e[0]}, n, bi.Fm + t0, bi.Fe + t0, bi.Bm + t0, bi.Be + t0, tF, tB);
   if (threadIdx.x == 0) {
     bi.BFm[b] = tF.m; bi.BFe[b] = tF.e;
     bi.BBm[b] = tB.m; bi.BBe[b] = tB.e;
@@ -263,9 +298,19 @@ __global__ void __launch_bounds__(32 * NW) k_block_scan(const ShardParams P, con
 // One CTA over the blocks: exclusive block carries in place and the rank's totals
 // {F at the segment end, B at its start} -> tot[0..3] (m, e as doubles).
 __global__ void __launch_bounds__(SCAN_NT) k_scan_blocks(const ShardParams P, const BlockIO bi, double* tot) {
+  __shared__ double pm[32];
+  __shared__ int pe[32];
+  if (threadIdx.x == 0) {  // (lambda^{256 TB})^{2^j} by repeated squaring
+    ER<double> x = powt(P, P.TB);
+    for (int j = 0; j < 32; ++j) {
+      pm[j] = x.m; pe[j] = x.e;
+      x = er_mul(x, x);
+    }
+  }
+  __syncthreads();
   ER<double> tF, tB;
-  cta_scan<SCAN_NT>(P, P.nblk, P.TB, P.T - (long long)(P.nblk - 1) * P.TB, bi.BFm, bi.BFe, bi.BBm, bi.BBe, tF,
-                    tB);
+  const ER<double> Ll = powt(P, P.T - (long long)(P.nblk - 1) * P.TB);
+  cta_scan<SCAN_NT>(PowTab{pm, pe}, Ll, P.nblk, bi.BFm, bi.BFe, bi.BBm, bi.BBe, tF, tB);
   if (threadIdx.x == 0) { tot[0] = tF.m; tot[1] = (double)tF.e; tot[2] = tB.m; tot[3] = (double)tB.e; }
 }
 
@@ -305,7 +350,8 @@ struct HalfIO {
   const double* allT;                              // [world][4] totals of x
   double* part;                                    // [gridDim] error partials
   int* flag;                                       // [2]: non-finite seen, first iteration
-  int l;                                           // iteration (for the non-finite record)
+  int l;                                           // iteration (for the non-finite record);
+                                                   // < 0: read it from flag[2] (graph replays)
 };
 
 template <bool CHECK, bool WRITE>
@@ -418,14 +464,17 @@ __global__ void __launch_bounds__(32 * NW) k_half(const ShardParams P, const Hal
   }
   if (__any_sync(FULL, bad) && lane == 0) {
     atomicOr(&io.flag[0], 1);
-    atomicMin(&io.flag[1], io.l);
+    atomicMin(&io.flag[1], io.l >= 0 ? io.l : io.flag[2]);
   }
 }
 
 __global__ void k_init_flag(int* flag) {
   flag[0] = 0;
   flag[1] = 0x7fffffff;
+  flag[2] = 1;  // device iteration counter l + 1 (advanced by k_tick)
 }
+// advance the device iteration counter (one per iteration, after the phi half-step)
+__global__ void k_tick(int* flag) { flag[2] += 1; }
 
 // deterministic sum of the per-CTA partials (fixed order) -> out[0]; out[1] = the first
 // iteration whose state was non-finite (0: none)

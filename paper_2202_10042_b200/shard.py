@@ -7,6 +7,9 @@ one all-gather, then each rank runs `fs1_shard_half` on its segment.  This modul
 is marshalling and loop control only (Algorithm 1's while, with the
 readings of DESIGN.md R2-R6); every arithmetic step runs in the CUDA kernels.
 
+With tol = 0 (fixed iterations) one iteration — both half-steps of every local rank and
+both exchanges — is captured once as a CUDA graph and replayed (`_run_graph`).
+
 Two drivers share `ShardRank`:
   * `solve_sharded`    one rank per process, totals moved by torch.distributed
                        (NCCL over NVLink on the GPU box; gloo in CPU tests);
@@ -119,6 +122,41 @@ def _run(ranks, segs_a, segs_b, gather, itr_max, tol, check_interval, want_cost)
     return l, qi, flag, err
 
 
+def _run_graph(ranks, segs_a, segs_b, gather, itr_max):
+    """The fixed-iteration loop (tol = 0) with one iteration captured as a
+    CUDA graph — both half-steps of every local rank and both exchanges — and replayed:
+    no host round trip or per-kernel launch cost per half-step.  The non-finite record
+    uses the plan's device iteration counter (l1 = -1).  Same kernels, same order, same
+    results as `_run`."""
+    for r, a, b in zip(ranks, segs_a, segs_b):
+        r.init(a, b)
+
+    def iteration():
+        allT = gather([r.tot for r in ranks])
+        outs = [r.half(0, 0, False, True, -1, 0, 0, allT) for r in ranks]
+        allT2 = gather([o[0].clone() for o in outs])
+        for r in ranks:
+            r.half(1, 1, False, True, -1, 0, 0, allT2)
+
+    if itr_max >= 1:
+        iteration()                      # l = 0, eager (also warms the capture path)
+    if itr_max >= 2:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            iteration()
+        for _ in range(itr_max - 1):     # l = 1 .. itr_max - 1
+            g.replay()
+    # loop top at l = itr_max: the exit check (PAPER.md:148), psi^(l) kept in buffer 0
+    allT = gather([r.tot for r in ranks])
+    outs = [r.half(0, 0, True, False, itr_max + 1, 0, 1, allT) for r in ranks]
+    ef = gather([o[1] for o in outs]).cpu()
+    err = float(sum(ef[k, 0].item() for k in range(ef.shape[0])))
+    bad = [int(ef[k, 1].item()) for k in range(ef.shape[0]) if ef[k, 1].item() > 0]
+    if bad:
+        return min(bad), 0, 2, err
+    return itr_max, 0, 4, err
+
+
 def _finish(ranks, qi, gather, flag, want_cost, dtype_dev):
     us, vs = [], []
     all8 = gather([r.cost_totals(qi).clone() for r in ranks]) if want_cost else None
@@ -134,7 +172,7 @@ def _finish(ranks, qi, gather, flag, want_cost, dtype_dev):
 
 
 def solve_segments(a, b, world, *, h, eps, itr_max, tol=0.0, check_interval=1, input_is_log=False,
-                   want_cost=True):
+                   want_cost=True, graph=True):
     """All `world` ranks in this process on a's device (lock step); a, b: [N] fp64 CUDA.
     Returns {u, v (full F, G), iters, err, flags, cost} like fs1.solve for batch 1."""
     n = a.numel()
@@ -144,7 +182,10 @@ def solve_segments(a, b, world, *, h, eps, itr_max, tol=0.0, check_interval=1, i
     sa = [a[r.lo:r.lo + r.len].contiguous() for r in ranks]
     sb = [b[r.lo:r.lo + r.len].contiguous() for r in ranks]
     gather = lambda ts: torch.stack([t.clone() for t in ts])  # noqa: E731
-    l, qi, flag, err = _run(ranks, sa, sb, gather, itr_max, tol, check_interval, want_cost)
+    if graph and tol == 0.0:
+        l, qi, flag, err = _run_graph(ranks, sa, sb, gather, itr_max)
+    else:
+        l, qi, flag, err = _run(ranks, sa, sb, gather, itr_max, tol, check_interval, want_cost)
     ok = flag != 2
     us, vs, parts = _finish(ranks, qi, gather, flag, want_cost and ok, lambda r: a.device)
     cost = float(sum(p.item() for p in parts)) if (want_cost and ok) else float("nan")
@@ -153,7 +194,7 @@ def solve_segments(a, b, world, *, h, eps, itr_max, tol=0.0, check_interval=1, i
 
 
 def solve_sharded(a_seg, b_seg, n, *, h, eps, itr_max, tol=0.0, check_interval=1, input_is_log=False,
-                  want_cost=True, group=None):
+                  want_cost=True, group=None, graph=True):
     """This process's rank of a torch.distributed job: a_seg, b_seg are its segment
     [lo, lo+len) of the N-point problem (see `segment`).  Collectives: one all-gather of
     4 doubles per half-step, of 2 per check, of 8 for the cost, one all-reduce at exit."""
@@ -169,7 +210,10 @@ def solve_sharded(a_seg, b_seg, n, *, h, eps, itr_max, tol=0.0, check_interval=1
         (t,) = ts
         return gather_totals(t, group)
 
-    l, qi, flag, err = _run([r], [a_seg], [b_seg], gather, itr_max, tol, check_interval, want_cost)
+    if graph and tol == 0.0:
+        l, qi, flag, err = _run_graph([r], [a_seg], [b_seg], gather, itr_max)
+    else:
+        l, qi, flag, err = _run([r], [a_seg], [b_seg], gather, itr_max, tol, check_interval, want_cost)
     ok = flag != 2
     us, vs, parts = _finish([r], qi, gather, flag, want_cost and ok, lambda _: a_seg.device)
     cost = float("nan")

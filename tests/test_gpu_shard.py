@@ -137,6 +137,33 @@ def test_segments_equal_streaming_kernel_at_config3_size():
     assert abs(o["err"] - k2["err"].item()) <= 1e-10 * max(1.0, k2["err"].item())
 
 
+@pytest.mark.parametrize("world", [1, 3])
+def test_graph_replay_equals_eager_loop(world):
+    """The captured-iteration driver (CUDA graph replays) runs the same kernels in the same
+    order as the eager loop: bitwise-equal state, error and cost."""
+    n = 5000
+    a, b = _pair(n, 21)
+    kw = dict(h=1 / n, eps=1e-3, itr_max=25, input_is_log=True)
+    og = shard.solve_segments(_cuda(a), _cuda(b), world, graph=True, **kw)
+    oe = shard.solve_segments(_cuda(a), _cuda(b), world, graph=False, **kw)
+    assert np.array_equal(og["u"].cpu().numpy(), oe["u"].cpu().numpy())
+    assert np.array_equal(og["v"].cpu().numpy(), oe["v"].cpu().numpy())
+    assert og["cost"] == oe["cost"] and og["err"] == oe["err"] and og["iters"] == oe["iters"] == 25
+
+
+def test_graph_replay_nonfinite_iteration():
+    """A +inf log-weight poisons the state at the first half-step: the device counter
+    records iteration 1 through the graph replays, as the eager loop does."""
+    n = 3000
+    a, b = _pair(n, 22)
+    a = a.copy()
+    a[1234] = np.inf
+    for graph in (True, False):
+        o = shard.solve_segments(_cuda(a), _cuda(b), 2, h=1 / n, eps=1e-2, itr_max=10, input_is_log=True,
+                                 graph=graph)
+        assert o["flags"] == 2 and o["iters"] == 1 and np.isnan(o["cost"]) and np.isnan(o["err"])
+
+
 def test_shard_plan_errors():
     import ctypes
     from paper_2202_10042_b200 import _lib as L

@@ -15,12 +15,16 @@ def tk2():
     torch.cuda.synchronize(); t = time.perf_counter()
     fs1.solve(A[None], B[None], h=1.0 / n, eps=eps, itr_max=itr, domain="log", input_is_log=True)
     torch.cuda.synchronize(); return time.perf_counter() - t
-def tsh(world):
+def tsh(world, it=None, graph=True):
     torch.cuda.synchronize(); t = time.perf_counter()
-    shard.solve_segments(A, B, world, h=1.0 / n, eps=eps, itr_max=itr, input_is_log=True)
+    shard.solve_segments(A, B, world, h=1.0 / n, eps=eps, itr_max=it or itr, input_is_log=True, graph=graph)
     torch.cuda.synchronize(); return time.perf_counter() - t
 tk2(); tsh(1)
 k2 = min(tk2() for _ in range(3))
 for world in (1, 2, 8):
-    ts = min(tsh(world) for _ in range(3))
-    print(f"N=2^{lg} world {world}: {ts / (2 * itr) * 1e6:.1f} us per half-step (all ranks, wall) vs K2 {k2 / (2 * itr) * 1e6:.1f} us", flush=True)
+    for graph in (True, False):
+        t1 = min(tsh(world, itr, graph) for _ in range(2))
+        t2 = min(tsh(world, 3 * itr, graph) for _ in range(2))
+        per = (t2 - t1) / (4 * itr)  # steady state: marginal cost of a half-step
+        print(f"N=2^{lg} world {world} graph {graph}: {per * 1e6:.1f} us per half-step (all ranks on one GPU) "
+              f"vs K2 {k2 / (2 * itr) * 1e6:.1f} us", flush=True)
