@@ -123,7 +123,15 @@ fs1_status fs1_shard_plan(const fs1_desc* desc, int world, int rank, int device,
   for (int j = 0; j < 40; ++j) er_pow_l(C, (long double)shd::TILE * ldexpl(1.0L, j), &P.t2m[j], &P.t2e[j]);
   // blocks of TB tiles, one CTA each (about 4 per SM): the tile kernels' work units and
   // the first level of the two-level tile scan
-  P.TB = std::max(shd::NW, (int)((P.T + 4LL * sms - 1) / (4LL * sms)));
+  // resident CTAs of the half-step kernel per SM (registers), one block each: a single
+  // balanced wave over the SMs
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)&shd::k_half<false, true>, 32 * shd::NW, 0) !=
+      cudaSuccess)
+    return FS1_ERR_CUDA;
+  occ = std::max(1, occ);
+  P.TB = std::max(shd::NW, (int)((P.T + (long long)occ * sms - 1) / ((long long)occ * sms)));
+  if (P.TB > shd::TBMAX) P.TB = shd::TBMAX;
   P.nblk = (P.T + P.TB - 1) / P.TB;
   s->grid = P.nblk;
   s->w = ws_layout(P.T, s->grid);

@@ -172,15 +172,20 @@ __global__ void __launch_bounds__(32 * NW) k_load(const ShardParams P, const dou
 // Powers of the per-element multiplier L = lambda^{256 s}: table pw[j] = L^{2^j}
 // (j < 32), powers by binary decomposition.
 struct PowTab {
-  const double* m;
+  const double* m;   // L^{2^j}, j < 32
   const int* e;
+  const double* dm;  // optional direct table L^k, k < dn (shared memory)
+  const int* de;
+  int dn;
 };
 __device__ __forceinline__ ER<double> tpow(PowTab t, long long k) {
+  if (k < t.dn) return ER<double>{t.dm[k], t.de[k]};
   ER<double> r{1.0, 0};
   for (int j = 0; j < 32 && k; ++j, k >>= 1)
     if (k & 1) r = er_mul(r, ER<double>{t.m[j], t.e[j]});
   return r;
 }
+constexpr int TBMAX = 512;  // tiles per block (the direct power table of k_half)
 
 // Warp-level inclusive scans of (F, span) forward and (G, span) backward with
 // multipliers tpow(span) (Hillis-Steele, 5 levels).
@@ -282,18 +287,19 @@ struct BlockIO {
   double *BFm, *BBm; // [nblocks] block totals -> block carries (k_scan_blocks)
   int *BFe, *BBe;
 };
-__device__ __forceinline__ void block_totals(const ShardParams& P, const BlockIO& bi) {
+__device__ __forceinline__ void block_totals(const ShardParams& P, const BlockIO& bi, PowTab tiles) {
   const int b = blockIdx.x;
   const int t0 = b * P.TB, n = min(P.T, t0 + P.TB) - t0;
   ER<double> tF, tB;
-  const PowTab tiles{P.t2m, P.t2e};  // lambda^{256 2^j}
   cta_scan<32 * NW>(tiles, ER<double>{P.t2m[0], P.t2e[0]}, n, bi.Fm + t0, bi.Fe + t0, bi.Bm + t0, bi.Be + t0, tF, tB);
   if (threadIdx.x == 0) {
     bi.BFm[b] = tF.m; bi.BFe[b] = tF.e;
     bi.BBm[b] = tB.m; bi.BBe[b] = tB.e;
   }
 }
-__global__ void __launch_bounds__(32 * NW) k_block_scan(const ShardParams P, const BlockIO bi) { block_totals(P, bi); }
+__global__ void __launch_bounds__(32 * NW) k_block_scan(const ShardParams P, const BlockIO bi) {
+  block_totals(P, bi, PowTab{P.t2m, P.t2e, nullptr, nullptr, 0});
+}
 
 // One CTA over the blocks: exclusive block carries in place and the rank's totals
 // {F at the segment end, B at its start} -> tot[0..3] (m, e as doubles).
@@ -310,7 +316,7 @@ __global__ void __launch_bounds__(SCAN_NT) k_scan_blocks(const ShardParams P, co
   __syncthreads();
   ER<double> tF, tB;
   const ER<double> Ll = powt(P, P.T - (long long)(P.nblk - 1) * P.TB);
-  cta_scan<SCAN_NT>(PowTab{pm, pe}, Ll, P.nblk, bi.BFm, bi.BFe, bi.BBm, bi.BBe, tF, tB);
+  cta_scan<SCAN_NT>(PowTab{pm, pe, nullptr, nullptr, 0}, Ll, P.nblk, bi.BFm, bi.BFe, bi.BBm, bi.BBe, tF, tB);
   if (threadIdx.x == 0) { tot[0] = tF.m; tot[1] = (double)tF.e; tot[2] = tB.m; tot[3] = (double)tB.e; }
 }
 
@@ -359,13 +365,21 @@ __global__ void __launch_bounds__(32 * NW) k_half(const ShardParams P, const Hal
   __shared__ double sEm[2];
   __shared__ int sEe[2];
   __shared__ double werr[NW];
+  __shared__ double pwm[TBMAX + 1];  // lambda^{256 k}, k <= TB (this block's tile spans)
+  __shared__ int pwe[TBMAX + 1];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int k = threadIdx.x; k <= P.TB; k += blockDim.x) {
+    const ER<double> t = powt(P, k);
+    pwm[k] = t.m;
+    pwe[k] = t.e;
+  }
   if (warp == 0) {
     ER<double> EF, EB;
     ext_carries(P, io.allT, lane, EF, EB);
     if (lane == 0) { sEm[0] = EF.m; sEe[0] = EF.e; sEm[1] = EB.m; sEe[1] = EB.e; }
   }
   __syncthreads();
+  const PowTab tiles{P.t2m, P.t2e, pwm, pwe, P.TB + 1};
   const ER<double> EF{sEm[0], sEe[0]}, EB{sEm[1], sEe[1]};
   const double lam = P.lam;
   const double lp = P.lanepow[lane], rp = P.lanepow[31 - lane];
@@ -379,8 +393,8 @@ __global__ void __launch_bounds__(32 * NW) k_half(const ShardParams P, const Hal
   const ER<double> CBb = er_fma(powt(P, P.T - t1), EB, ER<double>{io.BCBm[blk], io.BCBe[blk]});
   for (int i = t0 + warp; i < t1; i += NW) {
     // full carries of tile i relative to its reference exponent R
-    const ER<double> CF = er_fma(powt(P, i - t0), CFb, ER<double>{io.CFm[i], io.CFe[i]});
-    const ER<double> CB = er_fma(powt(P, t1 - 1 - i), CBb, ER<double>{io.CBm[i], io.CBe[i]});
+    const ER<double> CF = er_fma(tpow(tiles, i - t0), CFb, ER<double>{io.CFm[i], io.CFe[i]});
+    const ER<double> CB = er_fma(tpow(tiles, t1 - 1 - i), CBb, ER<double>{io.CBm[i], io.CBe[i]});
     const int X = io.xX[i];
     int R = X;
     if (X == ZE || CF.e - X > LIM || CB.e - X > LIM) R = max(CF.e, CB.e);
@@ -460,7 +474,7 @@ __global__ void __launch_bounds__(32 * NW) k_half(const ShardParams P, const Hal
   }
   if (WRITE) {  // y's tiles of this block: in-block exclusive carries and block totals
     __syncthreads();
-    block_totals(P, io.yb);
+    block_totals(P, io.yb, tiles);
   }
   if (__any_sync(FULL, bad) && lane == 0) {
     atomicOr(&io.flag[0], 1);
