@@ -153,6 +153,17 @@ fs1_status fs1_cost(const fs1_plan_t* plan, const void* u, const void* v, double
  * parity tests.  x, y: [batch][n*m], must not alias.                             */
 fs1_status fs1_apply(const fs1_plan_t* plan, const void* x, void* y, void* workspace, void* stream);
 
+/* fs1_transport_plan — materialise gamma = diag(phi) K diag(psi) (
+ * the plans compared in Tables 1-4, column 5) for problems of at most
+ * FS1_MAX_TPLAN points (n*m): gamma[p][k][l] = phi_k lambda^{dist(k,l)} psi_l with
+ * k, l flat indices (2D: column-major, l1 distance in cells weighted by h1, h2),
+ * formed as exp(F_k + G_l - dist/eps) in fp64 and rounded once to the plan dtype.
+ *   u, v  : [batch][n*m] state as fs1_solve returns it (LOG: F, G; SCALING: phi, psi).
+ *   gamma : [batch][n*m][n*m], caller-owned, the plan dtype.
+ * Errors: FS1_ERR_ARG (NULL), FS1_ERR_UNSUPPORTED (n*m > FS1_MAX_TPLAN).          */
+#define FS1_MAX_TPLAN 8192
+fs1_status fs1_transport_plan(const fs1_plan_t* plan, const void* u, const void* v, void* gamma, void* stream);
+
 fs1_status fs1_plan_info(const fs1_plan_t* plan, fs1_plan_info_t* info);
 void fs1_plan_destroy(fs1_plan_t* plan);
 const char* fs1_status_string(fs1_status s);

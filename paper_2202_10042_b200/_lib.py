@@ -16,7 +16,7 @@ FS1_F32, FS1_F64 = 0, 1
 FS1_SCALING, FS1_LOG = 0, 1
 FLAG_CONVERGED, FLAG_NONFINITE, FLAG_ITR_MAX = 1, 2, 4
 
-EXPORTS = ["fs1_plan", "fs1_solve", "fs1_cost", "fs1_apply", "fs1_plan_info",
+EXPORTS = ["fs1_plan", "fs1_solve", "fs1_cost", "fs1_apply", "fs1_transport_plan", "fs1_plan_info",
            "fs1_plan_destroy", "fs1_status_string", "fs1_abi_version",
            # include/fs1_shard.h
            "fs1_shard_plan", "fs1_shard_init", "fs1_shard_half", "fs1_shard_cost_totals",
@@ -80,6 +80,8 @@ def lib():
         L.fs1_cost.restype = st
         L.fs1_apply.argtypes = [vp] * 5
         L.fs1_apply.restype = st
+        L.fs1_transport_plan.argtypes = [vp] * 5
+        L.fs1_transport_plan.restype = st
         L.fs1_plan_info.argtypes = [vp, ctypes.POINTER(PlanInfo)]
         L.fs1_plan_info.restype = st
         L.fs1_plan_destroy.argtypes = [vp]

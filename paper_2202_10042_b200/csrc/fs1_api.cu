@@ -664,6 +664,16 @@ fs1_status fs1_cost(const fs1_plan_t* plan, const void* u, const void* v, double
   return FS1_ERR_UNSUPPORTED;
 }
 
+fs1_status fs1_transport_plan(const fs1_plan_t* plan, const void* u, const void* v, void* gamma, void* stream) {
+  if (!plan || !u || !v || !gamma) return FS1_ERR_ARG;
+  const fs1_desc& d = plan->d;
+  if (d.n * d.m > FS1_MAX_TPLAN) return FS1_ERR_UNSUPPORTED;
+  const double c1 = d.h1 / d.eps, c2 = d.ndim == 2 ? d.h2 / d.eps : 0.0;
+  const cudaError_t e = launch_tplan(d.dtype == FS1_F64 ? 1 : 0, u, v, gamma, d.batch, d.n, d.m, c1, c2,
+                                     d.domain == FS1_LOG ? 1 : 0, (cudaStream_t)stream);
+  return e == cudaSuccess ? FS1_OK : FS1_ERR_CUDA;
+}
+
 fs1_status fs1_apply(const fs1_plan_t* plan, const void* x, void* y, void* workspace, void* stream) {
   if (!plan || !x || !y || x == y) return FS1_ERR_ARG;
   if (plan->ws && (!workspace || ((uintptr_t)workspace & 255))) return FS1_ERR_WORKSPACE;

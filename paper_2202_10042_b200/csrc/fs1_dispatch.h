@@ -49,4 +49,8 @@ struct Sep2dwEntry {
 };
 const Sep2dwEntry* sep2dw_table(int* count);
 
+// transport-plan materialisation (fs1_tplan.cu)
+cudaError_t launch_tplan(int dtype, const void* u, const void* v, void* g, long long batch, long long n, long long m,
+                         double c1, double c2, int logd, cudaStream_t st);
+
 }  // namespace fs1

@@ -191,3 +191,21 @@ def apply(x, *, h, eps, domain="scaling", shape=None, h2=None, kernel=0):
     y = torch.empty_like(x)
     plan(spec, dev).apply_into(x, y)
     return y
+
+
+def transport_plan(u, v, *, h, eps, domain="scaling", shape=None, h2=None):
+    """gamma = diag(phi) K diag(psi) per problem: [batch, n*m, n*m] (fs1_transport_plan)."""
+    dev = u.device.index
+    ndim, n, m = (1, u.shape[-1], 1) if shape is None else (2, *shape)
+    size = n * m
+    _check(u, "u", u.dtype, dev, size)
+    _check(v, "v", u.dtype, dev, size)
+    batch = u.numel() // size
+    spec = Spec(ndim=ndim, n=n, m=m, h1=float(h), h2=float(h2 if h2 is not None else (h if ndim == 2 else 0.0)),
+                eps=float(eps), batch=batch, dtype=u.dtype, domain=domain, itr_max=0)
+    g = torch.empty(batch, size, size, dtype=u.dtype, device=u.device)
+    p = plan(spec, dev)
+    s = L.lib().fs1_transport_plan(p._h, _ptr(u), _ptr(v), _ptr(g), _stream(dev))
+    if s != L.FS1_OK:
+        raise L.FS1Error(s, "fs1_transport_plan")
+    return g

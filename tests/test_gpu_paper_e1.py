@@ -44,8 +44,7 @@ def test_e1_plan_difference_table1_column5():
                     itr_max=cfg.itr_max, domain="scaling")
     ref = sinkhorn.solve(A, B, n=cfg.n, h1=cfg.h1, eps=cfg.eps, itr_max=cfg.itr_max, domain="scaling")
     K = dense.kernel(cfg.n, np.exp(-cfg.h1 / cfg.eps))
-    phi, psi = out["u"].cpu().numpy()[0], out["v"].cpu().numpy()[0]
-    P_gpu = phi[:, None] * K * psi[None, :]
+    P_gpu = fs1.transport_plan(out["u"], out["v"], h=cfg.h1, eps=cfg.eps, domain="scaling").cpu().numpy()[0]
     P_ref = np.exp(ref["F"][0])[:, None] * K * np.exp(ref["G"][0])[None, :]
     d = np.linalg.norm(P_gpu - P_ref)
     assert d <= 1e-12 * np.linalg.norm(P_ref), d

@@ -264,3 +264,21 @@ def test_config5_shard_sampled():
                          n=cfg.n, h1=cfg.h1, eps=cfg.eps, itr_max=cfg.itr_max)
     assert np.all(np.isfinite(ref["F"])) and np.all(ref["flags"] == 4)
     assert_solve_parity(out, ref, "log", "f32", pairs=pairs)
+
+
+@pytest.mark.parametrize("dom", ["scaling", "log"])
+def test_transport_plan_materialised(dom):
+    """fs1_transport_plan against the dense plan diag(phi) K diag(psi) of the oracle's own
+    state, and its marginals after the phi update: rows sum to a exactly (Alg. 1 line 12)."""
+    n, pairs, itr = 300, 3, 40
+    rng = np.random.default_rng(5)
+    A = rng.uniform(0.1, 1.0, (pairs, n)); A /= A.sum(1, keepdims=True)
+    B = rng.uniform(0.1, 1.0, (pairs, n)); B /= B.sum(1, keepdims=True)
+    out = fs1.solve(_cuda(A, "f64"), _cuda(B, "f64"), h=1 / n, eps=1e-2, itr_max=itr, domain=dom)
+    g = fs1.transport_plan(out["u"], out["v"], h=1 / n, eps=1e-2, domain=dom).cpu().numpy()
+    ref = sinkhorn.solve(A, B, n=n, h1=1 / n, eps=1e-2, itr_max=itr, domain=dom)
+    K = dense.kernel(n, np.exp(-1.0 / n / 1e-2))
+    for p in range(pairs):
+        G = np.exp(ref["F"][p])[:, None] * K * np.exp(ref["G"][p])[None, :]
+        assert np.max(np.abs(g[p] - G)) <= 1e-10 * np.max(G)
+        assert np.max(np.abs(g[p].sum(1) - A[p])) <= 1e-12
