@@ -73,6 +73,8 @@ SOLVE_CASES = [
     (999, 0.005, 60, "f32", "scaling"),
     (2000, 0.005, 40, "f32", "scaling"),
     (300, 0.003, 50, "f32", "log"),
+    (2000, 0.002, 40, "f32", "log"),   # E64 W1 (one warp, 64 points per lane)
+    (7000, 0.001, 20, "f32", "log"),   # E64 W4
     (4096, 0.001, 40, "f32", "log"),
     (3000, 0.001, 40, "f32", "log"),
     (1000, 0.001, 40, "f64", "log"),
