@@ -368,11 +368,13 @@ def run_fs1(args, cfg):
                                 "kernel_ms": kern_avg_s * 1e3,
                                 "peak_source": f"derived: {props.multi_processor_count} SMs x "
                                                f"{clk_mhz:.0f} MHz x 16 MUFU/clk / 2 rcp per update",
-                                # context: the instruction-issue bound of this
-                                # kernel's measured mix (~31 thread-instructions per update, ncu)
-                                "issue_bound": props.multi_processor_count * clk_mhz * 1e6 * 128 / 31 / 1e9,
-                                "frac_of_issue_bound": kern_ups / (props.multi_processor_count * clk_mhz * 1e6
-                                                                   * 128 / 31)}
+                                }
+            if info["kernel"] == "persist_f32_log_E32_W1":
+                # context: the instruction-issue bound of this kernel's
+                # measured mix (~31 thread-instructions per update, ncu at C2)
+                ib = props.multi_processor_count * clk_mhz * 1e6 * 128 / 31
+                line["roofline"]["issue_bound"] = ib / 1e9
+                line["roofline"]["frac_of_issue_bound"] = kern_ups / ib
         if info["kernel"].startswith("sep2dw"):
             # K3w keeps its 64 MiB working set in L2 (measured DRAM traffic 0.4 GB per
             # 300-iteration solve), so its bound is the MUFU pipe: per
