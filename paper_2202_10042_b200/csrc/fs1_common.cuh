@@ -127,30 +127,28 @@ __device__ __forceinline__ int warp_min(int v) { return __reduce_min_sync(FULL, 
 // up:   v + m * v[lane - d]  (lane >= d), else v
 // down: v + m * v[lane + d]  (lane + d < 32), else v
 __device__ __forceinline__ double scan_up(double v, unsigned d, double m) {
-  double r = v;
   asm volatile(
       "{\n\t.reg .pred p;\n\t.reg .b32 lo, hi, a, b;\n\t.reg .f64 s;\n\t"
-      "mov.b64 {lo, hi}, %1;\n\t"
-      "shfl.sync.up.b32 a|p, lo, %2, 0, -1;\n\t"
-      "shfl.sync.up.b32 b, hi, %2, 0, -1;\n\t"
+      "mov.b64 {lo, hi}, %0;\n\t"
+      "shfl.sync.up.b32 a|p, lo, %1, 0, -1;\n\t"
+      "shfl.sync.up.b32 b, hi, %1, 0, -1;\n\t"
       "mov.b64 s, {a, b};\n\t"
-      "@p fma.rn.f64 %0, %3, s, %1;\n\t}"
-      : "+d"(r)
-      : "d"(v), "r"(d), "d"(m));
-  return r;
+      "@p fma.rn.f64 %0, %2, s, %0;\n\t}"
+      : "+d"(v)
+      : "r"(d), "d"(m));
+  return v;
 }
 __device__ __forceinline__ double scan_down(double v, unsigned d, double m) {
-  double r = v;
   asm volatile(
       "{\n\t.reg .pred p;\n\t.reg .b32 lo, hi, a, b;\n\t.reg .f64 s;\n\t"
-      "mov.b64 {lo, hi}, %1;\n\t"
-      "shfl.sync.down.b32 a|p, lo, %2, 31, -1;\n\t"
-      "shfl.sync.down.b32 b, hi, %2, 31, -1;\n\t"
+      "mov.b64 {lo, hi}, %0;\n\t"
+      "shfl.sync.down.b32 a|p, lo, %1, 31, -1;\n\t"
+      "shfl.sync.down.b32 b, hi, %1, 31, -1;\n\t"
       "mov.b64 s, {a, b};\n\t"
-      "@p fma.rn.f64 %0, %3, s, %1;\n\t}"
-      : "+d"(r)
-      : "d"(v), "r"(d), "d"(m));
-  return r;
+      "@p fma.rn.f64 %0, %2, s, %0;\n\t}"
+      : "+d"(v)
+      : "r"(d), "d"(m));
+  return v;
 }
 // exclusive neighbours: v[lane-1] (0 at lane 0) and v[lane+1] (0 at lane 31)
 __device__ __forceinline__ double prev_or0(double v) {

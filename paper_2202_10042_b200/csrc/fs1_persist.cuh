@@ -48,28 +48,23 @@ template <class T, int E, int WARPS, bool LOGD> struct Persist {
   static constexpr size_t OFF_INT = OFF_RED + 2 * WARPS * sizeof(double);  // [2][WARPS] int
   static constexpr size_t SMEM = OFF_INT + 2 * WARPS * sizeof(int);
 
-  __device__ __forceinline__ static int swz(int tid) {
-    if constexpr (V >= 8) return tid & 7;
-    else if constexpr (V == 4) return (tid >> 1) & 3;
-    else if constexpr (V == 2) return (tid >> 2) & 1;
-    else return 0;
-  }
+  // vector j of thread t at s[j * NT + t]: consecutive threads read consecutive 16-byte
+  // words (conflict-free) and every access is one base register plus an immediate offset
+  __device__ __forceinline__ static int vidx(int tid, int j) { return j * NT + tid; }
   __device__ __forceinline__ static void lds(const Vt* s, int tid, T (&o)[E]) {
-    const int sw = swz(tid);
 #pragma unroll
     for (int j = 0; j < V; ++j) {
-      Vt v = s[tid * V + (j ^ sw)];
+      Vt v = s[vidx(tid, j)];
       Tt::unpack(v, &o[j * VEC]);
     }
   }
   __device__ __forceinline__ static void sts(Vt* s, int tid, const T (&o)[E]) {
-    const int sw = swz(tid);
 #pragma unroll
-    for (int j = 0; j < V; ++j) s[tid * V + (j ^ sw)] = Tt::pack(&o[j * VEC]);
+    for (int j = 0; j < V; ++j) s[vidx(tid, j)] = Tt::pack(&o[j * VEC]);
   }
   __device__ __forceinline__ static T lds1(const Vt* s, int tid, int e) {  // one element
     const T* p = reinterpret_cast<const T*>(s);
-    return p[(tid * V + ((e / VEC) ^ swz(tid))) * VEC + (e % VEC)];
+    return p[vidx(tid, e / VEC) * VEC + (e % VEC)];
   }
 
   // ---------------------------------------------------------------- block sums
@@ -249,7 +244,6 @@ template <class T, int E, int WARPS, bool LOGD> struct Half {
     int kexp = 0;
     T errs = T(1);
     if constexpr (CHECK && LOGD) errs = Tt::pow2(max(min(ye + R - te, 120), -120));
-    const int sw = PS::swz(c.tid);
     T tv[NCH][VEC], yo[NCH][VEC];
 #pragma unroll
     for (int i = 0; i < S; ++i) {
@@ -257,8 +251,8 @@ template <class T, int E, int WARPS, bool LOGD> struct Half {
 #pragma unroll
         for (int r = 0; r < NCH; ++r) {
           const int e = r * S + S - 1 - i;
-          Tt::unpack(tgt[c.tid * PS::V + ((e / VEC) ^ sw)], tv[r]);
-          if constexpr (CHECK) Tt::unpack(sK[c.tid * PS::V + ((e / VEC) ^ sw)], yo[r]);
+          Tt::unpack(tgt[PS::vidx(c.tid, e / VEC)], tv[r]);
+          if constexpr (CHECK) Tt::unpack(sK[PS::vidx(c.tid, e / VEC)], yo[r]);
         }
       }
       T kx[NCH];
@@ -328,6 +322,34 @@ template <class T, int E, int WARPS, bool LOGD> struct Half {
     bool slow = false;
     if constexpr (!LOGD) {
       PS::carries_lin(f, g, cf, cb, P, c.xm, par, c.lane, c.warp, c.lA, c.lB, c.rA, c.rB);
+    } else if constexpr (WARPS == 1) {
+      // one warp: the ER carries of carries_er() in plain doubles relative to the warp's
+      // largest chunk exponent Rw; exact exponents only where the slow-path test needs them
+      const int xeff = (f > T(0)) ? xe : ZE;
+      const int Rw = warp_max(xeff);
+      const double si = pow2d(xe - Rw);
+      double F = (double)f * si, G = (double)g * si;
+#pragma unroll
+      for (int k = 0; k < 5; ++k) {
+        F = scan_up(F, 1u << k, P.lvd[k]);
+        G = scan_down(G, 1u << k, P.lvd[k]);
+      }
+      const double cfd = prev_or0(F), cbd = next_or0(G);
+      const int ecf = (cfd > 0.0) ? Rw + Tr<double>::expo(cfd) : ZE;
+      const int ecb = (cbd > 0.0) ? Rw + Tr<double>::expo(cbd) : ZE;
+      R = xeff;
+      slow = (ecf - xeff > Tt::LIM) || (ecb - xeff > Tt::LIM) || (Rw - xeff > 1000);
+      if (slow) {
+        R = max(R, max(ecf, ecb));
+        s = Tt::pow2(max(xe - R, -1000));
+        const double so = pow2d(Rw - R);
+        cf = (T)(cfd * so);
+        cb = (T)(cbd * so);
+      } else {
+        const double so = pow2d(Rw - xe);
+        cf = (T)(cfd * so);
+        cb = (T)(cbd * so);
+      }
     } else {
       ER<double> CF, CB;
       PS::carries_er(f, g, xe, CF, CB, P, c.xm, c.xi, par, c.lane, c.warp, c.lP, c.rP);
@@ -361,11 +383,10 @@ template <class T, int E, int WARPS, bool LOGD> struct Half {
   __device__ __forceinline__ static void finish(const Ctx& c, T (&y)[E], int& ye, const Vt* tgt,
                                                 int te, int R, int kexp) {
     const T sc = LOGD ? Tt::pow2(kexp) : T(1);
-    const int sw = PS::swz(c.tid);
 #pragma unroll
     for (int j = 0; j < PS::V; ++j) {
       T tv[PS::VEC];
-      Tt::unpack(tgt[c.tid * PS::V + (j ^ sw)], tv);
+      Tt::unpack(tgt[PS::vidx(c.tid, j)], tv);
 #pragma unroll
       for (int r = 0; r < PS::VEC; ++r) {
         const int e = j * PS::VEC + r;
