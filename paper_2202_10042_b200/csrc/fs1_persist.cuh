@@ -23,12 +23,15 @@
 #pragma once
 #include <math.h>
 
+#include <type_traits>
+
 #include "fs1_common.cuh"
 #include "fs1_params.h"
 
 namespace fs1 {
 
-constexpr int NF_EVERY = 16;  // non-finite detection interval of multi-warp CTAs
+constexpr int NF_EVERY = 16;
+constexpr int NOSC = 16;      // renormalisation skipped while |kexp| <= NOSC (LOGD)  // non-finite detection interval of multi-warp CTAs
 constexpr int FS1_NONFINITE_FLAG = 2;
 constexpr double LN2 = 0.69314718055994530942;
 
@@ -244,46 +247,61 @@ template <class T, int E, int WARPS, bool LOGD> struct Half {
     int kexp = 0;
     T errs = T(1);
     if constexpr (CHECK && LOGD) errs = Tt::pow2(max(min(ye + R - te, 120), -120));
-    T tv[NCH][VEC], yo[NCH][VEC];
+    // the exponent of K x at the chunk's last point renormalises y (LOGD)
+    if constexpr (LOGD) kexp = Tt::expo(fma(lam, t[NCH - 1], y[E - 1]));
+    auto back = [&](auto sc_on) {
+      constexpr bool SC = decltype(sc_on)::value;
+      T tv[NCH][VEC], yo[NCH][VEC];
 #pragma unroll
-    for (int i = 0; i < S; ++i) {
-      if (i % VEC == 0) {
+      for (int i = 0; i < S; ++i) {
+        if (i % VEC == 0) {
+#pragma unroll
+          for (int r = 0; r < NCH; ++r) {
+            const int e = r * S + S - 1 - i;
+            Tt::unpack(tgt[PS::vidx(c.tid, e / VEC)], tv[r]);
+            if constexpr (CHECK) Tt::unpack(sK[PS::vidx(c.tid, e / VEC)], yo[r]);
+          }
+        }
+        T kx[NCH];
+#pragma unroll
+        for (int rr = 0; rr < NCH; ++rr) {
+          const int r = NCH - 1 - rr;
+          const int e = r * S + S - 1 - i;
+          kx[r] = fma(lam, t[r], y[e]);
+          t[r] = fma(lam, t[r], xs(e));
+        }
 #pragma unroll
         for (int r = 0; r < NCH; ++r) {
           const int e = r * S + S - 1 - i;
-          Tt::unpack(tgt[PS::vidx(c.tid, e / VEC)], tv[r]);
-          if constexpr (CHECK) Tt::unpack(sK[PS::vidx(c.tid, e / VEC)], yo[r]);
-        }
-      }
-      T kx[NCH];
-#pragma unroll
-      for (int rr = 0; rr < NCH; ++rr) {
-        const int r = NCH - 1 - rr;  // the chunk's last point first: its Kx sets kexp
-        const int e = r * S + S - 1 - i;
-        kx[r] = fma(lam, t[r], y[e]);
-        t[r] = fma(lam, t[r], xs(e));
-        if constexpr (LOGD) {
-          if (i == 0 && r == NCH - 1) {
-            kexp = Tt::expo(kx[r]);
-            sc = Tt::pow2(kexp);
+          const int q = e % VEC;
+          if constexpr (CHECK) {
+            y[e] = kx[r];
+            if (!MASK || e < c.nv) errp += (double)fabs(fma(yo[r][q] * errs, kx[r], -tv[r][q]));
+          } else {
+            T v;
+            if constexpr (LOGD && SC) v = (tv[r][q] * sc) * Tt::rcp(kx[r]);
+            else v = tv[r][q] * Tt::rcp(kx[r]);
+            if (MASK && e >= c.nv) v = T(0);
+            y[e] = v;
           }
         }
       }
-#pragma unroll
-      for (int r = 0; r < NCH; ++r) {
-        const int e = r * S + S - 1 - i;
-        const int q = e % VEC;
-        if constexpr (CHECK) {
-          y[e] = kx[r];
-          if (!MASK || e < c.nv) errp += (double)fabs(fma(yo[r][q] * errs, kx[r], -tv[r][q]));
-        } else {
-          T v;
-          if constexpr (LOGD) v = (tv[r][q] * sc) * Tt::rcp(kx[r]);
-          else v = tv[r][q] * Tt::rcp(kx[r]);
-          if (MASK && e >= c.nv) v = T(0);
-          y[e] = v;
-        }
+    };
+    if constexpr (LOGD && !CHECK && sizeof(T) * E <= 128) {
+      // (only for chunks whose two state vectors leave registers to spare: the second
+      // copy of the loop costs the 64-element float variant more than it saves)
+      // The renormalisation is an exact power of two: skip its multiply when every chunk
+      // of the warp is already within 2^+-NOSC of it (y's exponent then keeps the offset).
+      if (__all_sync(FULL, kexp >= -NOSC && kexp <= NOSC)) {
+        kexp = 0;
+        back(std::false_type{});
+      } else {
+        sc = Tt::pow2(kexp);
+        back(std::true_type{});
       }
+    } else {
+      if constexpr (LOGD) sc = Tt::pow2(kexp);
+      back(std::true_type{});
     }
     kexp_out = kexp;
     return errp;
