@@ -371,8 +371,9 @@ def run_fs1(args, cfg):
                                 }
             if info["kernel"] == "persist_f32_log_E32_W1":
                 # context: the instruction-issue bound of this kernel's
-                # measured mix (~31 thread-instructions per update, ncu at C2)
-                ib = props.multi_processor_count * clk_mhz * 1e6 * 128 / 31
+                # measured mix (25.5 thread-instructions per update: smsp__inst_executed.sum
+                # x 32 / updates, ncu at C2, profiles/r01g_ncu_c2.txt)
+                ib = props.multi_processor_count * clk_mhz * 1e6 * 128 / 25.5
                 line["roofline"]["issue_bound"] = ib / 1e9
                 line["roofline"]["frac_of_issue_bound"] = kern_ups / ib
         if info["kernel"].startswith("sep2dw"):
