@@ -9,7 +9,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libfs1.so")
+LIB_PATH = os.environ.get("FS1_LIB") or os.path.join(HERE, "libfs1.so")  # FS1_LIB: variant builds (tools)
 
 FS1_OK, FS1_ERR_ARG, FS1_ERR_EPS, FS1_ERR_UNSUPPORTED, FS1_ERR_CUDA, FS1_ERR_WORKSPACE = range(6)
 FS1_F32, FS1_F64 = 0, 1
