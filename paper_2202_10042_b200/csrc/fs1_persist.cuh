@@ -31,7 +31,13 @@
 namespace fs1 {
 
 constexpr int NF_EVERY = 16;
-constexpr int NOSC = 16;      // renormalisation skipped while |kexp| <= NOSC (LOGD)  // non-finite detection interval of multi-warp CTAs
+#ifndef FS1_NOSC
+#define FS1_NOSC 16
+#endif
+#ifndef FS1_NCH
+#define FS1_NCH 4
+#endif
+constexpr int NOSC = FS1_NOSC;  // renormalisation skipped while |kexp| <= NOSC (LOGD)  // non-finite detection interval of multi-warp CTAs
 constexpr int FS1_NONFINITE_FLAG = 2;
 constexpr double LN2 = 0.69314718055994530942;
 
@@ -209,7 +215,7 @@ template <class T, int E, int WARPS, bool LOGD> struct Half {
   // points whose recursions run interleaved; run c enters with the carry
   // lam^S (carry of run c-1) + (run c-1's aggregate).  S stays a multiple of the
   // shared-memory vector width.
-  static constexpr int NCH = (E / PS::VEC >= 4) ? 4 : ((E / PS::VEC >= 2) ? 2 : 1);
+  static constexpr int NCH = (E / PS::VEC >= 4 && FS1_NCH >= 4) ? 4 : ((E / PS::VEC >= 2 && FS1_NCH >= 2) ? 2 : 1);
   static constexpr int S = E / NCH;
 
   // 3. the recursions from the exact carries (fq: forward run aggregates, gq: backward)
@@ -252,6 +258,8 @@ template <class T, int E, int WARPS, bool LOGD> struct Half {
     auto back = [&](auto sc_on) {
       constexpr bool SC = decltype(sc_on)::value;
       T tv[NCH][VEC], yo[NCH][VEC];
+      (void)yo;
+      (void)SC;
 #pragma unroll
       for (int i = 0; i < S; ++i) {
         if (i % VEC == 0) {
