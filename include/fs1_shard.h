@@ -11,7 +11,8 @@
  *     all-gather the ranks' totals of x  ->  fs1_shard_half  ->  totals of y
  *
  * and the caller (the Python driver, paper_2202_10042_b200/shard.py) moves the
- * totals between ranks with one NCCL all-gather per half-step and owns the loop
+ * totals between ranks with one NCCL all-gather per half-step — or lets the kernels
+ * move them over peer memory (fused exchange, below) — and owns the loop
  * control (Algorithm 1's while, with the readings of DESIGN.md R2-R6).
  *
  * Supported: ndim 1, FS1_F64, FS1_LOG, batch 1, check_interval >= 1, no warm
@@ -78,6 +79,34 @@ fs1_status fs1_shard_cost_totals(const fs1_shard_t* s, int psi, double* tot8, vo
  * of the partials over ranks (fixed rank order).  cost_partial may be NULL.        */
 fs1_status fs1_shard_finish(const fs1_shard_t* s, int psi, const double* all_tot8, void* u_seg, void* v_seg,
                             double* cost_partial, void* workspace, void* stream);
+
+/* ---- Fused exchange over peer memory.
+ * Instead of the caller's all-gather of the totals, the kernels move them: the
+ * totals kernel of every production writes this rank's row straight into every
+ * rank's mailbox (NVLink peer stores through IPC mappings) and raises a per-rank
+ * flag with a system-scope release; the next half-step's kernel acquires the flags
+ * and reads the rows from its own mailbox.  No host step, no collective launch.
+ *
+ * fs1_shard_mailbox_bytes — size of one rank's mailbox for `world` ranks
+ *   (world <= FS1_SHARD_MAXW = 16).
+ * fs1_shard_mailbox_alloc — cudaMalloc + zero a mailbox on `device` and return its
+ *   CUDA IPC handle (64 bytes into ipc_handle, may be NULL).  One mailbox per rank per
+ *   solve: its flags and epoch must start at zero.
+ * fs1_shard_mailbox_open / _close — map / unmap a peer's mailbox from its IPC handle
+ *   (another process; a rank's own mailbox or one in this process is used directly).
+ * fs1_shard_mailbox_free — free a mailbox from fs1_shard_mailbox_alloc.
+ * fs1_shard_set_mailboxes — boxes[world]: every rank's mailbox as seen from this
+ *   rank's device (boxes[rank] = its own); NULL switches back to the all_tot path.
+ *   With mailboxes set, fs1_shard_init and fs1_shard_half (write = 1) deliver the
+ *   totals themselves and fs1_shard_half ignores all_tot (may be NULL); tot4 still
+ *   receives this rank's totals.  All ranks must issue the same sequence of calls.
+ * Errors: FS1_ERR_ARG (world out of range, NULL pointers), FS1_ERR_CUDA.            */
+size_t fs1_shard_mailbox_bytes(int world);
+fs1_status fs1_shard_mailbox_alloc(int world, int device, void** box, void* ipc_handle);
+fs1_status fs1_shard_mailbox_open(const void* ipc_handle, int device, void** box);
+fs1_status fs1_shard_mailbox_close(void* box);
+fs1_status fs1_shard_mailbox_free(void* box);
+fs1_status fs1_shard_set_mailboxes(fs1_shard_t* s, void* const* boxes);
 
 void fs1_shard_destroy(fs1_shard_t* s);
 

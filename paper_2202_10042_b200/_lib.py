@@ -20,7 +20,9 @@ EXPORTS = ["fs1_plan", "fs1_solve", "fs1_cost", "fs1_apply", "fs1_transport_plan
            "fs1_plan_destroy", "fs1_status_string", "fs1_abi_version",
            # include/fs1_shard.h
            "fs1_shard_plan", "fs1_shard_init", "fs1_shard_half", "fs1_shard_cost_totals",
-           "fs1_shard_finish", "fs1_shard_destroy"]
+           "fs1_shard_finish", "fs1_shard_destroy", "fs1_shard_mailbox_bytes", "fs1_shard_mailbox_alloc",
+           "fs1_shard_mailbox_open", "fs1_shard_mailbox_close", "fs1_shard_mailbox_free",
+           "fs1_shard_set_mailboxes"]
 
 
 class Desc(ctypes.Structure):
@@ -108,5 +110,17 @@ def lib():
         L.fs1_shard_finish.restype = st
         L.fs1_shard_destroy.argtypes = [vp]
         L.fs1_shard_destroy.restype = None
+        L.fs1_shard_mailbox_bytes.argtypes = [st]
+        L.fs1_shard_mailbox_bytes.restype = ctypes.c_size_t
+        L.fs1_shard_mailbox_alloc.argtypes = [st, st, ctypes.POINTER(vp), vp]
+        L.fs1_shard_mailbox_alloc.restype = st
+        L.fs1_shard_mailbox_open.argtypes = [vp, st, ctypes.POINTER(vp)]
+        L.fs1_shard_mailbox_open.restype = st
+        L.fs1_shard_mailbox_close.argtypes = [vp]
+        L.fs1_shard_mailbox_close.restype = st
+        L.fs1_shard_mailbox_free.argtypes = [vp]
+        L.fs1_shard_mailbox_free.restype = st
+        L.fs1_shard_set_mailboxes.argtypes = [vp, vp]
+        L.fs1_shard_set_mailboxes.restype = st
         _lib = L
     return _lib

@@ -133,6 +133,9 @@ struct Sep2dParams {
 // One 1D problem sharded over ranks by contiguous whole-tile segments (K2s,
 // fs1_shard.cuh), fp64 log domain.  Per-rank scalars and tables; the workspace
 // pointers live in the host plan and are passed per launch.
+#ifndef FS1_SHARD_MAXW
+#define FS1_SHARD_MAXW 16  // ranks of a fused (mailbox) exchange
+#endif
 struct ShardParams {
   long long n;       // global points N
   long long lo;      // first global point of this segment (multiple of 256)
@@ -149,6 +152,10 @@ struct ShardParams {
   double lanepow[32];  // lambda^{8 l}
   double t2m[40];      // lambda^{256 2^j} = t2m 2^t2e (Remark 3.3)
   int t2e[40];
+  // Fused exchange (fs1_shard_set_mailboxes): every rank's mailbox, box[rank] = own,
+  // peers' through NVLink peer / IPC mappings; fused = 0: totals come from all_tot.
+  int fused;
+  double* box[FS1_SHARD_MAXW];
 };
 
 }  // namespace fs1

@@ -170,7 +170,7 @@ fs1_status fs1_shard_init(const fs1_shard_t* s, const void* a_seg, const void* b
 fs1_status fs1_shard_half(const fs1_shard_t* s, int which, int hs, int check, int write, int l1, int psi_in,
                           int psi_out, const double* all_tot, double* tot4, double* errflag, void* ws,
                           void* stream) {
-  if (!s || !all_tot || !ws || ((uintptr_t)ws & 255) || (which != 0 && which != 1) || hs < 0 ||
+  if (!s || (!all_tot && !s->P.fused) || !ws || ((uintptr_t)ws & 255) || (which != 0 && which != 1) || hs < 0 ||
       (psi_in & ~1) || (psi_out & ~1) || (write && !tot4) || (check && !errflag))
     return FS1_ERR_ARG;
   if (which == 1 && check) return FS1_ERR_ARG;  // the check rides on the psi half-step (R3)
@@ -201,6 +201,7 @@ fs1_status fs1_shard_half(const fs1_shard_t* s, int which, int hs, int check, in
   }
   if (check && write && which == 0 && psi_in == psi_out) return FS1_ERR_ARG;  // psi^(l) must survive
   const dim3 g(s->grid), b(32 * shd::NW);
+  if (P.fused) shd::k_box_wait<<<1, 32, 0, st>>>(P);
   if (check && write) shd::k_half<true, true><<<g, b, 0, st>>>(P, io);
   else if (check) shd::k_half<true, false><<<g, b, 0, st>>>(P, io);
   else if (write) shd::k_half<false, true><<<g, b, 0, st>>>(P, io);
@@ -239,6 +240,71 @@ fs1_status fs1_shard_finish(const fs1_shard_t* s, int psi, const double* all_tot
   shd::k_store<<<s->grid, 32 * shd::NW, 0, st>>>(s->P, at<double>(ws, Qoff[psi]), at<int>(ws, QXoff[psi]),
                                                  (double*)v_seg);
   return cudaGetLastError() == cudaSuccess ? FS1_OK : FS1_ERR_CUDA;
+}
+
+size_t fs1_shard_mailbox_bytes(int world) {
+  if (world < 1 || world > FS1_SHARD_MAXW) return 0;
+  return al256((size_t)world * 8 * sizeof(double) + ((size_t)world + 1) * sizeof(unsigned));
+}
+
+fs1_status fs1_shard_mailbox_alloc(int world, int device, void** box, void* ipc_handle) {
+  const size_t bytes = fs1_shard_mailbox_bytes(world);
+  if (!bytes || !box) return FS1_ERR_ARG;
+  int prev = 0;
+  if (cudaGetDevice(&prev) != cudaSuccess || cudaSetDevice(device) != cudaSuccess) return FS1_ERR_CUDA;
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, bytes);
+  if (e == cudaSuccess) e = cudaMemset(p, 0, bytes);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e == cudaSuccess && ipc_handle) {
+    cudaIpcMemHandle_t h;
+    e = cudaIpcGetMemHandle(&h, p);
+    if (e == cudaSuccess) memcpy(ipc_handle, &h, sizeof(h));
+  }
+  cudaSetDevice(prev);
+  if (e != cudaSuccess) {
+    if (p) cudaFree(p);
+    return FS1_ERR_CUDA;
+  }
+  *box = p;
+  return FS1_OK;
+}
+
+fs1_status fs1_shard_mailbox_open(const void* ipc_handle, int device, void** box) {
+  if (!ipc_handle || !box) return FS1_ERR_ARG;
+  int prev = 0;
+  if (cudaGetDevice(&prev) != cudaSuccess || cudaSetDevice(device) != cudaSuccess) return FS1_ERR_CUDA;
+  cudaIpcMemHandle_t h;
+  memcpy(&h, ipc_handle, sizeof(h));
+  const cudaError_t e = cudaIpcOpenMemHandle(box, h, cudaIpcMemLazyEnablePeerAccess);
+  cudaSetDevice(prev);
+  return e == cudaSuccess ? FS1_OK : FS1_ERR_CUDA;
+}
+
+fs1_status fs1_shard_mailbox_close(void* box) {
+  if (!box) return FS1_ERR_ARG;
+  return cudaIpcCloseMemHandle(box) == cudaSuccess ? FS1_OK : FS1_ERR_CUDA;
+}
+
+fs1_status fs1_shard_mailbox_free(void* box) {
+  if (!box) return FS1_ERR_ARG;
+  return cudaFree(box) == cudaSuccess ? FS1_OK : FS1_ERR_CUDA;
+}
+
+fs1_status fs1_shard_set_mailboxes(fs1_shard_t* s, void* const* boxes) {
+  if (!s) return FS1_ERR_ARG;
+  ShardParams& P = s->P;
+  if (!boxes) {
+    P.fused = 0;
+    memset(P.box, 0, sizeof(P.box));
+    return FS1_OK;
+  }
+  if (P.world > FS1_SHARD_MAXW) return FS1_ERR_ARG;
+  for (int k = 0; k < P.world; ++k)
+    if (!boxes[k]) return FS1_ERR_ARG;
+  for (int k = 0; k < P.world; ++k) P.box[k] = static_cast<double*>(boxes[k]);
+  P.fused = 1;
+  return FS1_OK;
 }
 
 void fs1_shard_destroy(fs1_shard_t* s) { delete s; }

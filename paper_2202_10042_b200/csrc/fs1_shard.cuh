@@ -301,6 +301,62 @@ __global__ void __launch_bounds__(32 * NW) k_block_scan(const ShardParams P, con
   block_totals(P, bi, PowTab{P.t2m, P.t2e, nullptr, nullptr, 0});
 }
 
+// ---------------------------------------------------------------- fused exchange
+// Mailbox of a rank (device memory its peers write through NVLink):
+//   double tot[2][world][4]  totals of production e in slot e & 1, one row per rank
+//   u32 flag[world]          flag[k] = the last production rank k delivered here
+//   u32 epoch                this rank's own production counter
+// Producer (k_scan_blocks, one thread): e = ++epoch; row `rank` of slot e & 1 in every
+// mailbox, one system-scope fence, then flag[rank] = e in every mailbox (release).
+// Consumer (k_box_wait, one warp, lane k = rank k): wait for flag[k] >= e (its own
+// epoch: the ranks produce in lock step), one fence (acquire); then k_half reads row
+// k of slot e & 1.  Two slots suffice:
+// a rank produces e + 2 only after consuming e + 1, i.e. after every rank produced
+// e + 1, i.e. after every rank finished consuming e.
+__device__ __forceinline__ unsigned* box_flags(double* box, int world) {
+  return reinterpret_cast<unsigned*>(box + 8 * world);
+}
+__device__ __forceinline__ unsigned ld_relaxed_sys(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_sys(unsigned* p, unsigned v) {
+  asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// one system-scope fence per side: data stores -> fence -> flag stores (release
+// pattern); flag loads -> fence -> data loads (acquire pattern)
+__device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+__device__ __forceinline__ void box_publish(const ShardParams& P, const double (&t)[4]) {
+  unsigned* ep = box_flags(P.box[P.rank], P.world) + P.world;
+  const unsigned e = __ldcg(ep) + 1u;
+  *ep = e;
+  const int slot = e & 1;
+  for (int p = 0; p < P.world; ++p) {
+    double* dst = P.box[p] + ((size_t)slot * P.world + P.rank) * 4;
+    dst[0] = t[0]; dst[1] = t[1]; dst[2] = t[2]; dst[3] = t[3];
+  }
+  fence_acq_rel_sys();
+  for (int p = 0; p < P.world; ++p) st_relaxed_sys(box_flags(P.box[p], P.world) + P.rank, e);
+}
+// Consumer side, one warp ahead of k_half (lane k = rank k): wait until every rank
+// delivered this rank's epoch e, then one system-scope fence (acquire pattern).  The
+// kernel boundary orders k_half's reads of the slot after it.  (Waiting inside the
+// producing kernel would save this launch but deadlocks the lock-stepped ranks of
+// one device, whose producers run one after another on one stream.)
+__global__ void k_box_wait(const ShardParams P) {
+  const unsigned* fl = box_flags(P.box[P.rank], P.world);
+  const unsigned e = __ldcg(fl + P.world);
+  for (int k = threadIdx.x; k < P.world; k += 32)
+    while (ld_relaxed_sys(fl + k) < e) {
+    }
+  fence_acq_rel_sys();
+}
+__device__ __forceinline__ const double* box_slot(const ShardParams& P) {
+  const unsigned e = __ldcg(box_flags(P.box[P.rank], P.world) + P.world);
+  return P.box[P.rank] + (size_t)(e & 1) * P.world * 4;
+}
+
 // One CTA over the blocks: exclusive block carries in place and the rank's totals
 // {F at the segment end, B at its start} -> tot[0..3] (m, e as doubles).
 __global__ void __launch_bounds__(SCAN_NT) k_scan_blocks(const ShardParams P, const BlockIO bi, double* tot) {
@@ -317,7 +373,11 @@ __global__ void __launch_bounds__(SCAN_NT) k_scan_blocks(const ShardParams P, co
   ER<double> tF, tB;
   const ER<double> Ll = powt(P, P.T - (long long)(P.nblk - 1) * P.TB);
   cta_scan<SCAN_NT>(PowTab{pm, pe, nullptr, nullptr, 0}, Ll, P.nblk, bi.BFm, bi.BFe, bi.BBm, bi.BBe, tF, tB);
-  if (threadIdx.x == 0) { tot[0] = tF.m; tot[1] = (double)tF.e; tot[2] = tB.m; tot[3] = (double)tB.e; }
+  if (threadIdx.x == 0) {
+    const double t[4] = {tF.m, (double)tF.e, tB.m, (double)tB.e};
+    if (tot) { tot[0] = t[0]; tot[1] = t[1]; tot[2] = t[2]; tot[3] = t[3]; }
+    if (P.fused) box_publish(P, t);
+  }
 }
 
 // Decay of the other ranks' totals to this segment: lane k of warp 0 takes rank k
@@ -331,10 +391,10 @@ __device__ __forceinline__ void ext_carries(const ShardParams& P, const double* 
     if (k == P.rank) continue;
     const long long T0k = (long long)k * P.Ttot / P.world, T1k = (long long)(k + 1) * P.Ttot / P.world;
     if (k < P.rank) {
-      const ER<double> t{allT[4 * k], (int)allT[4 * k + 1]};
+      const ER<double> t{__ldcg(allT + 4 * k), (int)__ldcg(allT + 4 * k + 1)};
       f = er_add(f, er_mul(powt(P, P.T0 - T1k), t));
     } else {
-      const ER<double> t{allT[4 * k + 2], (int)allT[4 * k + 3]};
+      const ER<double> t{__ldcg(allT + 4 * k + 2), (int)__ldcg(allT + 4 * k + 3)};
       b = er_add(b, er_mul(powt(P, T0k - (P.T0 + P.T)), t));
     }
   }
@@ -375,7 +435,8 @@ __global__ void __launch_bounds__(32 * NW) k_half(const ShardParams P, const Hal
   }
   if (warp == 0) {
     ER<double> EF, EB;
-    ext_carries(P, io.allT, lane, EF, EB);
+    const double* allT = P.fused ? box_slot(P) : io.allT;
+    ext_carries(P, allT, lane, EF, EB);
     if (lane == 0) { sEm[0] = EF.m; sEe[0] = EF.e; sEm[1] = EB.m; sEe[1] = EB.e; }
   }
   __syncthreads();

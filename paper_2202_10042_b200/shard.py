@@ -10,6 +10,13 @@ readings of DESIGN.md R2-R6); every arithmetic step runs in the CUDA kernels.
 With tol = 0 (fixed iterations) one iteration — both half-steps of every local rank and
 both exchanges — is captured once as a CUDA graph and replayed (`_run_graph`).
 
+`fused=True` replaces the per-half-step all-gather of the totals by the fused
+exchange of include/fs1_shard.h: the kernel producing a rank's totals stores them
+into every rank's mailbox over peer memory (CUDA IPC mappings of the peers'
+mailboxes on the NVLink box) and the next half-step's kernel waits on the flags —
+no collective and no host step per half-step.  The check-step error sum and the
+cost still go through torch.distributed.
+
 Two drivers share `ShardRank`:
   * `solve_sharded`    one rank per process, totals moved by torch.distributed
                        (NCCL over NVLink on the GPU box; gloo in CPU tests);
@@ -55,6 +62,11 @@ class ShardRank:
         self.tot8 = torch.zeros(8, dtype=torch.float64, device=dev)
         self.cost = torch.zeros(1, dtype=torch.float64, device=dev)
 
+    def set_mailboxes(self, boxes):
+        """boxes: every rank's mailbox pointer (int) as seen from this device; None = off."""
+        arr = None if boxes is None else (ctypes.c_void_p * len(boxes))(*boxes)
+        self._ok(L.lib().fs1_shard_set_mailboxes(self._h, arr), "fs1_shard_set_mailboxes")
+
     def __del__(self):
         h = getattr(self, "_h", None)
         if h is not None and h.value:
@@ -91,9 +103,11 @@ class ShardRank:
         return self.cost
 
 
-def _run(ranks, segs_a, segs_b, gather, itr_max, tol, check_interval, want_cost):
+def _run(ranks, segs_a, segs_b, gather, itr_max, tol, check_interval, want_cost, tgather=None):
     """Algorithm 1's loop over lock-stepped ranks.  gather(list of per-local-rank tensors)
-    -> [world, k] tensor of every rank's values in rank order (the one exchange)."""
+    -> [world, k] tensor of every rank's values in rank order (the one exchange);
+    tgather: the same for the totals (None: `gather`; fused exchange: returns None)."""
+    tgather = tgather or gather
     tots = [r.init(a, b) for r, a, b in zip(ranks, segs_a, segs_b)]
     use_tol = tol > 0.0
     l, qi, hs, flag, err = 0, 0, 0, 4, float("nan")
@@ -101,7 +115,7 @@ def _run(ranks, segs_a, segs_b, gather, itr_max, tol, check_interval, want_cost)
         check = l >= itr_max or (use_tol and l % check_interval == 0)
         last = l >= itr_max
         qo = qi ^ 1 if check else qi
-        allT = gather(tots)
+        allT = tgather(tots)
         outs = [r.half(0, hs, check, not last, l + 1, qi, qo, allT) for r in ranks]
         if check:
             ef = gather([o[1] for o in outs]).cpu()  # one host sync per check
@@ -115,26 +129,27 @@ def _run(ranks, segs_a, segs_b, gather, itr_max, tol, check_interval, want_cost)
                 break
             qi = qo
         hs += 1
-        allT = gather([o[0].clone() for o in outs])
+        allT = tgather([o[0].clone() for o in outs])
         tots = [r.half(1, hs, False, True, l + 1, qi, qi, allT)[0].clone() for r in ranks]
         hs += 1
         l += 1
     return l, qi, flag, err
 
 
-def _run_graph(ranks, segs_a, segs_b, gather, itr_max):
+def _run_graph(ranks, segs_a, segs_b, gather, itr_max, tgather=None):
     """The fixed-iteration loop (tol = 0) with one iteration captured as a
     CUDA graph — both half-steps of every local rank and both exchanges — and replayed:
     no host round trip or per-kernel launch cost per half-step.  The non-finite record
     uses the plan's device iteration counter (l1 = -1).  Same kernels, same order, same
     results as `_run`."""
+    tgather = tgather or gather
     for r, a, b in zip(ranks, segs_a, segs_b):
         r.init(a, b)
 
     def iteration():
-        allT = gather([r.tot for r in ranks])
+        allT = tgather([r.tot for r in ranks])
         outs = [r.half(0, 0, False, True, -1, 0, 0, allT) for r in ranks]
-        allT2 = gather([o[0].clone() for o in outs])
+        allT2 = tgather([o[0].clone() for o in outs])
         for r in ranks:
             r.half(1, 1, False, True, -1, 0, 0, allT2)
 
@@ -147,7 +162,7 @@ def _run_graph(ranks, segs_a, segs_b, gather, itr_max):
         for _ in range(itr_max - 1):     # l = 1 .. itr_max - 1
             g.replay()
     # loop top at l = itr_max: the exit check, psi^(l) kept in buffer 0
-    allT = gather([r.tot for r in ranks])
+    allT = tgather([r.tot for r in ranks])
     outs = [r.half(0, 0, True, False, itr_max + 1, 0, 1, allT) for r in ranks]
     ef = gather([o[1] for o in outs]).cpu()
     err = float(sum(ef[k, 0].item() for k in range(ef.shape[0])))
@@ -171,10 +186,44 @@ def _finish(ranks, qi, gather, flag, want_cost, dtype_dev):
     return us, vs, parts
 
 
+class Mailbox:
+    """One rank's mailbox of the fused exchange (fs1_shard_mailbox_*): device memory
+    its peers write into, with the CUDA IPC handle that maps it in their processes."""
+
+    def __init__(self, world, device):
+        self.ptr = ctypes.c_void_p()
+        h = (ctypes.c_ubyte * 64)()
+        s = L.lib().fs1_shard_mailbox_alloc(world, device, ctypes.byref(self.ptr), h)
+        if s != L.FS1_OK:
+            raise L.FS1Error(s, "fs1_shard_mailbox_alloc")
+        self.handle = bytes(h)
+        self.opened = []
+
+    def open_peer(self, handle, device):
+        p = ctypes.c_void_p()
+        s = L.lib().fs1_shard_mailbox_open(handle, device, ctypes.byref(p))
+        if s != L.FS1_OK:
+            raise L.FS1Error(s, "fs1_shard_mailbox_open")
+        self.opened.append(p)
+        return p.value
+
+    def free(self):
+        torch.cuda.synchronize()
+        for p in self.opened:
+            L.lib().fs1_shard_mailbox_close(p)
+        self.opened = []
+        if self.ptr.value:
+            L.lib().fs1_shard_mailbox_free(self.ptr)
+            self.ptr = ctypes.c_void_p()
+
+
 def solve_segments(a, b, world, *, h, eps, itr_max, tol=0.0, check_interval=1, input_is_log=False,
-                   want_cost=True, graph=True):
+                   want_cost=True, graph=True, fused=False):
     """All `world` ranks in this process on a's device (lock step); a, b: [N] fp64 CUDA.
-    Returns {u, v (full F, G), iters, err, flags, cost} like fs1.solve for batch 1."""
+    Returns {u, v (full F, G), iters, err, flags, cost} like fs1.solve for batch 1.
+    fused: the totals move through the ranks' mailboxes (here all on one device, so the
+    kernels' flag waits are already satisfied when they run: the lock step issues
+    every rank's producer before any consumer)."""
     n = a.numel()
     dev = a.device.index
     ranks = [ShardRank(n, world, r, h=h, eps=eps, itr_max=itr_max, tol=tol, check_interval=check_interval,
@@ -182,10 +231,23 @@ def solve_segments(a, b, world, *, h, eps, itr_max, tol=0.0, check_interval=1, i
     sa = [a[r.lo:r.lo + r.len].contiguous() for r in ranks]
     sb = [b[r.lo:r.lo + r.len].contiguous() for r in ranks]
     gather = lambda ts: torch.stack([t.clone() for t in ts])  # noqa: E731
-    if graph and tol == 0.0:
-        l, qi, flag, err = _run_graph(ranks, sa, sb, gather, itr_max)
-    else:
-        l, qi, flag, err = _run(ranks, sa, sb, gather, itr_max, tol, check_interval, want_cost)
+    tgather, boxes = None, []
+    if fused:
+        boxes = [Mailbox(world, dev) for _ in range(world)]
+        for r in ranks:
+            r.set_mailboxes([bx.ptr.value for bx in boxes])
+        tgather = lambda ts: None  # noqa: E731
+    try:
+        if graph and tol == 0.0:
+            l, qi, flag, err = _run_graph(ranks, sa, sb, gather, itr_max, tgather)
+        else:
+            l, qi, flag, err = _run(ranks, sa, sb, gather, itr_max, tol, check_interval, want_cost, tgather)
+    finally:
+        for bx in boxes:
+            bx.free()
+        if fused:
+            for r in ranks:
+                r.set_mailboxes(None)
     ok = flag != 2
     us, vs, parts = _finish(ranks, qi, gather, flag, want_cost and ok, lambda r: a.device)
     cost = float(sum(p.item() for p in parts)) if (want_cost and ok) else float("nan")
@@ -194,10 +256,11 @@ def solve_segments(a, b, world, *, h, eps, itr_max, tol=0.0, check_interval=1, i
 
 
 def solve_sharded(a_seg, b_seg, n, *, h, eps, itr_max, tol=0.0, check_interval=1, input_is_log=False,
-                  want_cost=True, group=None, graph=True):
+                  want_cost=True, group=None, graph=True, fused=False):
     """This process's rank of a torch.distributed job: a_seg, b_seg are its segment
     [lo, lo+len) of the N-point problem (see `segment`).  Collectives: one all-gather of
-    4 doubles per half-step, of 2 per check, of 8 for the cost, one all-reduce at exit."""
+    4 doubles per half-step (none with fused=True: the kernels deliver the totals into
+    the peers' IPC-mapped mailboxes), of 2 per check, of 8 for the cost."""
     import torch.distributed as dist
     world, rank = dist.get_world_size(group), dist.get_rank(group)
     dev = a_seg.device.index
@@ -210,10 +273,27 @@ def solve_sharded(a_seg, b_seg, n, *, h, eps, itr_max, tol=0.0, check_interval=1
         (t,) = ts
         return gather_totals(t, group)
 
-    if graph and tol == 0.0:
-        l, qi, flag, err = _run_graph([r], [a_seg], [b_seg], gather, itr_max)
-    else:
-        l, qi, flag, err = _run([r], [a_seg], [b_seg], gather, itr_max, tol, check_interval, want_cost)
+    tgather, box = None, None
+    if fused:
+        box = Mailbox(world, dev)
+        handles = [None] * world
+        dist.all_gather_object(handles, box.handle, group=group)
+        ptrs = [box.ptr.value if k == rank else box.open_peer(handles[k], dev) for k in range(world)]
+        r.set_mailboxes(ptrs)
+        tgather = lambda ts: None  # noqa: E731
+        dist.barrier(group)  # every mailbox mapped before any rank's first delivery
+    try:
+        if graph and tol == 0.0:
+            l, qi, flag, err = _run_graph([r], [a_seg], [b_seg], gather, itr_max, tgather)
+        else:
+            l, qi, flag, err = _run([r], [a_seg], [b_seg], gather, itr_max, tol, check_interval, want_cost,
+                                    tgather)
+    finally:
+        if box is not None:
+            torch.cuda.synchronize()
+            dist.barrier(group)  # no peer still writes into this mailbox
+            box.free()
+            r.set_mailboxes(None)
     ok = flag != 2
     us, vs, parts = _finish([r], qi, gather, flag, want_cost and ok, lambda _: a_seg.device)
     cost = float("nan")

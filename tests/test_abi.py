@@ -16,7 +16,7 @@ def _header_functions():
     for h in sorted(os.listdir(os.path.join(ROOT, "include"))):
         if h.endswith(".h"):
             src = open(os.path.join(ROOT, "include", h)).read()
-            names |= set(re.findall(r"^\s*(?:fs1_status|void|const char\*|int)\s+(fs1_\w+)\s*\(", src, re.M))
+            names |= set(re.findall(r"^\s*(?:fs1_status|void|const char\*|int|size_t)\s+(fs1_\w+)\s*\(", src, re.M))
     return sorted(names)
 
 

@@ -179,3 +179,50 @@ def test_shard_plan_errors():
     assert L.lib().fs1_shard_plan(ctypes.byref(d), 2, 0, 0, *args) == L.FS1_ERR_UNSUPPORTED
     d.eps = 0.0
     assert L.lib().fs1_shard_plan(ctypes.byref(d), 2, 0, 0, *args) == L.FS1_ERR_EPS
+
+
+# ---- fused exchange (mailboxes over peer memory, include/fs1_shard.h) ----------------
+@pytest.mark.parametrize("world,graph,tol", [(1, True, 0.0), (2, True, 0.0), (5, True, 0.0), (8, False, 0.0),
+                                             (3, False, 1e-9), (16, True, 0.0)])
+def test_fused_exchange_equals_gathered(world, graph, tol):
+    """The kernels deliver the totals into every rank's mailbox (row `rank` of slot
+    e & 1, flag release / acquire) instead of the host all-gather: the same values
+    reach the same kernels, so state, error, cost and iteration count are bitwise
+    those of the gathered exchange — over graph replays, the eager loop with the
+    tolerance stop (check steps), and the largest fused world (16)."""
+    n = 8000
+    a, b = _pair(n, 31 + world)
+    kw = dict(h=1 / n, eps=2e-3, itr_max=40 if tol == 0.0 else 3000, tol=tol, check_interval=3,
+              input_is_log=True, graph=graph)
+    of = shard.solve_segments(_cuda(a), _cuda(b), world, fused=True, **kw)
+    og = shard.solve_segments(_cuda(a), _cuda(b), world, fused=False, **kw)
+    assert np.array_equal(of["u"].cpu().numpy(), og["u"].cpu().numpy())
+    assert np.array_equal(of["v"].cpu().numpy(), og["v"].cpu().numpy())
+    assert of["cost"] == og["cost"] and of["err"] == og["err"]
+    assert of["iters"] == og["iters"] and of["flags"] == og["flags"]
+    if tol > 0.0:
+        assert of["flags"] == 1 and of["err"] <= tol
+
+
+def test_fused_exchange_oracle_parity_and_repeat():
+    """Fused exchange against the oracle, twice in a row (fresh mailboxes per solve:
+    flags and epochs start at zero), and the mailbox ABI's argument checks."""
+    import ctypes
+    from paper_2202_10042_b200 import _lib as L
+    n, world = 3001, 4
+    a, b = _pair(n, 41)
+    ref = sinkhorn.solve(a, b, n=n, h1=1 / n, eps=2e-3, itr_max=30, domain="log", input_is_log=True)
+    for _ in range(2):
+        o = shard.solve_segments(_cuda(a), _cuda(b), world, h=1 / n, eps=2e-3, itr_max=30, input_is_log=True,
+                                 fused=True)
+        _parity(o, ref)
+    lib = L.lib()
+    assert lib.fs1_shard_mailbox_bytes(0) == 0 and lib.fs1_shard_mailbox_bytes(17) == 0
+    assert lib.fs1_shard_mailbox_bytes(16) >= 16 * 8 * 8 + 17 * 4
+    p = ctypes.c_void_p()
+    assert lib.fs1_shard_mailbox_alloc(0, 0, ctypes.byref(p), None) == L.FS1_ERR_ARG
+    assert lib.fs1_shard_mailbox_alloc(2, 0, None, None) == L.FS1_ERR_ARG
+    assert lib.fs1_shard_set_mailboxes(None, None) == L.FS1_ERR_ARG
+    r = shard.ShardRank(n, 2, 0, h=1 / n, eps=2e-3, itr_max=1, input_is_log=True)
+    with pytest.raises(L.FS1Error):
+        r.set_mailboxes([0, 0])  # NULL mailbox

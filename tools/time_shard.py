@@ -15,16 +15,18 @@ def tk2():
     torch.cuda.synchronize(); t = time.perf_counter()
     fs1.solve(A[None], B[None], h=1.0 / n, eps=eps, itr_max=itr, domain="log", input_is_log=True)
     torch.cuda.synchronize(); return time.perf_counter() - t
-def tsh(world, it=None, graph=True):
+def tsh(world, it=None, graph=True, fused=False):
     torch.cuda.synchronize(); t = time.perf_counter()
-    shard.solve_segments(A, B, world, h=1.0 / n, eps=eps, itr_max=it or itr, input_is_log=True, graph=graph)
+    shard.solve_segments(A, B, world, h=1.0 / n, eps=eps, itr_max=it or itr, input_is_log=True, graph=graph,
+                         fused=fused)
     torch.cuda.synchronize(); return time.perf_counter() - t
 tk2(); tsh(1)
 k2 = min(tk2() for _ in range(3))
 for world in (1, 2, 8):
-    for graph in (True, False):
-        t1 = min(tsh(world, itr, graph) for _ in range(2))
-        t2 = min(tsh(world, 3 * itr, graph) for _ in range(2))
+    for graph, fused in ((True, False), (True, True), (False, False), (False, True)):
+        t1 = min(tsh(world, itr, graph, fused) for _ in range(2))
+        t2 = min(tsh(world, 3 * itr, graph, fused) for _ in range(2))
         per = (t2 - t1) / (4 * itr)  # steady state: marginal cost of a half-step
-        print(f"N=2^{lg} world {world} graph {graph}: {per * 1e6:.1f} us per half-step (all ranks on one GPU) "
+        print(f"N=2^{lg} world {world} graph {graph} fused {fused}: {per * 1e6:.1f} us per half-step "
+              f"(all ranks on one GPU) "
               f"vs K2 {k2 / (2 * itr) * 1e6:.1f} us", flush=True)
