@@ -276,8 +276,7 @@ def solve_sharded(a_seg, b_seg, n, *, h, eps, itr_max, tol=0.0, check_interval=1
     tgather, box = None, None
     if fused:
         box = Mailbox(world, dev)
-        handles = [None] * world
-        dist.all_gather_object(handles, box.handle, group=group)
+        handles = exchange_handles(box.handle, group)
         ptrs = [box.ptr.value if k == rank else box.open_peer(handles[k], dev) for k in range(world)]
         r.set_mailboxes(ptrs)
         tgather = lambda ts: None  # noqa: E731
@@ -302,6 +301,17 @@ def solve_sharded(a_seg, b_seg, n, *, h, eps, itr_max, tol=0.0, check_interval=1
         cost = float(sum(allc[k, 0].item() for k in range(world)))
     return {"u": us[0], "v": vs[0], "iters": l, "err": err if ok else float("nan"), "flags": flag,
             "cost": cost, "segment": (r.lo, r.len)}
+
+
+def exchange_handles(handle, group=None):
+    """Every rank's mailbox IPC handle (bytes) in rank order: one all_gather_object, once
+    per solve (host-side, any backend)."""
+    import torch.distributed as dist
+    handles = [None] * dist.get_world_size(group)
+    dist.all_gather_object(handles, handle, group=group)
+    if any(not isinstance(h, bytes) or len(h) != len(handle) for h in handles):
+        raise RuntimeError("mailbox handle exchange: malformed handle")
+    return handles
 
 
 def gather_totals(t, group=None):

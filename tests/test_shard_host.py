@@ -37,8 +37,10 @@ def _worker(rank, world, port, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     t = torch.tensor([rank + 0.5, -1.0 * rank, 2.0 ** (rank + 3), float(rank)], dtype=torch.float64)
     out = shard.gather_totals(t)
+    hs = shard.exchange_handles(bytes([rank + 7]) * 64)  # the fused exchange's IPC handles
     if rank == 0:
         q.put(out.numpy())
+        q.put(hs)
     dist.barrier()
     dist.destroy_process_group()
 
@@ -53,19 +55,21 @@ def test_gather_totals_gloo_world2():
     for p in ps:
         p.start()
     out = q.get(timeout=120)
+    hs = q.get(timeout=120)
     for p in ps:
         p.join(timeout=60)
         assert p.exitcode == 0
     assert out.shape == (2, 4)
     for r in range(2):
         assert list(out[r]) == [r + 0.5, -1.0 * r, 2.0 ** (r + 3), float(r)]
+    assert hs == [bytes([7]) * 64, bytes([8]) * 64]  # every rank's handle, in rank order
 
 
 class FakeRank:
     """Stands in for ShardRank: records calls; errors follow `errs` (per check)."""
 
-    def __init__(self, rank, errs, bad_at=None):
-        self.rank, self.errs, self.bad_at = rank, list(errs), bad_at
+    def __init__(self, rank, errs, bad_at=None, fused=False):
+        self.rank, self.errs, self.bad_at, self.fused = rank, list(errs), bad_at, fused
         self.calls = []
         self.tot = torch.zeros(4, dtype=torch.float64)
         self.ef = torch.zeros(2, dtype=torch.float64)
@@ -75,7 +79,7 @@ class FakeRank:
         return self.tot
 
     def half(self, which, hs, check, write, l1, psi_in, psi_out, all_tot):
-        assert all_tot.shape[1] == 4
+        assert (all_tot is None) if self.fused else (all_tot.shape[1] == 4)
         self.calls.append(("half", which, hs, check, write, l1, psi_in, psi_out))
         if check:
             e = self.errs.pop(0) if self.errs else 1.0
@@ -124,3 +128,15 @@ def test_loop_nonfinite_reports_first_iteration():
     l, qi, flag, err = shard._run([r0, r1], [None] * 2, [None] * 2, _gather, 50, 1e-12, 5, True)
     assert flag == 2
     assert l == 3  # the device-recorded first non-finite iteration, seen at the check at l = 5
+
+
+def test_loop_fused_exchange_same_calls_no_totals():
+    """fused exchange: the loop passes no totals (the kernels deliver them) and issues
+    exactly the gathered loop's calls; the check-step errors still use `gather`."""
+    for tol, errs in ((0.0, []), (1e-9, [1.0, 1e-6, 4e-10])):
+        g = [FakeRank(0, errs), FakeRank(1, errs)]
+        f = [FakeRank(0, errs, fused=True), FakeRank(1, errs, fused=True)]
+        rg = shard._run(g, [None] * 2, [None] * 2, _gather, 6, tol, 2, True)
+        rf = shard._run(f, [None] * 2, [None] * 2, _gather, 6, tol, 2, True, tgather=lambda ts: None)
+        assert rg == rf
+        assert [r.calls for r in g] == [r.calls for r in f]
