@@ -10,6 +10,14 @@ for c in c1 c3 c4 c5 e1_8000 e2_8000; do
   timeout 400 python bench.py --config $c --steps 5 --warmup 3 > $O/bench_$c.json 2> $O/bench_$c.err
 done
 timeout 300 python bench.py --impl reference --steps 2 --warmup 3 > $O/bench_ref.json 2> $O/bench_ref.err
+# the multi-GPU launch path at N = 1 (torchrun, NCCL) and the sharded driver (gathered / fused exchange)
+timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29533 \
+  bench.py --gpus 1 --steps 5 --warmup 3 > $O/bench_c2_torchrun.json 2> $O/bench_c2_torchrun.err
+for f in 0 1; do
+  timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29534 \
+    tools/shard_dist_demo.py 24 20 $f 2>&1 | grep world >> $O/shard_dist.txt
+done
+timeout 300 python tools/time_shard_graph.py 24 50 > $O/shard_graph_timing.txt 2>&1
 for c in c2 c3 c4; do
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_$c.csv \
     python bench.py --config $c --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > $O/ncu_launch_$c.log 2>&1
