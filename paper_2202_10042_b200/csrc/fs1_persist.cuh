@@ -37,6 +37,9 @@ constexpr int NF_EVERY = 16;
 #ifndef FS1_NCH
 #define FS1_NCH 4
 #endif
+#ifndef FS1_NEWTON_WARPS
+#define FS1_NEWTON_WARPS 4
+#endif
 constexpr int NOSC = FS1_NOSC;  // renormalisation skipped while |kexp| <= NOSC (LOGD)  // non-finite detection interval of multi-warp CTAs
 constexpr int FS1_NONFINITE_FLAG = 2;
 constexpr double LN2 = 0.69314718055994530942;
@@ -47,6 +50,9 @@ template <class T, int E, int WARPS, bool LOGD> struct Persist {
   static constexpr int VEC = Tt::VEC;
   static constexpr int V = E / VEC;
   static constexpr int NT = 32 * WARPS;
+  // fp64 quotient by Newton refinement in the small-CTA variants (latency-bound: one
+  // or a few problems), by the correctly rounded reciprocal in the 8-32-warp ones
+  static constexpr bool NEWTON = (WARPS <= FS1_NEWTON_WARPS);
   static_assert(E % VEC == 0, "E must be a multiple of the vector width");
 
   // shared memory layout (bytes)
@@ -287,8 +293,8 @@ template <class T, int E, int WARPS, bool LOGD> struct Half {
             if (!MASK || e < c.nv) errp += (double)fabs(fma(yo[r][q] * errs, kx[r], -tv[r][q]));
           } else {
             T v;
-            if constexpr (LOGD && SC) v = (tv[r][q] * sc) * Tt::rcp(kx[r]);
-            else v = tv[r][q] * Tt::rcp(kx[r]);
+            if constexpr (LOGD && SC) v = Tt::template div<PS::NEWTON>(tv[r][q] * sc, kx[r]);
+            else v = Tt::template div<PS::NEWTON>(tv[r][q], kx[r]);
             if (MASK && e >= c.nv) v = T(0);
             y[e] = v;
           }
@@ -416,7 +422,7 @@ template <class T, int E, int WARPS, bool LOGD> struct Half {
 #pragma unroll
       for (int r = 0; r < PS::VEC; ++r) {
         const int e = j * PS::VEC + r;
-        T val = (tv[r] * sc) * Tt::rcp(y[e]);
+        T val = Tt::template div<PS::NEWTON>(tv[r] * sc, y[e]);
         if (MASK && e >= c.nv) val = T(0);
         y[e] = val;
       }
