@@ -284,3 +284,30 @@ def test_transport_plan_materialised(dom):
         G = np.exp(ref["F"][p])[:, None] * K * np.exp(ref["G"][p])[None, :]
         assert np.max(np.abs(g[p] - G)) <= 1e-10 * np.max(G)
         assert np.max(np.abs(g[p].sum(1) - A[p])) <= 1e-12
+
+
+@pytest.mark.parametrize("spread", [0.0, 12.0, 30.0])
+def test_log_fp32_renormalisation_skip_and_apply(spread):
+    """The C2 kernel (fp32 log, E32 W1) skips the output renormalisation while every chunk
+    of the warp has |kexp| <= 16 and applies it otherwise.  Smooth
+    weights (spread 0) keep kexp small; iid log-weights spread over `spread` nats at
+    c = h/eps = 0.49 (the largest c the E32 W1 tile takes: c 32 E <= 650) let Kx at a
+    chunk's last point fall up to lambda^31 = 2^-22 below the chunk scale, past the
+    skip bound, so the renormalising branch runs too.  Parity with the oracle
+    either way (the skip changes exponents, not values)."""
+    n, eps, P = 1024, 2e-3, 6
+    rng = np.random.default_rng(77 + int(spread))
+    x = (np.arange(n) + 0.5) / n
+    la = np.stack([-(x - 0.3 - 0.05 * p) ** 2 / 0.01 - spread * rng.random(n) for p in range(P)])
+    lb = np.stack([-(x - 0.6 + 0.04 * p) ** 2 / 0.02 - spread * rng.random(n) for p in range(P)])
+    la -= np.logaddexp.reduce(la, axis=1, keepdims=True)
+    lb -= np.logaddexp.reduce(lb, axis=1, keepdims=True)
+    A, B = la.astype(np.float32), lb.astype(np.float32)
+    out = fs1.solve(_cuda(A, "f32"), _cuda(B, "f32"), h=1 / n, eps=eps, itr_max=60, domain="log",
+                    input_is_log=True)
+    spec = fs1.Spec(ndim=1, n=n, m=1, h1=1 / n, h2=0.0, eps=eps, batch=P, dtype=torch.float32, domain="log",
+                    input_is_log=True, itr_max=60)
+    assert fs1.plan(spec, 0).info()["kernel"] == "persist_f32_log_E32_W1"  # the C2 kernel
+    ref = sinkhorn.solve(A.astype(np.float64), B.astype(np.float64), n=n, h1=1 / n, eps=eps, itr_max=60,
+                         domain="log", input_is_log=True, apply="recur")
+    assert_solve_parity(out, ref, "log", "f32")
