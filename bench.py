@@ -183,10 +183,21 @@ def sample_plan(cfg):
     return [0], 1, "1 pair, 1 iteration, plain-C LSE recursion"
 
 
+def host_threads():
+    """Rank 0 runs the oracle alone (the other ranks exit): give its BLAS every host core,
+    also under torchrun, which sets OMP_NUM_THREADS=1 per process."""
+    try:
+        from threadpoolctl import threadpool_limits
+        return threadpool_limits(limits=os.cpu_count())
+    except Exception:
+        return None
+
+
 def run_reference(args, cfg):
     ws, rank, _ = dist_env()
     if rank != 0:
         return
+    _limits = host_threads()  # noqa: F841 (kept alive for the run)
     pairs, iters, what = sample_plan(cfg)
     oracle_sample(cfg, pairs[:1], 1)          # warm-up (builds the C oracle, BLAS threads)
     times = []
