@@ -68,22 +68,50 @@ void fs1o_sweep_scaling(const double* x, long n, long stride, long lines, long l
   }
 }
 
+/* The two sweeps of one line are independent of each other (lines 5 and 6 of
+ * Algorithm 1 read only x), so they are written as two loops; for a single line
+ * (config 3) they run on two threads.  Each sweep is still sequential and its
+ * arithmetic is unchanged. */
+static void fwd_log(const double* xl, long n, long stride, ld C, ld* r) {
+  r[0] = xl[0];
+  for (long i = 1; i <= n - 1; ++i) r[i] = lae(r[i - 1] - C, (ld)xl[i * stride]);
+}
+
+static void bwd_log(const double* xl, long n, long stride, ld C, ld* s) {
+  s[n - 1] = -INFINITY;
+  for (long i = 1; i <= n - 1; ++i) {
+    long k = n - 1 - i;
+    s[k] = -C + lae(s[k + 1], (ld)xl[(k + 1) * stride]);
+  }
+}
+
 void fs1o_sweep_log(const double* X, long n, long stride, long lines, long lstride,
                     double c, double* Y) {
+  const ld C = (ld)c;
+  if (lines == 1) {
+    ld* r = (ld*)malloc(sizeof(ld) * n);
+    ld* s = (ld*)malloc(sizeof(ld) * n);
+#pragma omp parallel sections num_threads(2)
+    {
+#pragma omp section
+      fwd_log(X, n, stride, C, r);
+#pragma omp section
+      bwd_log(X, n, stride, C, s);
+    }
+#pragma omp parallel for schedule(static)
+    for (long i = 0; i < n; ++i) Y[i * stride] = (double)lae(r[i], s[i]);
+    free(r);
+    free(s);
+    return;
+  }
 #pragma omp parallel for schedule(static)
   for (long l = 0; l < lines; ++l) {
     const double* xl = X + l * lstride;
     double* yl = Y + l * lstride;
     ld* r = (ld*)malloc(sizeof(ld) * n);
     ld* s = (ld*)malloc(sizeof(ld) * n);
-    const ld C = (ld)c;
-    r[0] = xl[0];
-    s[n - 1] = -INFINITY;
-    for (long i = 1; i <= n - 1; ++i) {
-      r[i] = lae(r[i - 1] - C, (ld)xl[i * stride]);
-      long k = n - 1 - i;
-      s[k] = -C + lae(s[k + 1], (ld)xl[(k + 1) * stride]);
-    }
+    fwd_log(xl, n, stride, C, r);
+    bwd_log(xl, n, stride, C, s);
     for (long i = 0; i < n; ++i) yl[i * stride] = (double)lae(r[i], s[i]);
     free(r);
     free(s);
