@@ -254,3 +254,52 @@ def test_2d_separable_converged_cost_sandwich():
     assert r["flags"][0] == sinkhorn.CONVERGED
     gap = r["cost"][0] - lp
     assert -1e-9 <= gap <= eps * min(w1.entropy(a), w1.entropy(b)) + 1e-9
+
+
+# ------------------------------------------------------------------ log-weight inputs
+@pytest.mark.parametrize("apply", ["dense", "recur"])
+def test_input_is_log_equals_linear_input(apply):
+    """solve(log a, log b, input_is_log=True) is the run on a, b (the branch that feeds
+    every C3/C4 reference, oracle/sinkhorn.py): log domain against the log domain at
+    1e-13, and against the independent scaling-domain path (plain K @ x) at 1e-11."""
+    n = 150
+    x = (np.arange(n) + 0.5) / n
+    rng = np.random.default_rng(20)
+    # smooth log-weights spanning ~200 nats (finite after exp: the linear paths can run)
+    la = -((x - 0.3) / 0.07) ** 2 + 0.1 * rng.standard_normal(n)
+    lb = -((x - 0.6) / 0.05) ** 2 + 0.1 * rng.standard_normal(n)
+    la -= np.log(np.sum(np.exp(la)))
+    lb -= np.log(np.sum(np.exp(lb)))
+    kw = dict(n=n, h1=1.0 / n, eps=0.02, itr_max=60, apply=apply)
+    rl = sinkhorn.solve(la, lb, domain="log", input_is_log=True, **kw)
+    rlin = sinkhorn.solve(np.exp(la), np.exp(lb), domain="log", **kw)
+    rs = sinkhorn.solve(np.exp(la), np.exp(lb), domain="scaling", **kw)
+    for k in ("F", "G"):
+        np.testing.assert_allclose(rl[k], rlin[k], rtol=1e-13, atol=1e-13)
+        np.testing.assert_allclose(rl[k], rs[k], rtol=1e-11, atol=1e-11)
+    assert rl["cost"][0] == pytest.approx(rlin["cost"][0], rel=1e-13)
+    assert rl["cost"][0] == pytest.approx(rs["cost"][0], rel=1e-12)
+    assert rl["err"][0] == pytest.approx(rs["err"][0], rel=1e-9)
+
+
+def test_input_is_log_minus_inf_weights():
+    """-inf log-weights (zero mass) in the log domain give F = -inf (G = -inf) exactly
+    there and equal the scaling-domain run with exact zeros elsewhere (the scaling
+    path divides a_i = 0 by K psi > 0 and never forms a logarithm of the weights)."""
+    rng = np.random.default_rng(21)
+    n = 64
+    a, b = gi.random_positive(rng, n), gi.random_positive(rng, n)
+    a[[0, 7, 8, 40]] = 0.0
+    b[[3, 63]] = 0.0
+    a, b = a / a.sum(), b / b.sum()
+    with np.errstate(divide="ignore"):
+        la, lb = np.log(a), np.log(b)
+    kw = dict(n=n, h1=1.0 / n, eps=0.05, itr_max=30)
+    rl = sinkhorn.solve(la, lb, domain="log", input_is_log=True, apply="recur", **kw)
+    rs = sinkhorn.solve(a, b, domain="scaling", **kw)
+    assert np.array_equal(np.isneginf(rl["F"][0]), a == 0)
+    assert np.array_equal(np.isneginf(rl["G"][0]), b == 0)
+    for k in ("F", "G"):
+        m = np.isfinite(rs[k][0])
+        np.testing.assert_allclose(rl[k][0][m], rs[k][0][m], rtol=1e-11, atol=1e-11)
+    assert rl["cost"][0] == pytest.approx(rs["cost"][0], rel=1e-12)
