@@ -3,9 +3,12 @@
 
 A "step" is one full FS-1 solve (Algorithm 1: every iteration, the marginal
 error at exit and the fused return-line cost) over one batch of synthetic
-histogram pairs of BASELINE.json's configuration.  Default workload: configs[1]
-("c2": 4096 pairs, N=1024, fp32, eps=5e-3, 500 iterations) — the config the
-metric is quoted on that fits one GPU.
+histogram pairs of BASELINE.json's configuration.  Default workload: configs[2]
+("c3": one pair, N = 2^24, fp64 log domain, eps = 1e-4, 1000 iterations) —
+BASELINE.json quotes its metric on no particular config, so the bench line is
+the largest single-GPU configuration (the HBM-streaming kernel K2, the one the
+metric's "achieved HBM GB/s" half is about).  Every other config runs with
+--config cK.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl fs1|reference]
 
@@ -16,6 +19,7 @@ results {cost, iters, err, flags} are all-gathered with NCCL inside each step.
 from __future__ import annotations
 
 import argparse
+import dataclasses
 import json
 import os
 import statistics
@@ -40,7 +44,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c2", choices=sorted(gi.CONFIGS))
+    ap.add_argument("--config", default="c3", choices=sorted(gi.CONFIGS))
     ap.add_argument("--impl", default="fs1", choices=["fs1", "reference"])
     ap.add_argument("--batch", type=int, default=None, help="pairs per GPU (default: config)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -114,17 +118,73 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- roofline
-MUFU_PER_SM_CLK = 16        # SFU lanes per SM per clock (guide: B300 has 2x B200's SFU rate)
-FMA_PER_SM_CLK = 128        # FP32 lanes per SM per clock
+NOMINAL_HBM_GBS = 8000.0    # the north_star's "~8 TB/s" denominator
+MUFU_PER_SM_CLK = 16        # fp32 MUFU ops per SM per clock (tools/ubench.cu, profiles/r02_ubench.txt)
+DFMA_PER_SM_CLK = 64        # fp64 FMA per SM per clock (same micro-benchmark)
+# fp64 persistent kernels, per update: 2 half-steps x (2 recursion FMAs + 1 combine +
+# 5 for the quotient y = tgt / Kx: MUFU.RCP64H seed, 2 Newton FMA pairs, 1 multiply)
+DFMA_PER_UPDATE = 16
 
 
-def alu_peak_updates(sms, clk_mhz):
-    """Issue/MUFU roofline of the persistent kernel: per grid-point
-    update the path needs at least 2 reciprocals (one per half-step, MUFU) and 8
-    FP32 FMA-pipe ops (4 recursion FMAs, 2 p+q combines, 2 b*rcp); the MUFU term
-    dominates: 2/16 SM-clk per update."""
-    per_update = max(2.0 / MUFU_PER_SM_CLK, 8.0 / FMA_PER_SM_CLK)
-    return sms * clk_mhz * 1e6 / per_update
+def launches_per_solve(info, batch):
+    """Library kernels one fs1_solve launches: K1 one launch for the whole batch; K2 and
+    K3w / K3 one cooperative launch per problem (each preceded by a cudaMemsetAsync of
+    its grid-barrier counter, which is not a kernel)."""
+    return 1 if info["kernel"].startswith("persist") else batch
+
+
+def roofline(cfg, info, updates, it_run, batch, kern_s, peaks, src, props):
+    """Roofline object of the dominant kernel + achieved algorithmic HBM GB/s.
+
+    Algorithmic HBM bytes: a streaming kernel (K2, K3w / K3) reads
+    x and the target and writes y once per half-step, 6 words per update (fixed-iteration
+    runs: no check word); a persistent kernel (K1) keeps the state on chip and moves 4
+    words per grid point per solve (reads a, b; writes u, v)."""
+    kern = info["kernel"]
+    wb = 8 if cfg.dtype == "f64" else 4
+    sms = props.multi_processor_count
+    clk = peaks.get("sm_max_mhz", 1965.0)
+    if kern.startswith("persist"):
+        alg = 4 * wb * cfg.size * batch
+    else:
+        alg = 6 * wb * updates
+    hbm = alg / kern_s / 1e9
+    ups = updates / kern_s
+    if not kern.startswith("persist"):
+        peak = peaks.get("hbm_gbs", 6650.0)
+        r = {"bound": "hbm", "achieved": hbm, "peak": peak, "unit": "GB/s", "frac": hbm / peak,
+             "traffic": profile_traffic(cfg.name), "kernel_ms": kern_s * 1e3,
+             "algorithmic_bytes_per_launch": alg / launches_per_solve(info, batch),
+             "bytes_per_update": 6 * wb,
+             "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({src})",
+             "peak_nominal": NOMINAL_HBM_GBS, "frac_nominal": hbm / NOMINAL_HBM_GBS}
+        if kern.startswith("sep2dw"):
+            r["note"] = ("the 64 MiB working set stays in L2 (traffic << algorithmic bytes); "
+                         "the kernel is MUFU/latency-bound, DESIGN.md §6.4")
+        return r, hbm
+    ctas = info.get("ctas_per_problem", 1) * batch
+    if ctas < sms:
+        # fewer CTAs than SMs (C1: one pair on one SM): a latency-bound sequential chain
+        return {"bound": "latency", "achieved": kern_s * 1e6 / max(it_run, 1), "peak": None,
+                "unit": "us/iteration", "frac": None, "traffic": profile_traffic(cfg.name),
+                "kernel_ms": kern_s * 1e3,
+                "note": f"{ctas} CTA(s) on {sms} SMs: time per iteration is the figure of merit"}, hbm
+    if cfg.dtype == "f64":
+        peak = sms * clk * 1e6 * DFMA_PER_SM_CLK / DFMA_PER_UPDATE
+        how = f"{sms} SMs x {clk:.0f} MHz x {DFMA_PER_SM_CLK} DFMA/clk / {DFMA_PER_UPDATE} DFMA per update"
+    else:
+        peak = sms * clk * 1e6 * MUFU_PER_SM_CLK / 2.0
+        how = f"{sms} SMs x {clk:.0f} MHz x {MUFU_PER_SM_CLK} MUFU/clk / 2 rcp per update"
+    r = {"bound": "alu", "achieved": ups / 1e9, "peak": peak / 1e9, "unit": "Gupdate/s",
+         "frac": ups / peak, "traffic": profile_traffic(cfg.name), "kernel_ms": kern_s * 1e3,
+         "peak_source": "derived: " + how}
+    if kern == "persist_f32_log_E32_W1":
+        # context (DESIGN.md §6.2): the instruction-issue bound of this kernel's measured
+        # mix (thread-instructions per update from ncu at C2)
+        ib = sms * clk * 1e6 * 128 / 25.5
+        r["issue_bound"] = ib / 1e9
+        r["frac_of_issue_bound"] = ups / ib
+    return r, hbm
 
 
 def load_peaks():
@@ -145,9 +205,12 @@ def profile_traffic(cfg_name):
 
 
 # ----------------------------------------------------------------------------- oracle legs
-def oracle_sample(cfg, pairs, iters):
-    """Time the oracle (as it stands) on a bounded sample; returns (updates, seconds)."""
+def oracle_sample(cfg, pairs, iters, n=None):
+    """Time the oracle (as it stands) on a bounded sample; returns (updates, seconds).
+    ``n`` shrinks the grid (same recipe) for untimed warm-up calls."""
     from oracle import sinkhorn
+    if n is not None:
+        cfg = dataclasses.replace(cfg, n=n, m=(n if cfg.ndim == 2 else 1))
     A, B = gi.batch(cfg, pairs)
     A64, B64 = A.astype(np.float64), B.astype(np.float64)
     t0 = time.perf_counter()
@@ -170,7 +233,8 @@ def oracle_cores():
 
 
 def sample_plan(cfg):
-    """Bounded oracle sample (about 10-30 s of CPU work) for the config."""
+    """Bounded oracle sample (about 10-30 s of CPU work) for the config (C3: one
+    iteration of the plain-C LSE recursion over all 2^24 points, ~7 s)."""
     if cfg.name == "c2":
         return list(range(256)), cfg.itr_max, "256 of 4096 pairs, all 500 iterations, dense fp64 (BLAS)"
     if cfg.name == "c5":
@@ -199,11 +263,13 @@ def run_reference(args, cfg):
         return
     _limits = host_threads()  # noqa: F841 (kept alive for the run)
     pairs, iters, what = sample_plan(cfg)
-    oracle_sample(cfg, pairs[:1], 1)          # warm-up (builds the C oracle, BLAS threads)
+    # warm-up steps: the same oracle on a short prefix of the workload (builds the C
+    # oracle, starts the BLAS / OpenMP threads); the large configs' full sample would
+    # cost seconds per untimed step
+    for _ in range(max(1, args.warmup)):
+        oracle_sample(cfg, pairs[:1], 1, n=None if cfg.size <= 65536 else 256)
     times = []
     ups = 0
-    for _ in range(args.warmup):
-        oracle_sample(cfg, pairs[:2], 2)
     for _ in range(args.steps):
         u, t = oracle_sample(cfg, pairs, iters)
         ups, times = u, times + [t]
@@ -290,8 +356,13 @@ def run_fs1(args, cfg):
         dist.all_reduce(T, op=dist.ReduceOp.MAX)
     total_s = T.item() / 1e3
     it_run = int(iters.max().item())
-    updates_per_step_rank = cfg.size * it_run * B
-    value = ws * updates_per_step_rank * args.steps / total_s
+    # updates this rank did per step: N x (executed iterations) summed over its pairs
+    updates_per_step_rank = cfg.size * int(iters.to(torch.int64).sum().item())
+    U = torch.tensor([updates_per_step_rank], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(U, op=dist.ReduceOp.SUM)
+    updates_per_step = U.item()
+    value = updates_per_step * args.steps / total_s
     kern_avg_s = statistics.mean(kern_ms) / 1e3
 
     # ---- end-to-end through the public API with host buffers (pinned): every step copies
@@ -309,7 +380,8 @@ def run_fs1(args, cfg):
         ready = [torch.cuda.Event() for _ in range(2)]
         freed = [torch.cuda.Event() for _ in range(2)]
         kw = dict(h=cfg.h1, eps=cfg.eps, itr_max=cfg.itr_max, tol=cfg.tol, domain=cfg.domain,
-                  input_is_log=cfg.input_is_log, shape=shape, h2=cfg.h2 if cfg.ndim == 2 else None)
+                  input_is_log=cfg.input_is_log, shape=shape, h2=cfg.h2 if cfg.ndim == 2 else None,
+                  kernel=args.kernel)
 
         def issue_copy(k):
             with torch.cuda.stream(cs):
@@ -341,7 +413,7 @@ def run_fs1(args, cfg):
         Te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
         if ws > 1:
             dist.all_reduce(Te, op=dist.ReduceOp.MAX)
-        e2e = {"value": ws * updates_per_step_rank * args.steps / (Te.item() / 1e3), "unit": UNIT,
+        e2e = {"value": updates_per_step * args.steps / (Te.item() / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": int(ha.numel() * ha.element_size() + hb.numel() * hb.element_size()),
                "d2h_bytes_per_step": int(hcs[0].numel() * hcs[0].element_size()),
                "pipelined": "inputs of step k+1 copied on a second stream while step k solves"}
@@ -359,9 +431,8 @@ def run_fs1(args, cfg):
                            "n": cfg.n, "m": cfg.m, "iters": it_run, "domain": cfg.domain,
                            "kernel": info["kernel"], "parallelism": f"batch-sharded x{ws} (weak)",
                            "l2": "flushed between timed steps (256 MiB write, untimed)"},
-                "gpu_launches": args.steps * 1,
+                "gpu_launches": args.steps * launches_per_solve(info, B),
                 "clocks": clocks}
-        kern_ups = updates_per_step_rank / kern_avg_s
         if cfg.name in gi.PAPER_TABLE1_SECONDS:
             # the paper's own FS-1 number for this exact workload (Table 1, PAPER.md:371-373:
             # seconds per 1000-iteration trial on a 14-core Xeon Gold 5117, CPU): context
@@ -370,51 +441,12 @@ def run_fs1(args, cfg):
             table = "Table 1" if cfg.name.startswith("e1") else "Table 2"
             line["baseline"] = {"value": paper_ups, "unit": UNIT, "source": f"PAPER.md {table} (CPU, "
                                 "Xeon Gold 5117), N x iterations / seconds per trial", "hardware": "CPU"}
-        if info["kernel"].startswith("persist"):
-            clk_mhz = peaks.get("sm_max_mhz", 1965.0)
-            peak = alu_peak_updates(props.multi_processor_count, clk_mhz) / 1e9
-            line["roofline"] = {"bound": "alu", "achieved": kern_ups / 1e9, "peak": peak,
-                                "unit": "Gupdate/s", "frac": kern_ups / 1e9 / peak,
-                                "traffic": profile_traffic(cfg.name),
-                                "kernel_ms": kern_avg_s * 1e3,
-                                "peak_source": f"derived: {props.multi_processor_count} SMs x "
-                                               f"{clk_mhz:.0f} MHz x 16 MUFU/clk / 2 rcp per update",
-                                }
-            if info["kernel"] == "persist_f32_log_E32_W1":
-                # context: the instruction-issue bound of this kernel's
-                # measured mix (25.5 thread-instructions per update: smsp__inst_executed.sum
-                # x 32 / updates, ncu at C2, profiles/r01g_ncu_c2.txt)
-                ib = props.multi_processor_count * clk_mhz * 1e6 * 128 / 25.5
-                line["roofline"]["issue_bound"] = ib / 1e9
-                line["roofline"]["frac_of_issue_bound"] = kern_ups / ib
-        if info["kernel"].startswith("sep2dw"):
-            # K3w keeps its 64 MiB working set in L2 (measured DRAM traffic 0.4 GB per
-            # 300-iteration solve), so its bound is the MUFU pipe: per
-            # update 8 MUFU ops (ex2 in and lg2 out of each of the 4 line applies).
-            clk_mhz = peaks.get("sm_max_mhz", 1965.0)
-            peak = props.multi_processor_count * clk_mhz * 1e6 * MUFU_PER_SM_CLK / 8.0 / 1e9
-            line["roofline"] = {"bound": "alu", "achieved": kern_ups / 1e9, "peak": peak,
-                                "unit": "Gupdate/s", "frac": kern_ups / 1e9 / peak,
-                                "traffic": profile_traffic(cfg.name), "kernel_ms": kern_avg_s * 1e3,
-                                "peak_source": f"derived: {props.multi_processor_count} SMs x {clk_mhz:.0f} MHz "
-                                               f"x 16 MUFU/clk / 8 MUFU per update"}
-        elif info["kernel"].startswith(("stream", "sep2d")):
-            # HBM roofline: SURVEY.md §8(d)'s 6 words per update (read x,
-            # tgt and write y in both half-steps) x N x iterations; the once-per-solve
-            # prologue, exit check, cost and epilogue passes (16 words per point) are
-            # real traffic but not counted, so the fraction is conservative.
-            wb = 8 if cfg.dtype == "f64" else 4
-            alg = 6 * wb * cfg.size * it_run
-            peak = peaks.get("hbm_gbs", 6650.0)
-            ach = alg / kern_avg_s / 1e9
-            line["roofline"] = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
-                                "frac": ach / peak, "traffic": profile_traffic(cfg.name),
-                                "kernel_ms": kern_avg_s * 1e3, "algorithmic_bytes_per_launch": alg,
-                                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({src})"}
+        line["roofline"], line["hbm_gbs"] = roofline(cfg, info, updates_per_step_rank, it_run, B,
+                                                     kern_avg_s, peaks, src, props)
         line["e2e"] = e2e
         if not args.no_cpu_baseline:
             pairs, it, what = sample_plan(cfg)
-            oracle_sample(cfg, pairs[:1], 1)
+            oracle_sample(cfg, pairs[:1], 1, n=None if cfg.size <= 65536 else 256)   # warm-up
             u_, t_ = oracle_sample(cfg, pairs, it)
             line["cpu_baseline"] = {"value": u_ / t_, "unit": UNIT, "cores": oracle_cores(),
                                     "kind": "oracle", "sample": what, "seconds": t_}

@@ -346,8 +346,6 @@ void fill_persist_tables(PersistParams& P, double c, int E) {
   }
 }
 
-std::mutex g_attr_mu;
-
 // Dynamic shared memory of a persistent-kernel plan: the instantiation's own need.
 // (Padding it to trade resident CTAs for an even last wave was measured slower: the
 // kernel is latency-bound, so the extra resident warps of a full first wave win —
@@ -365,6 +363,9 @@ cudaError_t size_persist_smem(const PersistEntry* pe, long long batch, int devic
 }
 
 }  // namespace
+
+// serialises get/set-device around attribute and occupancy queries (also fs1_shard.cu)
+std::mutex g_attr_mu;
 
 extern "C" {
 

@@ -6,10 +6,13 @@
 #include <string.h>
 
 #include <algorithm>
+#include <mutex>
 #include <new>
 
 #include "../../include/fs1_shard.h"
 #include "fs1_shard.cuh"
+
+extern std::mutex g_attr_mu;  // fs1_api.cu: serialises get/set-device around attribute queries
 
 using namespace fs1;
 
@@ -126,9 +129,21 @@ fs1_status fs1_shard_plan(const fs1_desc* desc, int world, int rank, int device,
   // resident CTAs of the half-step kernel per SM (registers), one block each: a single
   // balanced wave over the SMs
   int occ = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)&shd::k_half<false, true>, 32 * shd::NW, 0) !=
-      cudaSuccess)
-    return FS1_ERR_CUDA;
+  {
+    // the occupancy query runs on the current device: make it `device` for the query
+    // (the same guard fs1_plan uses, fs1_api.cu)
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    int cur = -1;
+    cudaError_t e = cudaGetDevice(&cur);
+    if (e == cudaSuccess && cur != device) e = cudaSetDevice(device);
+    if (e == cudaSuccess)
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)&shd::k_half<false, true>, 32 * shd::NW, 0);
+    if (cur >= 0 && cur != device) cudaSetDevice(cur);
+    if (e != cudaSuccess) {
+      delete s;
+      return FS1_ERR_CUDA;
+    }
+  }
   occ = std::max(1, occ);
   P.TB = std::max(shd::NW, (int)((P.T + (long long)occ * sms - 1) / ((long long)occ * sms)));
   if (P.TB > shd::TBMAX) P.TB = shd::TBMAX;

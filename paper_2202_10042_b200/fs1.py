@@ -6,6 +6,7 @@ kernels behind the C ABI.  See DESIGN.md §1 for the boundary.
 """
 from __future__ import annotations
 
+import collections
 import ctypes
 import dataclasses
 
@@ -67,7 +68,7 @@ class Plan:
         if s != L.FS1_OK:
             raise L.FS1Error(s, "fs1_plan")
         self.workspace_bytes = ws.value
-        self._ws = None
+        self._ws = {}            # one workspace per CUDA stream (solves on two streams never share one)
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -88,13 +89,18 @@ class Plan:
                 "smem_bytes": pi.smem_bytes, "workspace_bytes": pi.workspace_bytes}
 
     def workspace(self):
-        if self.workspace_bytes and self._ws is None:
-            self._ws = torch.empty(self.workspace_bytes + 256, dtype=torch.uint8,
-                                   device=f"cuda:{self.device}")
-        if self._ws is None:
+        """This plan's workspace for the current stream of its device (allocated on first
+        use).  The grid-barrier counters and scratch vectors of the multi-CTA kernels live
+        there, so two streams running the same plan concurrently each get their own."""
+        if not self.workspace_bytes:
             return None
-        off = (-self._ws.data_ptr()) % 256
-        return self._ws[off:]
+        sid = torch.cuda.current_stream(self.device).cuda_stream
+        ws = self._ws.get(sid)
+        if ws is None:
+            ws = self._ws[sid] = torch.empty(self.workspace_bytes + 256, dtype=torch.uint8,
+                                             device=f"cuda:{self.device}")
+        off = (-ws.data_ptr()) % 256
+        return ws[off:]
 
     # raw entry points (tensors must be on this plan's device, contiguous)
     def solve_into(self, a, b, u, v, iters, err, flags, cost):
@@ -115,7 +121,8 @@ class Plan:
             raise L.FS1Error(s, "fs1_apply")
 
 
-_CACHE: dict = {}
+_CACHE: "collections.OrderedDict" = collections.OrderedDict()
+CACHE_PLANS = 16          # least-recently-used plans (and their workspaces) kept alive
 
 
 def plan(spec: Spec, device: int = 0) -> Plan:
@@ -123,16 +130,22 @@ def plan(spec: Spec, device: int = 0) -> Plan:
     p = _CACHE.get(key)
     if p is None:
         p = _CACHE[key] = Plan(spec, device)
+        while len(_CACHE) > CACHE_PLANS:
+            _CACHE.popitem(last=False)
+    else:
+        _CACHE.move_to_end(key)
     return p
 
 
-def _check(t, name, dtype, device, size):
+def _check(t, name, dtype, device, size, numel=None):
     if not isinstance(t, torch.Tensor) or t.device.type != "cuda":
         raise ValueError(f"{name} must be a CUDA tensor")
     if t.dtype != dtype or t.device.index != device or not t.is_contiguous():
         raise ValueError(f"{name}: expected contiguous {dtype} on cuda:{device}")
-    if t.numel() % size:
-        raise ValueError(f"{name}: numel {t.numel()} is not a multiple of {size}")
+    if t.numel() == 0 or t.numel() % size:
+        raise ValueError(f"{name}: numel {t.numel()} is not a positive multiple of {size}")
+    if numel is not None and t.numel() != numel:
+        raise ValueError(f"{name}: numel {t.numel()} != {numel} (one row per pair of a)")
 
 
 def solve(a, b, *, h, eps, itr_max, tol=0.0, domain="scaling", input_is_log=False,
@@ -146,7 +159,12 @@ def solve(a, b, *, h, eps, itr_max, tol=0.0, domain="scaling", input_is_log=Fals
         ndim, (n, m) = 2, shape
     size = n * m
     _check(a, "a", a.dtype, dev, size)
-    _check(b, "b", a.dtype, dev, size)
+    _check(b, "b", a.dtype, dev, size, a.numel())
+    if (u0 is None) != (v0 is None):
+        raise ValueError("warm start needs both u0 and v0 (or neither)")
+    if u0 is not None:
+        _check(u0, "u0", a.dtype, dev, size, a.numel())
+        _check(v0, "v0", a.dtype, dev, size, a.numel())
     batch = a.numel() // size
     spec = Spec(ndim=ndim, n=n, m=m, h1=float(h), h2=float(h2 if h2 is not None else (h if ndim == 2 else 0.0)),
                 eps=float(eps), batch=batch, dtype=a.dtype, domain=domain,
@@ -154,7 +172,8 @@ def solve(a, b, *, h, eps, itr_max, tol=0.0, domain="scaling", input_is_log=Fals
                 check_interval=int(check_interval), warm_start=u0 is not None, kernel=int(kernel))
     p = plan(spec, dev)
     if u0 is not None:
-        u, v = u0.clone(), v0.clone()
+        u = u0.clone(memory_format=torch.contiguous_format)
+        v = v0.clone(memory_format=torch.contiguous_format)
     else:
         u, v = torch.empty_like(a), torch.empty_like(b)
     iters = torch.empty(batch, dtype=torch.int32, device=a.device)
@@ -170,7 +189,7 @@ def cost(u, v, *, h, eps, domain="scaling", shape=None, h2=None, kernel=0):
     ndim, n, m = (1, u.shape[-1], 1) if shape is None else (2, *shape)
     size = n * m
     _check(u, "u", u.dtype, dev, size)
-    _check(v, "v", u.dtype, dev, size)
+    _check(v, "v", u.dtype, dev, size, u.numel())
     batch = u.numel() // size
     spec = Spec(ndim=ndim, n=n, m=m, h1=float(h), h2=float(h2 if h2 is not None else (h if ndim == 2 else 0.0)),
                 eps=float(eps), batch=batch, dtype=u.dtype, domain=domain, itr_max=0, kernel=int(kernel))
@@ -199,7 +218,7 @@ def transport_plan(u, v, *, h, eps, domain="scaling", shape=None, h2=None):
     ndim, n, m = (1, u.shape[-1], 1) if shape is None else (2, *shape)
     size = n * m
     _check(u, "u", u.dtype, dev, size)
-    _check(v, "v", u.dtype, dev, size)
+    _check(v, "v", u.dtype, dev, size, u.numel())
     batch = u.numel() // size
     spec = Spec(ndim=ndim, n=n, m=m, h1=float(h), h2=float(h2 if h2 is not None else (h if ndim == 2 else 0.0)),
                 eps=float(eps), batch=batch, dtype=u.dtype, domain=domain, itr_max=0)

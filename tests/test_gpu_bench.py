@@ -26,7 +26,7 @@ def _line(*args):
     return json.loads(lines[0])
 
 
-@pytest.mark.parametrize("cfg", ["c1", "c4"])
+@pytest.mark.parametrize("cfg", ["c1", "c3", "c4"])
 def test_bench_line_keys(cfg):
     d = _line("--config", cfg, "--steps", "2", "--warmup", "3")
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
@@ -37,14 +37,25 @@ def test_bench_line_keys(cfg):
     assert d["value"] > 0 and d["ms_per_step"] > 0 and d["config"]["workload"] == cfg
     assert "l2" in d["config"]
     r = d["roofline"]
-    assert r["bound"] in ("hbm", "tensor", "alu") and 0 < r["frac"] < 1 and r["peak"] > 0
-    assert abs(r["achieved"] / r["peak"] - r["frac"]) < 1e-9
+    if cfg == "c1":   # one pair on one SM: latency-bound, reported per iteration
+        assert r["bound"] == "latency" and r["unit"] == "us/iteration" and r["achieved"] > 0
+    else:             # the streaming kernels: HBM roofline, both denominators
+        assert r["bound"] == "hbm" and 0 < r["frac"] < 1 and r["peak"] > 0
+        assert abs(r["achieved"] / r["peak"] - r["frac"]) < 1e-9
+        assert abs(r["achieved"] / 8000.0 - r["frac_nominal"]) < 1e-9
+        assert d["hbm_gbs"] == pytest.approx(r["achieved"])
     cb = d["cpu_baseline"]
     assert cb["kind"] == "oracle" and cb["value"] > 0 and cb["cores"] >= 1 and cb["sample"]
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     assert d["gpu_launches"] >= d["steps"]
     assert set(d["clocks"]) >= {"sm_mhz", "sm_max_mhz", "reasons"}
+
+
+def test_bench_default_is_c3():
+    """The driver's line (no --config) is the largest single-GPU config, C3."""
+    d = _line("--steps", "1", "--warmup", "3", "--no-cpu-baseline", "--no-e2e")
+    assert d["config"]["workload"] == "c3" and d["roofline"]["bound"] == "hbm"
 
 
 def test_bench_reference_arm():
