@@ -155,3 +155,32 @@ double fs1o_sum_exp2(const double* A, const double* B, long n) {
   }
   return (double)s;
 }
+
+/* fs1o_stab_sweep : Remark 3.2's replacement lines, the
+ *                   paper's log-domain-stabilised recursion, in plain fp64.
+ *   With the absorbed potentials read as alpha <- alpha + eps ln phi (DESIGN.md
+ *   R8) and passed divided by eps (own = beta/eps, other = alpha/eps for lines
+ *   5-6, the psi half-step; own = alpha/eps, other = beta/eps for lines 10-11,
+ *   the phi half-step):
+ *     r_1     = e^{other_1 + own_1} x_1                       (line 3, rescaled: R29)
+ *     r_{i+1} = lam e^{own_{i+1} - own_i} r_i + e^{other_{i+1} + own_{i+1}} x_{i+1}     (line 5 / 10)
+ *     s_N     = 0
+ *     s_{N-i} = lam e^{own_{N-i} - own_{N-i+1}} (s_{N-i+1} + e^{other_{N-i+1} + own_{N-i+1}} x_{N-i+1})
+ *                                                                                      (line 6 / 11)
+ *     y = r + s  (= diag(e^own) K diag(e^other) x, the rescaled kernel of Remark 2.1)
+ * Each factor is formed exactly as printed: lam * exp(difference), exp(sum). */
+void fs1o_stab_sweep(const double* x, const double* own, const double* other, long n, double lam,
+                     double* y) {
+  double* r = (double*)malloc(sizeof(double) * n);
+  double* s = (double*)malloc(sizeof(double) * n);
+  r[0] = exp(other[0] + own[0]) * x[0];
+  s[n - 1] = 0.0;
+  for (long i = 1; i <= n - 1; ++i) {            /* for i = 1 : N-1 (1-based) */
+    r[i] = lam * exp(own[i] - own[i - 1]) * r[i - 1] + exp(other[i] + own[i]) * x[i];
+    long k = n - 1 - i;                          /* 0-based index of s_{N-i} */
+    s[k] = lam * exp(own[k] - own[k + 1]) * (s[k + 1] + exp(other[k + 1] + own[k + 1]) * x[k + 1]);
+  }
+  for (long i = 0; i < n; ++i) y[i] = r[i] + s[i];
+  free(r);
+  free(s);
+}

@@ -34,6 +34,7 @@ def lib():
         _lib.fs1o_sweep_scaling.argtypes = [p, l, l, l, l, d, p]
         _lib.fs1o_sweep_log.argtypes = [p, l, l, l, l, d, p]
         _lib.fs1o_wsweep_log.argtypes = [p, l, l, l, l, d, d, p]
+        _lib.fs1o_stab_sweep.argtypes = [p, p, p, l, d, p]
         _lib.fs1o_sum_exp2.argtypes = [p, p, l]
         _lib.fs1o_sum_exp2.restype = d
     return _lib
@@ -80,3 +81,13 @@ def wsweep_log(X, c, h, axis=1):
 def sum_exp2(A, B) -> float:
     A, B = _c(A).ravel(), _c(B).ravel()
     return float(lib().fs1o_sum_exp2(A.ctypes.data, B.ctypes.data, A.size))
+
+
+def stab_sweep(x, own, other, lam):
+    """Remark 3.2's recursions: diag(e^own) K diag(e^other) x with only
+    neighbour-difference exponentials; own/other are the absorbed potentials divided by eps."""
+    x, own, other = _c(x), _c(own), _c(other)
+    y = np.empty_like(x)
+    lib().fs1o_stab_sweep(x.ctypes.data, own.ctypes.data, other.ctypes.data, x.size, float(lam),
+                          y.ctypes.data)
+    return y
