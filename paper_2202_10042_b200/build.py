@@ -8,8 +8,11 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-OBJ = os.path.join(HERE, "_build")
-LIB = os.path.join(HERE, "libfs1.so")
+# variant builds for A/B measurements (tools/variant.sh): extra nvcc flags and a separate
+# object directory / library path; the product build uses neither
+OBJ = os.environ.get("FS1_OBJ_DIR") or os.path.join(HERE, "_build")
+LIB = os.environ.get("FS1_BUILD_OUT") or os.path.join(HERE, "libfs1.so")
+EXTRA = os.environ.get("FS1_NVCC_EXTRA", "").split()
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-O2"]
@@ -40,7 +43,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
 
     def run(job):
         src, obj = job
-        cmd = [NVCC, *FLAGS, "-c", src, "-o", obj]
+        cmd = [NVCC, *FLAGS, *EXTRA, "-c", src, "-o", obj]
         if verbose:
             print(" ".join(cmd), flush=True)
         r = subprocess.run(cmd, capture_output=True, text=True)

@@ -134,6 +134,13 @@ template <class T> __device__ __forceinline__ ER<T> shfl_down_er(ER<T> a, int d)
   return r;
 }
 
+template <class T> __device__ __forceinline__ ER<T> shfl_idx_er(ER<T> a, int src) {
+  ER<T> r;
+  r.m = __shfl_sync(FULL, a.m, src);
+  r.e = __shfl_sync(FULL, a.e, src);
+  return r;
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);

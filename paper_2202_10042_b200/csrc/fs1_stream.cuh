@@ -388,13 +388,11 @@ __device__ __forceinline__ void block_tile_scan(Ctx& c, double* Fm, int* Fe, dou
   }
   mx = warp_max(mx);
   mn = warp_min(mn);
-  int* wi = c.rede + 384;
-  __syncthreads();
+  int* wi = c.rede + 384;  // (callers enter after a block synchronisation)
   if (lane == 0) { wi[warp] = mx; wi[32 + warp] = mn; }
   __syncthreads();
-  mx = ZE;
-  mn = 0x7fffffff;
-  for (int w = 0; w < c.NW; ++w) { mx = max(mx, wi[w]); mn = min(mn, wi[32 + w]); }
+  mx = warp_max(lane < c.NW ? wi[lane] : ZE);
+  mn = warp_min(lane < c.NW ? wi[32 + lane] : 0x7fffffff);
   if (mx != ZE && mn < mx - 900) {
     block_tile_scan_er(c, Fm, Fe, Bm, Be, totF, totB);
     return;
@@ -427,13 +425,26 @@ __device__ __forceinline__ void block_tile_scan(Ctx& c, double* Fm, int* Fe, dou
   double* wG = c.redm + 64;
   int* wFs = c.rede + 128;
   int* wGs = c.rede + 192;
-  __syncthreads();
   if (lane == 31) { wF[warp] = F; wFs[warp] = sF; }
   if (lane == 0) { wG[warp] = G; wGs[warp] = sG; }
   __syncthreads();
-  double cw = 0.0, cg = 0.0;
-  for (int w = 0; w < warp; ++w) cw = fma(cw, c.pwd[wFs[w]], wF[w]);
-  for (int w = c.NW - 1; w > warp; --w) cg = fma(cg, c.pwd[wGs[w]], wG[w]);
+  // carries from the other warps: every warp scans the NW warp totals across its lanes
+  // (lane j <-> warp j; 5 shuffle levels instead of a serial loop over the warps)
+  double xF = 0.0, xG = 0.0;
+  int xsF = 0, xsG = 0;
+  if (lane < c.NW) { xF = wF[lane]; xsF = wFs[lane]; xG = wG[lane]; xsG = wGs[lane]; }
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const double uf = __shfl_up_sync(FULL, xF, d);
+    const int us = __shfl_up_sync(FULL, xsF, d);
+    const double dg = __shfl_down_sync(FULL, xG, d);
+    const int ds = __shfl_down_sync(FULL, xsG, d);
+    if (lane >= d) { xF = fma(uf, c.pwd[xsF], xF); xsF += us; }
+    if (lane + d < 32) { xG = fma(dg, c.pwd[xsG], xG); xsG += ds; }
+  }
+  // exclusive: the warps before (after) this one
+  const double cw = warp > 0 ? __shfl_sync(FULL, xF, warp - 1) : 0.0;
+  const double cg = warp + 1 < c.NW ? __shfl_sync(FULL, xG, warp + 1) : 0.0;
   double cf = fma(cw, c.pwd[esF], eF);
   double cb = fma(cg, c.pwd[esG], eG);
   for (int i = i0; i < i1; ++i) {
@@ -448,13 +459,10 @@ __device__ __forceinline__ void block_tile_scan(Ctx& c, double* Fm, int* Fe, dou
     Bm[i] = o.m; Be[i] = o.e;
     cb = fma(cb, L1, t);
   }
-  __syncthreads();
-  if (c.tid == NT - 1) { wF[0] = cf; }
-  if (c.tid == 0) { wG[0] = cb; }
-  __syncthreads();
-  totF = er_norm<double>(wF[0], M);
-  totB = er_norm<double>(wG[0], M);
-  __syncthreads();
+  // range totals: the forward one is the inclusive value at the last warp's end (every
+  // warp has it: lane NW-1 of the cross-warp scan), the backward one at warp 0's start
+  totF = er_norm<double>(__shfl_sync(FULL, xF, c.NW - 1), M);
+  totB = er_norm<double>(__shfl_sync(FULL, xG, 0), M);
 }
 
 // Deterministic block sum (fixed tree) of per-tile ER values vm/ve[0..nt).
@@ -536,6 +544,72 @@ __device__ __forceinline__ void tile_carries(Ctx& c, const StreamParams& P, int 
     c.Rr[i] = R;
   }
   __syncthreads();
+}
+
+// After the grid barrier: thread k reads range k's published (totals, error share, flag)
+// of slot `par` (all loads in flight at once) and decays the other ranges' totals by the
+// precomputed lambda^{256 d_k}; per-warp partial sums go through shared memory (one block
+// synchronisation); then every warp folds them in the same fixed order (identical values
+// in all warps: the external carries, the error sum, the OR of the flags) and forms the
+// full carries of its own tiles of the consumed vector (tables F/B hold its local
+// exclusive carries, Xx its tile exponents) for the next stream_half, with no second
+// block synchronisation.
+__device__ __forceinline__ void warp_step_in(Ctx& c, const StreamParams& P, int par, const double* Fm, const int* Fe,
+                                             const double* Bm, const int* Be, const int* Xx, double& err,
+                                             int& flag) {
+  const double* gt = P.gtot + (size_t)par * P.G * 4;
+  const int* ge = P.gtote + (size_t)par * P.G * 4;
+  ER<double> f = er_zero<double>(), b = er_zero<double>();
+  double es = 0.0;
+  int fl = 0;
+  const int k = c.tid;
+  if (k < P.G) {
+    es = __ldcg(gt + 4 * k + 2);
+    fl = __ldcg(ge + 4 * k + 2);
+    if (k != c.r) {
+      const ER<double> dp{c.dpm[k], c.dpe[k]};
+      if (k < c.r) f = er_mul(dp, ER<double>{__ldcg(gt + 4 * k), __ldcg(ge + 4 * k)});
+      else b = er_mul(dp, ER<double>{__ldcg(gt + 4 * k + 1), __ldcg(ge + 4 * k + 1)});
+    }
+  }
+  f = warp_er_sum(f);
+  b = warp_er_sum(b);
+  es = warp_sum(es);
+  fl = __reduce_or_sync(FULL, (unsigned)fl);
+  double* wm = c.redm + 700;  // scratch used by nothing else in the solve loop
+  int* we = c.rede + 700;
+  if (c.lane == 0) {
+    wm[3 * c.warp] = f.m; we[3 * c.warp] = f.e;
+    wm[3 * c.warp + 1] = b.m; we[3 * c.warp + 1] = b.e;
+    wm[3 * c.warp + 2] = es; we[3 * c.warp + 2] = fl;
+  }
+  __syncthreads();
+  // lane j takes warp j's partials; fixed-tree warp sums (the same in every warp)
+  ER<double> xf = er_zero<double>(), xb = er_zero<double>();
+  double xs = 0.0;
+  int xl = 0;
+  if (c.lane < c.NW) {
+    const int j = c.lane;
+    xf = ER<double>{wm[3 * j], we[3 * j]};
+    xb = ER<double>{wm[3 * j + 1], we[3 * j + 1]};
+    xs = wm[3 * j + 2];
+    xl = we[3 * j + 2];
+  }
+  const ER<double> CFx = warp_er_sum(xf), CBx = warp_er_sum(xb);
+  err = warp_sum(xs);
+  flag = __reduce_or_sync(FULL, (unsigned)xl);
+  for (int i = c.warp + c.lane * c.NW; i < c.nt; i += 32 * c.NW) {
+    const ER<double> CF = er_fma(pw(c, i), CFx, ER<double>{Fm[i], Fe[i]});
+    const ER<double> CB = er_fma(pw(c, c.nt - 1 - i), CBx, ER<double>{Bm[i], Be[i]});
+    const int X = Xx[i];
+    int R = X;
+    if (X == ZE || CF.e - X > LIM || CB.e - X > LIM) R = max(CF.e, CB.e);
+    if (R == ZE) R = 0;
+    c.cfr[i] = er_rel(CF, R);
+    c.cbr[i] = er_rel(CB, R);
+    c.Rr[i] = R;
+  }
+  __syncwarp();
 }
 
 // ---------------------------------------------------------------- streamed half-step
@@ -1205,14 +1279,17 @@ __global__ void __launch_bounds__(32 * NW, 1) fs1_stream_kernel(const __grid_con
   int l = 0, qi = 0, flag = 0;
   bool pre = false;
   double errv = NAN;
+  {
+    double e;
+    int f;
+    warp_step_in(c, P, par, c.PFm, c.PFe, c.PBm, c.PBe, c.PX, e, f);
+  }
   while (true) {
     const bool check = (l >= P.itr_max) || (use_tol && (l % P.check_interval) == 0);
     const bool last = l >= P.itr_max;
     // ---- lines 2-7: psi = b ./ (K^T phi), with the marginal error on check iterations
     unsigned long long* td = (P.tdbg && c.tid == 0 && l < 64) ? P.tdbg + ((size_t)c.r * 64 + l) * 8 : nullptr;
     if (td) td[0] = gtimer();
-    tile_carries(c, P, par, c.PFm, c.PFe, c.PBm, c.PBe, c.PX, td);
-    if (td) td[1] = gtimer();
     const int qo = check ? (qi ^ 1) : qi;  // a checking step keeps psi^(l) in Qm[qi]
     double* Qi = qi ? P.Qm1 : P.Qm0;
     int* QXi = qi ? c.QX1 : c.QX0;
@@ -1226,6 +1303,7 @@ __global__ void __launch_bounds__(32 * NW, 1) fs1_stream_kernel(const __grid_con
     else stream_half<NW, S, true, true, false>(c, P, A, nonfinite, pre);
     pre = !check;
     __syncthreads();
+    if (td) td[1] = gtimer();
     if (td) td[2] = gtimer();
     {
       ER<double> tF = er_zero<double>(), tB = er_zero<double>();
@@ -1253,7 +1331,10 @@ __global__ void __launch_bounds__(32 * NW, 1) fs1_stream_kernel(const __grid_con
     {
       double e;
       int f;
-      read_slot(c, P, par, e, f);
+      // err / flags of this step and the carries of psi for the phi step (which reads
+      // Qm[qo]: on a check that continues, qi flips to qo)
+      warp_step_in(c, P, par, c.QFm, c.QFe, c.QBm, c.QBe, QXo, e, f);
+      if (td) td[4] = gtimer();
       if (check) {
         errv = e;
         if (last || errv <= P.tol) {
@@ -1270,7 +1351,6 @@ __global__ void __launch_bounds__(32 * NW, 1) fs1_stream_kernel(const __grid_con
     // ---- lines 8-12: phi = a ./ (K psi)
     double* Qc = qi ? P.Qm1 : P.Qm0;
     int* QXc = qi ? c.QX1 : c.QX0;
-    tile_carries(c, P, par, c.QFm, c.QFe, c.QBm, c.QBe, QXc);
     HalfArgs B{Qc, QXc, P.Am, c.AX, nullptr, nullptr, P.Pm, c.PX, c.PFm, c.PBm, c.PFe, c.PBe, c.tzA};
     nonfinite = 0;
     stream_half<NW, S, true, false, true>(c, P, B, nonfinite, pre, P.Pm, P.Bm);
@@ -1285,7 +1365,7 @@ __global__ void __launch_bounds__(32 * NW, 1) fs1_stream_kernel(const __grid_con
       par ^= 1;
       double e;
       int f;
-      read_slot(c, P, par, e, f);
+      warp_step_in(c, P, par, c.PFm, c.PFe, c.PBm, c.PBe, c.PX, e, f);
       ++l;  // line 13
       if (f) {
         drain_prefetch<NW, S>(c);

@@ -21,16 +21,14 @@ lib.fs1__set_stream_timers(p._h, ctypes.c_void_p(buf.data_ptr()))
 o = fs1.solve(A, B, **kw); torch.cuda.synchronize()
 t = buf.cpu().numpy().reshape(G, 64, 8).astype(np.float64)
 t = t[:, 5:59]  # steady state
-carries = t[:, :, 1] - t[:, :, 0]
-stream = t[:, :, 2] - t[:, :, 1]
-scan = t[:, :, 3] - t[:, :, 2]
+# stamps (thread 0): [0] loop top, [1] stream done (block synced), [3] tile scan + publish
+# done, [4] grid barrier passed + warp 0's fold and tile carries done
+stream = t[:, :, 1] - t[:, :, 0]
+scan = t[:, :, 3] - t[:, :, 1]
+wait_fold = t[:, :, 4] - t[:, :, 3]
 step = t[:, 1:, 0] - t[:, :-1, 0]   # psi-start to next psi-start = full iteration
-waitb = t[:, :, 0] - 0
-# barrier wait: from my publish to the next psi start is phi step + barrier; report slowest CTA stream
-print(f"CTAs {G}; per psi half-step (us): carries {np.median(carries)/1e3:.2f}  stream med {np.median(stream)/1e3:.2f} "
-      f"max {np.median(stream.max(0))/1e3:.2f} min {np.median(stream.min(0))/1e3:.2f}  scan+publish {np.median(scan)/1e3:.2f}  "
-      f"iteration {np.median(step)/1e3:.2f}")
-ext = t[:, :, 4] - t[:, :, 0]
-sync1 = t[:, :, 5] - t[:, :, 4]
-tiles = t[:, :, 1] - t[:, :, 5]
-print(f"  carries split (us): ext fold {np.median(ext)/1e3:.2f}  first sync {np.median(sync1)/1e3:.2f}  per-tile {np.median(tiles)/1e3:.2f}")
+med = lambda x: np.median(x) / 1e3
+print(f"CTAs {G}; psi half-step (us): stream med {med(stream):.2f} max {med(stream.max(0)):.2f} "
+      f"min {med(stream.min(0)):.2f} | tile scan+publish {med(scan):.2f} | barrier+fold {med(wait_fold):.2f} "
+      f"| iteration {med(step):.2f}")
+print("  per-CTA stream (us): p10 %.2f p50 %.2f p90 %.2f" % tuple(np.percentile(stream, [10, 50, 90]) / 1e3))

@@ -31,12 +31,13 @@ __global__ void kern(float* out, double* outd, int iters, float m, float c, doub
   for (int it = 0; it < iters; ++it) {
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      if (OP == 0) asm volatile("rcp.approx.ftz.f32 %0, %0;" : "+f"(a[i]));
+      // rcp is an involution: ptxas folds rcp(rcp(x)) pairs, so each step adds c (FMA pipe)
+      if (OP == 0) asm volatile("rcp.approx.ftz.f32 %0, %0;\n\tadd.ftz.f32 %0, %0, %1;" : "+f"(a[i]) : "f"(c));
       if (OP == 1) asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(a[i]));
       if (OP == 2) asm volatile("lg2.approx.ftz.f32 %0, %0;" : "+f"(a[i]));
       if (OP == 3) a[i] = fmaf(a[i], m, c);
       if (OP == 4) d[i] = fma(d[i], md, cd);
-      if (OP == 5) asm volatile("rcp.approx.ftz.f64 %0, %0;" : "+d"(d[i]));
+      if (OP == 5) asm volatile("rcp.approx.ftz.f64 %0, %0;\n\tadd.f64 %0, %0, %1;" : "+d"(d[i]) : "d"(cd));
       if (OP == 6) d[i] = __drcp_rn(d[i]);
     }
   }
