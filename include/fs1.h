@@ -46,7 +46,7 @@
 extern "C" {
 #endif
 
-#define FS1_ABI_VERSION 1
+#define FS1_ABI_VERSION 2
 
 typedef enum {
   FS1_OK = 0,
@@ -68,8 +68,18 @@ typedef enum { FS1_F32 = 0, FS1_F64 = 1 } fs1_dtype;
  *              / Remark 3.2 carried out every
  *              half-step in exact powers of two.  It never
  *              overflows and matches the log-sum-exp iteration of the
- *              north star to rounding.                                         */
-typedef enum { FS1_SCALING = 0, FS1_LOG = 1 } fs1_domain;
+ *              north star to rounding.
+ * FS1_STABILIZED: the paper's own log-domain stabilisation (Remark 2.1 +
+ *              Remark 3.2): the scaling-domain
+ *              iteration on the rescaled kernel diag(e^{alpha/eps}) K
+ *              diag(e^{beta/eps}) evaluated by the variable-coefficient
+ *              recursions of Remark 3.2, with the absorption alpha += eps ln phi,
+ *              beta += eps ln psi, phi = psi = 1 whenever max(|phi|, |psi|) >
+ *              desc.tau after a full iteration (R8, R29, R30).  u, v hold
+ *              F = alpha/eps + ln phi, G = beta/eps + ln psi (as FS1_LOG).  1D, fp64,
+ *              n <= FS1_MAX_STAB, no warm start; fs1_apply is unsupported.       */
+typedef enum { FS1_SCALING = 0, FS1_LOG = 1, FS1_STABILIZED = 2 } fs1_domain;
+#define FS1_MAX_STAB 8192
 
 /* per-problem flags (bit set) */
 #define FS1_FLAG_CONVERGED 1  /* stopped because err <= tol (tol > 0)               */
@@ -91,6 +101,8 @@ typedef struct {
                             0 = fixed iterations (the paper's §5 protocol)     */
   int32_t check_interval;/* >= 1: the error is evaluated when l % check_interval == 0       */
   int32_t warm_start;    /* 1: u, v hold the initial phi, psi (LOG: F, G); 0: 1/(n m)        */
+  double tau;            /* FS1_STABILIZED: absorption threshold (> 1; 0 selects 1e10, the
+                            reading of the unstated tau, R30); ignored otherwise   */
 } fs1_desc;
 
 typedef struct fs1_plan_s fs1_plan_t;

@@ -13,7 +13,7 @@ LIB_PATH = os.environ.get("FS1_LIB") or os.path.join(HERE, "libfs1.so")  # FS1_L
 
 FS1_OK, FS1_ERR_ARG, FS1_ERR_EPS, FS1_ERR_UNSUPPORTED, FS1_ERR_CUDA, FS1_ERR_WORKSPACE = range(6)
 FS1_F32, FS1_F64 = 0, 1
-FS1_SCALING, FS1_LOG = 0, 1
+FS1_SCALING, FS1_LOG, FS1_STABILIZED = 0, 1, 2
 FLAG_CONVERGED, FLAG_NONFINITE, FLAG_ITR_MAX = 1, 2, 4
 
 EXPORTS = ["fs1_plan", "fs1_solve", "fs1_cost", "fs1_apply", "fs1_transport_plan", "fs1_plan_info",
@@ -41,6 +41,7 @@ class Desc(ctypes.Structure):
         ("tol", ctypes.c_double),
         ("check_interval", ctypes.c_int32),
         ("warm_start", ctypes.c_int32),
+        ("tau", ctypes.c_double),
     ]
 
 

@@ -24,6 +24,8 @@ struct fs1_plan_s {
   const StreamEntry* se;
   StreamParams sbase;  // K2: scalars + multiplier tables; pointers filled per call
   Sep2dParams tbase;   // K3
+  const StabEntry* ke = nullptr;  // K4 stabilised kernel
+  StabParams kbase;
   int grid;            // K2 / K3: co-resident CTAs
   const Sep2dwEntry* sw = nullptr;  // K3w solve kernel (nullptr: K3)
   int gridw = 0;                    // K3w co-resident CTAs
@@ -37,6 +39,7 @@ namespace {
 constexpr int KIND_PERSIST = 0;
 constexpr int KIND_STREAM = 1;
 constexpr int KIND_SEP2D = 2;
+constexpr int KIND_STAB = 3;
 void er_pow(long double c, long double L, double* m, int* e);
 void fill_persist_tables(PersistParams& P, double c, int E);
 constexpr int TILE = 256;
@@ -393,7 +396,8 @@ static fs1_status plan_impl(const fs1_desc* desc, int device, int force, fs1_pla
   if (!(d.tol >= 0.0) || !isfinite(d.tol)) return FS1_ERR_ARG;
   if (d.ndim == 1 && d.m != 1) return FS1_ERR_ARG;
   if (d.dtype != FS1_F32 && d.dtype != FS1_F64) return FS1_ERR_ARG;
-  if (d.domain != FS1_SCALING && d.domain != FS1_LOG) return FS1_ERR_ARG;
+  if (d.domain != FS1_SCALING && d.domain != FS1_LOG && d.domain != FS1_STABILIZED) return FS1_ERR_ARG;
+  if (d.domain == FS1_STABILIZED && !(d.tau == 0.0 || (d.tau > 1.0 && isfinite(d.tau)))) return FS1_ERR_ARG;
   if (!(d.eps > 0.0) || !isfinite(d.eps) || !(d.h1 > 0.0) || !isfinite(d.h1)) return FS1_ERR_EPS;
   if (d.ndim == 2 && (!(d.h2 > 0.0) || !isfinite(d.h2))) return FS1_ERR_EPS;
   if (d.batch > 0x7fffffffLL) return FS1_ERR_UNSUPPORTED;
@@ -405,7 +409,52 @@ static fs1_status plan_impl(const fs1_desc* desc, int device, int force, fs1_pla
   const bool logd = d.domain == FS1_LOG;
   const double c = d.h1 / d.eps;
 
-  if (d.ndim == 1 && (force == 2 || (force >= 10 && force < 20))) {
+  if (d.domain == FS1_STABILIZED) {
+    // K4: the paper's stabilised FS-1 (Remark 2.1 + 3.2), one CTA per problem
+    if (d.ndim != 1 || d.dtype != FS1_F64 || d.warm_start || d.n > FS1_MAX_STAB) {
+      delete p;
+      return FS1_ERR_UNSUPPORTED;
+    }
+    int cnt = 0;
+    const StabEntry* tab = stab_table(&cnt);
+    const StabEntry* best = nullptr;
+    for (int i = 0; i < cnt; ++i)
+      if (32LL * tab[i].W * tab[i].E >= d.n && (!best || 32 * tab[i].W * tab[i].E < 32 * best->W * best->E))
+        best = &tab[i];
+    if (!best) { delete p; return FS1_ERR_UNSUPPORTED; }
+    {
+      std::lock_guard<std::mutex> lk(g_attr_mu);
+      int cur = 0;
+      if (cudaGetDevice(&cur) != cudaSuccess) { delete p; return FS1_ERR_CUDA; }
+      if (cur != device && cudaSetDevice(device) != cudaSuccess) { delete p; return FS1_ERR_CUDA; }
+      const cudaError_t e =
+          cudaFuncSetAttribute(best->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)best->smem());
+      if (cur != device) cudaSetDevice(cur);
+      if (e != cudaSuccess) { delete p; return FS1_ERR_CUDA; }
+    }
+    p->kind = KIND_STAB;
+    p->ke = best;
+    StabParams& K = p->kbase;
+    memset(&K, 0, sizeof(K));
+    K.n = d.n;
+    K.lam = exp(-c);
+    K.h = d.h1;
+    K.tol = d.tol;
+    K.tau = d.tau == 0.0 ? 1e10 : d.tau;
+    K.itr_max = d.itr_max;
+    K.check_interval = d.check_interval;
+    K.input_is_log = d.input_is_log;
+    const long long P = 32LL * best->W * best->E;
+    p->ws = al256((size_t)d.batch * 9 * P * 8);
+    p->smem = best->smem();
+    snprintf(p->info.kernel, sizeof(p->info.kernel), "stab_f64_E%d_W%d", best->E, best->W);
+    p->info.chunk = best->E;
+    p->info.threads = 32 * best->W;
+    p->info.ctas_per_problem = 1;
+    p->info.grid = d.batch;
+    p->info.smem_bytes = p->smem;
+    p->info.workspace_bytes = p->ws;
+  } else if (d.ndim == 1 && (force == 2 || (force >= 10 && force < 20))) {
     std::lock_guard<std::mutex> lk(g_attr_mu);
     int cur = 0;
     if (cudaGetDevice(&cur) != cudaSuccess) { delete p; return FS1_ERR_CUDA; }
@@ -560,6 +609,14 @@ fs1_status fs1_solve(const fs1_plan_t* plan, const void* a, const void* b, void*
     cudaError_t e = plan->pe->launch_solve(P, plan->d.batch, plan->smem, (cudaStream_t)stream);
     return e == cudaSuccess ? FS1_OK : FS1_ERR_CUDA;
   }
+  if (plan->kind == KIND_STAB) {
+    StabParams P = plan->kbase;
+    P.a = a; P.b = b; P.u = u; P.v = v;
+    P.iters = iters; P.err = err; P.flags = flags; P.cost = cost;
+    P.ws = (double*)workspace;
+    P.mode = 0;
+    return plan->ke->launch(P, plan->d.batch, (cudaStream_t)stream) == cudaSuccess ? FS1_OK : FS1_ERR_CUDA;
+  }
   if (plan->kind == KIND_SEP2D) {
     const long long nm = plan->d.n * plan->d.m;
     for (long long k = 0; k < plan->d.batch; ++k) {
@@ -641,6 +698,15 @@ fs1_status fs1_cost(const fs1_plan_t* plan, const void* u, const void* v, double
     }
     return FS1_OK;
   }
+  if (plan->kind == KIND_STAB) {
+    // the return line on (alpha/eps, beta/eps) = (F, G), phi = psi = 1 (an absorbed state)
+    StabParams P = plan->kbase;
+    P.u = const_cast<void*>(u); P.v = const_cast<void*>(v);
+    P.cost = cost;
+    P.ws = (double*)workspace;
+    P.mode = 1;
+    return plan->ke->launch(P, plan->d.batch, (cudaStream_t)stream) == cudaSuccess ? FS1_OK : FS1_ERR_CUDA;
+  }
   return FS1_ERR_UNSUPPORTED;
 }
 
@@ -650,7 +716,7 @@ fs1_status fs1_transport_plan(const fs1_plan_t* plan, const void* u, const void*
   if (d.n * d.m > FS1_MAX_TPLAN) return FS1_ERR_UNSUPPORTED;
   const double c1 = d.h1 / d.eps, c2 = d.ndim == 2 ? d.h2 / d.eps : 0.0;
   const cudaError_t e = launch_tplan(d.dtype == FS1_F64 ? 1 : 0, u, v, gamma, d.batch, d.n, d.m, c1, c2,
-                                     d.domain == FS1_LOG ? 1 : 0, (cudaStream_t)stream);
+                                     d.domain != FS1_SCALING ? 1 : 0, (cudaStream_t)stream);
   return e == cudaSuccess ? FS1_OK : FS1_ERR_CUDA;
 }
 

@@ -49,6 +49,15 @@ struct Sep2dwEntry {
 };
 const Sep2dwEntry* sep2dw_table(int* count);
 
+// K4 stabilised FS-1 (fs1_stab.cu): one CTA of 32 W threads per problem, E points each
+struct StabEntry {
+  int E, W;
+  const void* fn;
+  size_t (*smem)();
+  cudaError_t (*launch)(const StabParams&, long long batch, cudaStream_t);
+};
+const StabEntry* stab_table(int* count);
+
 // transport-plan materialisation (fs1_tplan.cu)
 cudaError_t launch_tplan(int dtype, const void* u, const void* v, void* g, long long batch, long long n, long long m,
                          double c1, double c2, int logd, cudaStream_t st);

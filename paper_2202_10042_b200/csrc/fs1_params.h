@@ -159,3 +159,29 @@ struct ShardParams {
 };
 
 }  // namespace fs1
+
+namespace fs1 {
+
+// K4: the paper's stabilised FS-1 (Remark 2.1 + 3.2), fp64, one CTA per problem.
+struct StabParams {
+  const void* a;     // [batch][n] histograms (linear; log-weights when input_is_log)
+  const void* b;
+  void* u;           // [batch][n] out: F = alpha/eps + ln phi
+  void* v;           //               G = beta/eps + ln psi
+  int32_t* iters;
+  double* err;
+  int32_t* flags;
+  double* cost;
+  double* ws;        // [batch][9][T E] workspace (fs1_stab.cuh WN arrays)
+  long long n;
+  double lam;        // lambda = e^{-h/eps}
+  double h;
+  double tol;
+  double tau;        // absorption threshold (Remark 2.1)
+  int itr_max;
+  int check_interval;
+  int input_is_log;
+  int mode;          // 0 solve; 1 cost of the given (u, v) = (F, G)
+};
+
+}  // namespace fs1

@@ -15,6 +15,7 @@ import torch
 from . import _lib as L
 
 _DT = {torch.float32: L.FS1_F32, torch.float64: L.FS1_F64}
+_DOMAIN = {"scaling": L.FS1_SCALING, "log": L.FS1_LOG, "stabilized": L.FS1_STABILIZED}
 
 
 def _ptr(t):
@@ -41,14 +42,16 @@ class Spec:
     tol: float = 0.0
     check_interval: int = 1
     warm_start: bool = False
+    tau: float = 0.0         # "stabilized": absorption threshold (0 = the library default 1e10)
     kernel: int = 0          # 0 auto; test-only overrides (fs1__plan_kind in fs1_api.cu)
 
     def desc(self) -> L.Desc:
         return L.Desc(ndim=self.ndim, n=self.n, m=self.m, h1=self.h1, h2=self.h2, eps=self.eps,
                       batch=self.batch, dtype=_DT[self.dtype],
-                      domain=L.FS1_LOG if self.domain == "log" else L.FS1_SCALING,
+                      domain=_DOMAIN[self.domain],
                       input_is_log=int(self.input_is_log), itr_max=self.itr_max, tol=self.tol,
-                      check_interval=self.check_interval, warm_start=int(self.warm_start))
+                      check_interval=self.check_interval, warm_start=int(self.warm_start),
+                      tau=float(self.tau))
 
 
 class Plan:
@@ -149,9 +152,11 @@ def _check(t, name, dtype, device, size, numel=None):
 
 
 def solve(a, b, *, h, eps, itr_max, tol=0.0, domain="scaling", input_is_log=False,
-          check_interval=1, u0=None, v0=None, shape=None, h2=None, want_cost=True, kernel=0):
+          check_interval=1, u0=None, v0=None, shape=None, h2=None, want_cost=True, kernel=0, tau=0.0):
     """Batched FS-1 solve.  a, b: CUDA tensors [batch, n] (1D) or [batch, n*m] with
-    shape=(n, m) (2D, column-major).  Returns dict u, v, iters, err, flags, cost."""
+    shape=(n, m) (2D, column-major).  domain: "scaling" | "log" | "stabilized" (the
+    paper's Remark 2.1 / 3.2 stabilisation, absorption threshold tau).
+    Returns dict u, v, iters, err, flags, cost."""
     dev = a.device.index
     if shape is None:
         ndim, n, m = 1, a.shape[-1], 1
@@ -169,7 +174,8 @@ def solve(a, b, *, h, eps, itr_max, tol=0.0, domain="scaling", input_is_log=Fals
     spec = Spec(ndim=ndim, n=n, m=m, h1=float(h), h2=float(h2 if h2 is not None else (h if ndim == 2 else 0.0)),
                 eps=float(eps), batch=batch, dtype=a.dtype, domain=domain,
                 input_is_log=bool(input_is_log), itr_max=int(itr_max), tol=float(tol),
-                check_interval=int(check_interval), warm_start=u0 is not None, kernel=int(kernel))
+                check_interval=int(check_interval), warm_start=u0 is not None, kernel=int(kernel),
+                tau=float(tau))
     p = plan(spec, dev)
     if u0 is not None:
         u = u0.clone(memory_format=torch.contiguous_format)

@@ -26,7 +26,7 @@ def test_library_exports_every_header_symbol():
     assert set(names) == set(L.EXPORTS)
     for n in names:
         assert hasattr(lib, n), n
-    assert lib.fs1_abi_version() == 1
+    assert lib.fs1_abi_version() == 2
 
 
 def test_status_strings():
@@ -57,6 +57,13 @@ def _desc(**kw):
     (dict(h1=0.0), L.FS1_ERR_EPS),
     (dict(eps=float("inf")), L.FS1_ERR_EPS),
     (dict(ndim=2, m=4, h2=0.0), L.FS1_ERR_EPS),
+    (dict(domain=3), L.FS1_ERR_ARG),
+    (dict(domain=L.FS1_STABILIZED, dtype=L.FS1_F64, tau=0.5), L.FS1_ERR_ARG),      # tau must exceed 1
+    (dict(domain=L.FS1_STABILIZED, dtype=L.FS1_F64, tau=float("inf")), L.FS1_ERR_ARG),
+    (dict(domain=L.FS1_STABILIZED), L.FS1_ERR_UNSUPPORTED),                        # fp32
+    (dict(domain=L.FS1_STABILIZED, dtype=L.FS1_F64, ndim=2, m=4, h2=0.25), L.FS1_ERR_UNSUPPORTED),
+    (dict(domain=L.FS1_STABILIZED, dtype=L.FS1_F64, warm_start=1), L.FS1_ERR_UNSUPPORTED),
+    (dict(domain=L.FS1_STABILIZED, dtype=L.FS1_F64, n=8193), L.FS1_ERR_UNSUPPORTED),  # > FS1_MAX_STAB
 ])
 def test_plan_rejects_invalid(kw, status):
     lib = L.lib()
