@@ -130,7 +130,7 @@ def launches_per_solve(info, batch):
     """Library kernels one fs1_solve launches: K1 one launch for the whole batch; K2 and
     K3w / K3 one cooperative launch per problem (each preceded by a cudaMemsetAsync of
     its grid-barrier counter, which is not a kernel)."""
-    return 1 if info["kernel"].startswith("persist") else batch
+    return 1 if info["kernel"].startswith(("persist", "stab")) else batch
 
 
 def roofline(cfg, info, updates, it_run, batch, kern_s, peaks, src, props):
@@ -144,13 +144,14 @@ def roofline(cfg, info, updates, it_run, batch, kern_s, peaks, src, props):
     wb = 8 if cfg.dtype == "f64" else 4
     sms = props.multi_processor_count
     clk = peaks.get("sm_max_mhz", 1965.0)
-    if kern.startswith("persist"):
+    onchip = kern.startswith(("persist", "stab"))   # state on chip (K1, K4)
+    if onchip:
         alg = 4 * wb * cfg.size * batch
     else:
         alg = 6 * wb * updates
     hbm = alg / kern_s / 1e9
     ups = updates / kern_s
-    if not kern.startswith("persist"):
+    if not onchip:
         peak = peaks.get("hbm_gbs", 6650.0)
         r = {"bound": "hbm", "achieved": hbm, "peak": peak, "unit": "GB/s", "frac": hbm / peak,
              "traffic": profile_traffic(cfg.name), "kernel_ms": kern_s * 1e3,
@@ -214,7 +215,11 @@ def oracle_sample(cfg, pairs, iters, n=None):
     A, B = gi.batch(cfg, pairs)
     A64, B64 = A.astype(np.float64), B.astype(np.float64)
     t0 = time.perf_counter()
-    if cfg.ndim == 1 and cfg.n <= 8192:
+    if cfg.domain == "stabilized":
+        from oracle import stabilized
+        for p in range(len(pairs)):
+            stabilized.solve_stab(A64[p], B64[p], n=cfg.n, h=cfg.h1, eps=cfg.eps, itr_max=iters)
+    elif cfg.ndim == 1 and cfg.n <= 8192:
         sinkhorn.solve(A64, B64, n=cfg.n, h1=cfg.h1, eps=cfg.eps, itr_max=iters,
                        domain="scaling", input_is_log=cfg.input_is_log)
     else:
@@ -241,6 +246,9 @@ def sample_plan(cfg):
         return list(range(8)), 200, "8 pairs, 200 of 1000 iterations, dense fp64 (BLAS)"
     if cfg.name == "c1":
         return [0], 700, "1 pair, 700 iterations, dense fp64"
+    if cfg.name.startswith("e2s_"):
+        it = {500: 2000, 2000: 1000, 8000: 300}.get(cfg.n, 100)
+        return [0], it, f"1 of 100 pairs, {it} of {cfg.itr_max} iterations, the stabilised oracle (plain C recursions)"
     if cfg.name.startswith(("e1_", "e2_")):
         it = {500: 500, 2000: 50, 8000: 20}.get(cfg.n, 20)
         return [0], it, f"1 of 100 pairs, {it} of {cfg.itr_max} iterations, dense fp64"

@@ -100,6 +100,17 @@ for _k, _n in enumerate((500, 2000, 8000)):
         f"normalised with delta=1e-3, eps=1e-2, 500 iters, 100 repetitions, fp64 scaling domain",
         h=8.0 / (_n - 1), seed_index=21 + _k)
 
+# The paper's stabilisation study (Figure 1 right): the same Ricker pair at
+# eps = 1e-3, where the unstabilised iteration terminates abnormally; run with the paper's
+# own stabilisation (Remark 2.1 + 3.2, domain "stabilized", tau = 1e10) for 2000
+# iterations, 100 repetitions.  fp64.
+for _k, _n in enumerate((500, 2000, 8000)):
+    CONFIGS[f"e2s_{_n}"] = Config(
+        f"e2s_{_n}", 1, _n, 1, 100, "f64", "stabilized", 1e-3, 2000, 0.0, False,
+        f"paper E2 stabilisation study (PAPER.md:410): Ricker pair on [-4,4], N={_n}, eps=1e-3, "
+        f"2000 iters, 100 repetitions, the paper's stabilised FS-1 (absorption tau=1e10)",
+        h=8.0 / (_n - 1), seed_index=31 + _k)
+
 # the paper's FS-1 time per trial on its CPU (Xeon Gold 5117): Table 1 (PAPER.md:371-373,
 # 1000 iterations) and Table 2 (PAPER.md:422-424, 500 iterations); context for the paper
 # workload bench lines (updates/s = N x iterations / time)
@@ -228,7 +239,7 @@ def pair(cfg: Config | str, p: int, n: int | None = None):
                                   h=(6.0 / (n - 1) if cfg.h and n > 1 else cfg.h))
     idx = cfg.seed_index or int(cfg.name[1:])
     rng = pair_rng(idx, p)
-    if cfg.name.startswith("e2"):  # deterministic signals: every repetition is the same pair
+    if cfg.name.startswith("e2"):  # deterministic signals: every repetition is the same pair (e2, e2s)
         return ricker_pair(cfg.n)
     draw = _DRAW[cfg.name.split("_")[0]]
     a = draw(rng, cfg)
