@@ -144,7 +144,7 @@ def roofline(cfg, info, updates, it_run, batch, kern_s, peaks, src, props):
     wb = 8 if cfg.dtype == "f64" else 4
     sms = props.multi_processor_count
     clk = peaks.get("sm_max_mhz", 1965.0)
-    onchip = kern.startswith(("persist", "stab"))   # state on chip (K1, K4)
+    onchip = kern.startswith(("persist", "stab", "sep2d64"))   # one CTA per problem (K1, K4, K5)
     if onchip:
         alg = 4 * wb * cfg.size * batch
     else:

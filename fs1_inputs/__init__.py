@@ -40,6 +40,7 @@ class Config:
     description: str
     h: float = 0.0        # axis-1 spacing when not 1/n (E1: 6/(N-1) on [-3, 3])
     seed_index: int = 0   # seed_c = SEED_BASE + seed_index (0: the digit of "cK")
+    hh2: float = 0.0      # axis-2 spacing when not 1/m (E3: h2 = 1)
 
     @property
     def size(self) -> int:
@@ -51,6 +52,8 @@ class Config:
 
     @property
     def h2(self) -> float:
+        if self.hh2:
+            return self.hh2
         return 1.0 / self.m if self.ndim == 2 else 0.0
 
     @property
@@ -99,6 +102,16 @@ for _k, _n in enumerate((500, 2000, 8000)):
         f"paper E2 (Table 2): Ricker wavelet R(t) vs R(t+1.2032) on [-4,4], N={_n}, squared, "
         f"normalised with delta=1e-3, eps=1e-2, 500 iters, 100 repetitions, fp64 scaling domain",
         h=8.0 / (_n - 1), seed_index=21 + _k)
+
+# The paper's 2D random distributions (Table 3): N x N grids, h1 = h2 = 1,
+# the 1D recipe's iid U[0,1] weights normalised over the N^2 points, eps = 0.01 (so
+# lambda = e^{-100} on both axes), 1000 iterations, 100 trials (one batch of 100 pairs).
+# fp64 scaling domain, the paper's unstabilised FS-1 (Algorithm 2).
+for _k, _n in enumerate((10, 20, 40, 80, 160)):
+    CONFIGS[f"e3_{_n}"] = Config(
+        f"e3_{_n}", 2, _n, _n, 100, "f64", "scaling", 1e-2, 1000, 0.0, False,
+        f"paper E3 (Table 3): 100 trials, 2D {_n}x{_n}, h1=h2=1, u,v iid U[0,1] normalised, "
+        f"eps=1e-2, 1000 iters, fp64 scaling domain", h=1.0, seed_index=41 + _k, hh2=1.0)
 
 # The paper's stabilisation study (Figure 1 right): the same Ricker pair at
 # eps = 1e-3, where the unstabilised iteration terminates abnormally; run with the paper's
@@ -225,6 +238,7 @@ _DRAW = {
     "c4": lambda rng, cfg: _c4_loghist(rng, cfg.n, cfg.m),
     "c5": lambda rng, cfg: _c5_hist(rng, cfg.n),
     "e1": lambda rng, cfg: _e1_hist(rng, cfg.n),
+    "e3": lambda rng, cfg: _e1_hist(rng, cfg.n * cfg.m),
 }
 
 
@@ -236,7 +250,7 @@ def pair(cfg: Config | str, p: int, n: int | None = None):
         cfg = CONFIGS[cfg]
     if n is not None and n != cfg.n:
         cfg = dataclasses.replace(cfg, n=n, m=(n if cfg.ndim == 2 else 1),
-                                  h=(6.0 / (n - 1) if cfg.h and n > 1 else cfg.h))
+                                  h=(6.0 / (n - 1) if cfg.name.startswith("e1") and n > 1 else cfg.h))
     idx = cfg.seed_index or int(cfg.name[1:])
     rng = pair_rng(idx, p)
     if cfg.name.startswith("e2"):  # deterministic signals: every repetition is the same pair (e2, e2s)

@@ -26,6 +26,8 @@ struct fs1_plan_s {
   Sep2dParams tbase;   // K3
   const StabEntry* ke = nullptr;  // K4 stabilised kernel
   StabParams kbase;
+  Sep2d64Params dbase;            // K5 fp64 2D kernel
+  int threads = 0;
   int grid;            // K2 / K3: co-resident CTAs
   const Sep2dwEntry* sw = nullptr;  // K3w solve kernel (nullptr: K3)
   int gridw = 0;                    // K3w co-resident CTAs
@@ -40,6 +42,7 @@ constexpr int KIND_PERSIST = 0;
 constexpr int KIND_STREAM = 1;
 constexpr int KIND_SEP2D = 2;
 constexpr int KIND_STAB = 3;
+constexpr int KIND_SEP64 = 4;
 void er_pow(long double c, long double L, double* m, int* e);
 void fill_persist_tables(PersistParams& P, double c, int E);
 constexpr int TILE = 256;
@@ -454,6 +457,33 @@ static fs1_status plan_impl(const fs1_desc* desc, int device, int force, fs1_pla
     p->info.grid = d.batch;
     p->info.smem_bytes = p->smem;
     p->info.workspace_bytes = p->ws;
+  } else if (d.ndim == 2 && d.dtype == FS1_F64) {
+    // K5: Algorithm 2 in fp64 (scaling domain), one CTA per problem, a thread per line
+    if (d.domain != FS1_SCALING || d.n > 1024 || d.m > 1024) { delete p; return FS1_ERR_UNSUPPORTED; }
+    p->kind = KIND_SEP64;
+    Sep2d64Params& D = p->dbase;
+    memset(&D, 0, sizeof(D));
+    D.n = (int)d.n;
+    D.m = (int)d.m;
+    D.lam1 = exp(-d.h1 / d.eps);
+    D.lam2 = exp(-d.h2 / d.eps);
+    D.h1 = d.h1;
+    D.h2 = d.h2;
+    D.tol = d.tol;
+    D.itr_max = d.itr_max;
+    D.check_interval = d.check_interval;
+    D.warm = d.warm_start;
+    const long long lines = std::max(d.n, d.m);
+    p->threads = (int)std::min<long long>(1024, ((lines + 31) / 32) * 32);
+    p->ws = al256((size_t)d.batch * 2 * (size_t)d.n * (size_t)d.m * 8);
+    p->smem = 0;
+    snprintf(p->info.kernel, sizeof(p->info.kernel), "sep2d64_f64_scaling");
+    p->info.chunk = 1;
+    p->info.threads = p->threads;
+    p->info.ctas_per_problem = 1;
+    p->info.grid = d.batch;
+    p->info.smem_bytes = 0;
+    p->info.workspace_bytes = p->ws;
   } else if (d.ndim == 1 && (force == 2 || (force >= 10 && force < 20))) {
     std::lock_guard<std::mutex> lk(g_attr_mu);
     int cur = 0;
@@ -609,6 +639,15 @@ fs1_status fs1_solve(const fs1_plan_t* plan, const void* a, const void* b, void*
     cudaError_t e = plan->pe->launch_solve(P, plan->d.batch, plan->smem, (cudaStream_t)stream);
     return e == cudaSuccess ? FS1_OK : FS1_ERR_CUDA;
   }
+  if (plan->kind == KIND_SEP64) {
+    Sep2d64Params P = plan->dbase;
+    P.a = (const double*)a; P.b = (const double*)b; P.u = (double*)u; P.v = (double*)v;
+    P.iters = iters; P.err = err; P.flags = flags; P.cost = cost;
+    P.ws = (double*)workspace;
+    P.mode = 0;
+    return launch_sep2d64(P, plan->d.batch, plan->threads, (cudaStream_t)stream) == cudaSuccess ? FS1_OK
+                                                                                            : FS1_ERR_CUDA;
+  }
   if (plan->kind == KIND_STAB) {
     StabParams P = plan->kbase;
     P.a = a; P.b = b; P.u = u; P.v = v;
@@ -698,6 +737,15 @@ fs1_status fs1_cost(const fs1_plan_t* plan, const void* u, const void* v, double
     }
     return FS1_OK;
   }
+  if (plan->kind == KIND_SEP64) {
+    Sep2d64Params P = plan->dbase;
+    P.u = (double*)const_cast<void*>(u); P.v = (double*)const_cast<void*>(v);
+    P.cost = cost;
+    P.ws = (double*)workspace;
+    P.mode = 1;
+    return launch_sep2d64(P, plan->d.batch, plan->threads, (cudaStream_t)stream) == cudaSuccess ? FS1_OK
+                                                                                            : FS1_ERR_CUDA;
+  }
   if (plan->kind == KIND_STAB) {
     // the return line on (alpha/eps, beta/eps) = (F, G), phi = psi = 1 (an absorbed state)
     StabParams P = plan->kbase;
@@ -726,6 +774,14 @@ fs1_status fs1_apply(const fs1_plan_t* plan, const void* x, void* y, void* works
   if (plan->kind == KIND_PERSIST) {
     cudaError_t e = plan->pe->launch_apply(plan->base, x, y, plan->d.batch, (cudaStream_t)stream);
     return e == cudaSuccess ? FS1_OK : FS1_ERR_CUDA;
+  }
+  if (plan->kind == KIND_SEP64) {
+    Sep2d64Params P = plan->dbase;
+    P.x = (const double*)x; P.y = (double*)y;
+    P.ws = (double*)workspace;
+    P.mode = 2;
+    return launch_sep2d64(P, plan->d.batch, plan->threads, (cudaStream_t)stream) == cudaSuccess ? FS1_OK
+                                                                                            : FS1_ERR_CUDA;
   }
   if (plan->kind == KIND_SEP2D) {
     const long long nm = plan->d.n * plan->d.m;

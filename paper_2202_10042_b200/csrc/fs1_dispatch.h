@@ -58,6 +58,9 @@ struct StabEntry {
 };
 const StabEntry* stab_table(int* count);
 
+// K5 fp64 scaling-domain 2D solve, one CTA per problem (fs1_sep2d64.cu)
+cudaError_t launch_sep2d64(const Sep2d64Params& P, long long batch, int threads, cudaStream_t st);
+
 // transport-plan materialisation (fs1_tplan.cu)
 cudaError_t launch_tplan(int dtype, const void* u, const void* v, void* g, long long batch, long long n, long long m,
                          double c1, double c2, int logd, cudaStream_t st);

@@ -185,3 +185,26 @@ struct StabParams {
 };
 
 }  // namespace fs1
+
+namespace fs1 {
+
+// K5: Algorithm 2 in fp64, scaling domain, one CTA per 2D problem (fs1_sep2d64.cu).
+struct Sep2d64Params {
+  const double* a;   // [batch][n m] column-major histograms
+  const double* b;
+  double* u;         // [batch][n m] phi (in when warm)
+  double* v;         //              psi
+  int32_t* iters;
+  double* err;
+  int32_t* flags;
+  double* cost;
+  const double* x;   // apply: input / output
+  double* y;
+  double* ws;        // [batch][2][n m]
+  int n, m;
+  double lam1, lam2, h1, h2, tol;
+  int itr_max, check_interval, warm;
+  int mode;          // 0 solve, 1 cost, 2 apply
+};
+
+}  // namespace fs1

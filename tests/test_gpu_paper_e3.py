@@ -1,0 +1,94 @@
+"""The paper's 2D random-distribution workload (E3, Table 3) on the GPU:
+K5, Algorithm 2 in fp64 (scaling domain, the paper's unstabilised FS-1), against the
+oracle's dense Algorithm 2 (oracle/sinkhorn.py, K = T_M (x) T_N applied per axis).
+
+N x N for N = 10 ... 160, h1 = h2 = 1, eps = 0.01 (lambda = e^{-100}: fp32 cannot hold it),
+u, v iid U[0,1] normalised, the full 1000 iterations.  Column 5 of Table 3 (the Frobenius
+norm between the FS-1 and the dense Sinkhorn transport plans, 1e-17 .. 1e-18 there) is
+reproduced as the Frobenius norm between the GPU's plan (fs1_transport_plan) and the
+oracle's dense-Sinkhorn plan.
+"""
+import numpy as np
+import pytest
+
+import fs1_inputs as gi
+from oracle import dense, sinkhorn
+from tests.gpu_util import assert_solve_parity, rel
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_2202_10042_b200 import fs1  # noqa: E402
+
+
+def _solve(cfg, A, B, itr=None, **kw):
+    return fs1.solve(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), h=cfg.h1, h2=cfg.h2,
+                     shape=(cfg.n, cfg.m), eps=cfg.eps, itr_max=cfg.itr_max if itr is None else itr,
+                     domain="scaling", **kw)
+
+
+def _ref(cfg, A, B, itr=None, **kw):
+    return sinkhorn.solve(A, B, n=cfg.n, m=cfg.m, h1=cfg.h1, h2=cfg.h2, eps=cfg.eps,
+                          itr_max=cfg.itr_max if itr is None else itr, **kw)
+
+
+@pytest.mark.parametrize("name", ["e3_10", "e3_20", "e3_40", "e3_80", "e3_160"])
+def test_e3_full_protocol(name):
+    cfg = gi.CONFIGS[name]
+    A, B = gi.batch(cfg, range(2))
+    out = _solve(cfg, A, B)
+    ref = _ref(cfg, A, B)
+    assert fs1.plan(fs1.Spec(ndim=2, n=cfg.n, m=cfg.m, h1=cfg.h1, h2=cfg.h2, eps=cfg.eps, batch=2,
+                             dtype=torch.float64, itr_max=cfg.itr_max)).info()["kernel"].startswith("sep2d64")
+    assert_solve_parity(out, ref, "scaling", "f64")
+
+
+@pytest.mark.parametrize("name", ["e3_10", "e3_20", "e3_40", "e3_80"])
+def test_e3_plan_frobenius(name):
+    """Table 3 column 5: ||P_FS1 - P_Sinkhorn||_F at rounding level (the paper: 1.2e-17 at
+    10x10 down to 7.7e-19 at 160x160)."""
+    cfg = gi.CONFIGS[name]
+    A, B = gi.batch(cfg, range(1))
+    out = _solve(cfg, A, B)
+    ref = _ref(cfg, A, B)
+    g = fs1.transport_plan(out["u"], out["v"], h=cfg.h1, h2=cfg.h2, eps=cfg.eps, shape=(cfg.n, cfg.m))
+    Pg = g[0].cpu().numpy()
+    # the oracle's dense plan gamma = diag(phi) K diag(psi), K = T_M (x) T_N (column-major)
+    K = np.kron(dense.kernel(cfg.m, dense.lam(cfg.h2, cfg.eps)), dense.kernel(cfg.n, dense.lam(cfg.h1, cfg.eps)))
+    phi, psi = np.exp(ref["F"][0]), np.exp(ref["G"][0])
+    Po = phi[:, None] * K * psi[None, :]
+    d = np.linalg.norm(Pg - Po)
+    assert d <= 1e-14, d
+    # marginals of the plan: the u-marginal is exact after the phi update
+    np.testing.assert_allclose(Po.sum(1), A[0], rtol=1e-9, atol=1e-15)
+
+
+def test_tolerance_stop_and_apply():
+    """tol-stopped 2D fp64 run (R22) on a smaller-c case that converges, and the plain K x."""
+    cfg = gi.CONFIGS["e3_20"]
+    A, B = gi.batch(cfg, range(1))
+    kw = dict(h=0.05, h2=0.05, shape=(20, 20), eps=0.02, domain="scaling")
+    ref = sinkhorn.solve(A, B, n=20, m=20, h1=0.05, h2=0.05, eps=0.02, itr_max=20000, tol=1e-10)
+    assert ref["flags"][0] == 1
+    out = fs1.solve(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), itr_max=20000, tol=1e-10, **kw)
+    assert out["flags"].item() == 1 and abs(out["iters"].item() - ref["iters"][0]) <= 1
+    x = np.random.default_rng(3).uniform(0, 1, (3, 20 * 20))
+    y = fs1.apply(torch.from_numpy(x).cuda(), h=0.05, h2=0.05, shape=(20, 20), eps=0.02).cpu().numpy()
+    K = np.kron(dense.kernel(20, dense.lam(0.05, 0.02)), dense.kernel(20, dense.lam(0.05, 0.02)))
+    np.testing.assert_allclose(y, x @ K.T, rtol=1e-13)
+    c = fs1.cost(out["u"], out["v"], h=0.05, h2=0.05, shape=(20, 20), eps=0.02)
+    assert rel(c.item(), out["cost"].item()) <= 1e-13
+
+
+@pytest.mark.parametrize("shape", [(1, 1), (1, 7), (7, 1), (31, 33), (33, 64), (100, 3)])
+def test_ragged_shapes(shape):
+    n, m = shape
+    rng = np.random.default_rng(n * 100 + m)
+    A, B = gi.random_positive(rng, (3, n * m)), gi.random_positive(rng, (3, n * m))
+    kw = dict(h=1.0 / n, h2=1.0 / m, shape=(n, m), eps=0.03, itr_max=60, domain="scaling")
+    out = fs1.solve(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), **kw)
+    ref = sinkhorn.solve(A, B, n=n, m=m, h1=1.0 / n, h2=1.0 / m, eps=0.03, itr_max=60)
+    assert_solve_parity(out, ref, "scaling", "f64")
