@@ -247,3 +247,86 @@ def solve(a, b, *, n, m=1, h1, h2=0.0, eps, itr_max, tol=0.0, domain="scaling",
             Fo, Go = np.log(phi), np.log(psi)
     return {"F": Fo.T.copy(), "G": Go.T.copy(), "iters": iters, "err": err,
             "flags": flags, "cost": cost}
+
+
+# ---------------------------------------------------------------------------------------
+# Steps either side of the loop
+
+def log_gibbs(n, m, h1, h2, eps):
+    """-C_kl / eps for the flat (column-major, k = j n + i) grid points: the exponent of
+    the Gibbs kernel K_kl = lambda1^{|di|} lambda2^{|dj|}."""
+    i = np.tile(np.arange(n), m)
+    j = np.repeat(np.arange(m), n)
+    C = np.abs(i[:, None] - i[None, :]) * h1 + np.abs(j[:, None] - j[None, :]) * h2
+    return -C / eps
+
+
+def dual_objective(a, b, F, G, *, n, m=1, h1, h2=0.0, eps):
+    """The dual of the entropic problem Eq. (2.3) at log-scalings F, G,
+    written out densely (small problems):
+
+        D = eps (<F, a> + <G, b> - sum_kl gamma_kl) + eps (sum a + sum b) / 2,
+        gamma_kl = exp(F_k + G_l - C_kl / eps)
+
+    From the Lagrangian of PAPER.md:77-83 with gamma = exp((alpha_k + beta_l - C_kl)/eps - 1)
+    and F = alpha/eps - 1/2, G = beta/eps - 1/2 (the paper's phi = e^{-1/2 - alpha/eps}
+    with the multiplier sign flipped).  By weak duality D <= sum gamma C + eps sum gamma
+    ln gamma for every feasible gamma, with equality at the optimum; every Sinkhorn
+    half-step maximises D over one block.  Terms with a_k = 0 (F_k = -inf) count 0."""
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    F = np.asarray(F, np.float64)
+    G = np.asarray(G, np.float64)
+    L = log_gibbs(n, m, h1, h2, eps)
+    with np.errstate(invalid="ignore"):
+        fa = np.where(a > 0, F * a, 0.0).sum()
+        gb = np.where(b > 0, G * b, 0.0).sum()
+        gam = np.exp(F[:, None] + G[None, :] + L).sum()
+    return float(eps * (fa + gb - gam) + eps * (a.sum() + b.sum()) / 2)
+
+
+def primal_objective(F, G, *, n, m=1, h1, h2=0.0, eps):
+    """sum gamma C + eps sum gamma ln gamma at gamma = exp(F_k + G_l - C_kl/eps)
+    (Eq. 2.3's objective), dense."""
+    L = log_gibbs(n, m, h1, h2, eps)
+    lg = np.asarray(F, np.float64)[:, None] + np.asarray(G, np.float64)[None, :] + L
+    gam = np.exp(lg)
+    with np.errstate(invalid="ignore"):
+        ent = np.where(gam > 0, gam * lg, 0.0).sum()
+    return float((gam * (-L * eps)).sum() + eps * ent)
+
+
+def eps_schedule(eps, eps0, factor):
+    """eps_k = max(eps, eps0 factor^k), k = 0, 1, ... down to eps (factor in (0, 1),
+    eps0 >= eps): the stages of the eps-scaling continuation."""
+    assert 0.0 < factor < 1.0 and eps0 >= eps > 0.0
+    out = []
+    e = eps0
+    while e > eps * (1.0 + 1e-12):
+        out.append(e)
+        e *= factor
+    out.append(eps)
+    return out
+
+
+def solve_eps_scaling(a, b, *, n, m=1, h1, h2=0.0, eps, eps0, factor, stage_iters, itr_max,
+                      tol=0.0, check_interval=1, input_is_log=False, apply="dense"):
+    """eps-scaling continuation in the log domain: run Algorithm 1 / 2 at eps_0 > eps_1 >
+    ... > eps, each stage warm-started from the previous stage's dual potentials f = eps F,
+    g = eps G held fixed (F <- F eps_{k-1}/eps_k), the intermediate stages for
+    `stage_iters` fixed iterations, the last with itr_max / tol.  Returns the last stage's
+    result (plus 'stages')."""
+    sched = eps_schedule(eps, eps0, factor)
+    u0 = v0 = None
+    prev = None
+    for k, ek in enumerate(sched):
+        if prev is not None:
+            u0 = r["F"] * (prev / ek)
+            v0 = r["G"] * (prev / ek)
+        final = k == len(sched) - 1
+        r = solve(a, b, n=n, m=m, h1=h1, h2=h2, eps=ek, itr_max=itr_max if final else stage_iters,
+                  tol=tol if final else 0.0, check_interval=check_interval, domain="log",
+                  input_is_log=input_is_log, apply=apply, u0=u0, v0=v0)
+        prev = ek
+    r["stages"] = sched
+    return r

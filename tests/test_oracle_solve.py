@@ -303,3 +303,76 @@ def test_input_is_log_minus_inf_weights():
         m = np.isfinite(rs[k][0])
         np.testing.assert_allclose(rl[k][0][m], rs[k][0][m], rtol=1e-11, atol=1e-11)
     assert rl["cost"][0] == pytest.approx(rs["cost"][0], rel=1e-12)
+
+
+# ------------------------------------------------------------------ dual objective, eps-scaling
+def test_dual_objective_weak_and_strong_duality():
+    """D <= the primal objective of every feasible plan (weak duality, checked against the
+    exact LP-free N=2 entropic plan of oracle.w1) and D = primal at convergence."""
+    for (a1, b1, eps) in [(0.3, 0.6, 0.5), (0.8, 0.2, 0.2)]:
+        a, b = np.array([a1, 1 - a1]), np.array([b1, 1 - b1])
+        r = sinkhorn.solve(a, b, n=2, h1=1.0, eps=eps, itr_max=100000, tol=1e-15, domain="log")
+        D = sinkhorn.dual_objective(a, b, r["F"][0], r["G"][0], n=2, h1=1.0, eps=eps)
+        # the exact entropic plan: gamma_11 = x (w1.n2_plan), the rest by the marginals
+        x, _ = w1.n2_plan(a1, b1, math.exp(-1.0 / eps))
+        g = np.array([[x, a1 - x], [b1 - x, 1 - a1 - b1 + x]])
+        C = np.array([[0.0, 1.0], [1.0, 0.0]])
+        primal = float((g * C).sum() + eps * (g * np.log(g)).sum())
+        assert D == pytest.approx(primal, rel=1e-9, abs=1e-12)
+        # any other feasible plan has a larger primal value
+        for t in (0.5 * x, x + 0.5 * (min(a1, b1) - x)):
+            g2 = np.array([[t, a1 - t], [b1 - t, 1 - a1 - b1 + t]])
+            p2 = float((g2 * C).sum() + eps * (g2 * np.log(g2)).sum())
+            assert D <= p2 + 1e-12
+
+
+def test_dual_objective_monotone_and_converges_to_primal():
+    rng = np.random.default_rng(40)
+    n, eps = 30, 0.04
+    a, b = gi.random_positive(rng, n), gi.random_positive(rng, n)
+    trace = []
+    sinkhorn.solve(a, b, n=n, h1=1.0 / n, eps=eps, itr_max=40, domain="log", trace=trace)
+    vals = [sinkhorn.dual_objective(a, b, F[:, 0], G[:, 0], n=n, h1=1.0 / n, eps=eps) for (_, _, F, G) in trace]
+    assert all(vals[i + 1] >= vals[i] - 1e-14 for i in range(len(vals) - 1))
+    r = sinkhorn.solve(a, b, n=n, h1=1.0 / n, eps=eps, itr_max=100000, tol=1e-14, domain="log")
+    D = sinkhorn.dual_objective(a, b, r["F"][0], r["G"][0], n=n, h1=1.0 / n, eps=eps)
+    P = sinkhorn.primal_objective(r["F"][0], r["G"][0], n=n, h1=1.0 / n, eps=eps)
+    assert D == pytest.approx(P, rel=1e-10) and D >= vals[-1] - 1e-14
+    # 2D: the same identity on a 4 x 3 grid
+    n2, m2 = 4, 3
+    a2, b2 = gi.random_positive(rng, n2 * m2), gi.random_positive(rng, n2 * m2)
+    kw = dict(n=n2, m=m2, h1=0.3, h2=0.2, eps=0.1)
+    r2 = sinkhorn.solve(a2, b2, itr_max=100000, tol=1e-14, domain="log", **kw)
+    assert sinkhorn.dual_objective(a2, b2, r2["F"][0], r2["G"][0], **kw) == pytest.approx(
+        sinkhorn.primal_objective(r2["F"][0], r2["G"][0], **kw), rel=1e-10)
+
+
+def test_eps_scaling_single_stage_is_plain_solve():
+    rng = np.random.default_rng(41)
+    n = 40
+    a, b = gi.random_positive(rng, n), gi.random_positive(rng, n)
+    kw = dict(n=n, h1=1.0 / n, eps=0.02, itr_max=50)
+    r1 = sinkhorn.solve_eps_scaling(a, b, eps0=0.02, factor=0.5, stage_iters=7, **kw)
+    r2 = sinkhorn.solve(a, b, domain="log", **kw)
+    np.testing.assert_array_equal(r1["F"], r2["F"])
+    assert r1["stages"] == [0.02]
+
+
+def test_eps_scaling_reaches_the_same_fixed_point():
+    """Continuation changes the path, not the limit: converged to tol, the plan equals the
+    direct solve's (the entropic optimum is unique) and the dual objectives agree."""
+    rng = np.random.default_rng(42)
+    n = 60
+    a, b = gi.random_positive(rng, n), gi.random_positive(rng, n)
+    kw = dict(n=n, h1=1.0 / n, eps=0.005, itr_max=200000, tol=1e-12)
+    rs = sinkhorn.solve_eps_scaling(a, b, eps0=0.16, factor=0.5, stage_iters=30, **kw)
+    rd = sinkhorn.solve(a, b, domain="log", **kw)
+    assert rs["stages"] == [0.16, 0.08, 0.04, 0.02, 0.01, 0.005]
+    assert rs["flags"][0] == sinkhorn.CONVERGED and rd["flags"][0] == sinkhorn.CONVERGED
+    D = dense.dist(n)
+    gs = np.exp(rs["F"][0][:, None] + rs["G"][0][None, :] - D * (1.0 / n) / 0.005)
+    gd = np.exp(rd["F"][0][:, None] + rd["G"][0][None, :] - D * (1.0 / n) / 0.005)
+    np.testing.assert_allclose(gs, gd, atol=1e-10)
+    assert rs["cost"][0] == pytest.approx(rd["cost"][0], rel=1e-8)
+    # ... and needs fewer iterations at the target eps than the cold start
+    assert rs["iters"][0] < rd["iters"][0]
