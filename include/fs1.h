@@ -176,6 +176,35 @@ fs1_status fs1_apply(const fs1_plan_t* plan, const void* x, void* y, void* works
 #define FS1_MAX_TPLAN 8192
 fs1_status fs1_transport_plan(const fs1_plan_t* plan, const void* u, const void* v, void* gamma, void* stream);
 
+/* fs1_dual — the dual objective of the entropic problem Eq. (2.3) at the
+ * state (u, v) as fs1_solve returns it:
+ *   D = eps (sum_k a_k F_k + sum_l b_l G_l - sum_kl gamma_kl) + eps (sum a + sum b) / 2,
+ *   gamma_kl = e^{F_k + G_l} K_kl,  F = log phi, G = log psi  (terms with zero weight count 0).
+ * max D = W_eps (strong duality) and D <= the objective of every feasible plan; every
+ * Sinkhorn half-step maximises D over one block.  One kernel apply (as fs1_apply) into
+ * `scratch` ([batch][n*m] of the plan dtype, caller-owned) and one reduction.
+ *   a, b : as for fs1_solve;  dual : [batch] fp64.
+ * Errors: FS1_ERR_ARG, FS1_ERR_UNSUPPORTED (FS1_STABILIZED, or no apply for the plan).     */
+fs1_status fs1_dual(const fs1_plan_t* plan, const void* a, const void* b, const void* u, const void* v,
+                    void* scratch, double* dual, void* workspace, void* stream);
+
+/* eps-scaling continuation (the slow convergence at small eps that
+ * PAPER.md:529 names): Algorithm 1 / 2 at eps_k = max(eps, eps0 factor^k), k = 0, 1, ...,
+ * each stage warm-started from the previous one with the dual potentials f = eps F,
+ * g = eps G held fixed (F <- F eps_{k-1} / eps_k); intermediate stages run `stage_iters`
+ * fixed iterations, the last (eps_k = desc->eps) desc->itr_max / tol / check_interval.
+ * FS1_LOG only.  Outputs are the last stage's (iters counts its iterations only).
+ * fs1_eps_scaling_plan returns the number of stages and the workspace the calls need;
+ * the library creates and destroys one plan per stage on the host (no device allocation).
+ * Errors: FS1_ERR_ARG (factor not in (0,1), eps0 < eps, ...), FS1_ERR_UNSUPPORTED,
+ * FS1_ERR_WORKSPACE (workspace_bytes too small).                                            */
+fs1_status fs1_eps_scaling_plan(const fs1_desc* desc, int device, double eps0, double factor, int32_t* stages,
+                                size_t* workspace_bytes);
+fs1_status fs1_solve_eps_scaling(const fs1_desc* desc, int device, double eps0, double factor, int32_t stage_iters,
+                                 const void* a, const void* b, void* u, void* v, int32_t* iters, double* err,
+                                 int32_t* flags, double* cost, void* workspace, size_t workspace_bytes,
+                                 void* stream);
+
 fs1_status fs1_plan_info(const fs1_plan_t* plan, fs1_plan_info_t* info);
 void fs1_plan_destroy(fs1_plan_t* plan);
 const char* fs1_status_string(fs1_status s);

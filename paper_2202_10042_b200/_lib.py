@@ -16,7 +16,8 @@ FS1_F32, FS1_F64 = 0, 1
 FS1_SCALING, FS1_LOG, FS1_STABILIZED = 0, 1, 2
 FLAG_CONVERGED, FLAG_NONFINITE, FLAG_ITR_MAX = 1, 2, 4
 
-EXPORTS = ["fs1_plan", "fs1_solve", "fs1_cost", "fs1_apply", "fs1_transport_plan", "fs1_plan_info",
+EXPORTS = ["fs1_plan", "fs1_solve", "fs1_cost", "fs1_apply", "fs1_transport_plan", "fs1_dual",
+           "fs1_eps_scaling_plan", "fs1_solve_eps_scaling", "fs1_plan_info",
            "fs1_plan_destroy", "fs1_status_string", "fs1_abi_version",
            # include/fs1_shard.h
            "fs1_shard_plan", "fs1_shard_init", "fs1_shard_half", "fs1_shard_cost_totals",
@@ -85,6 +86,15 @@ def lib():
         L.fs1_apply.restype = st
         L.fs1_transport_plan.argtypes = [vp] * 5
         L.fs1_transport_plan.restype = st
+        L.fs1_dual.argtypes = [vp] * 9
+        L.fs1_dual.restype = st
+        dd = ctypes.c_double
+        L.fs1_eps_scaling_plan.argtypes = [ctypes.POINTER(Desc), st, dd, dd, ctypes.POINTER(ctypes.c_int32),
+                                           ctypes.POINTER(ctypes.c_size_t)]
+        L.fs1_eps_scaling_plan.restype = st
+        L.fs1_solve_eps_scaling.argtypes = [ctypes.POINTER(Desc), st, dd, dd, ctypes.c_int32] + [vp] * 9 + \
+            [ctypes.c_size_t, vp]
+        L.fs1_solve_eps_scaling.restype = st
         L.fs1_plan_info.argtypes = [vp, ctypes.POINTER(PlanInfo)]
         L.fs1_plan_info.restype = st
         L.fs1_plan_destroy.argtypes = [vp]

@@ -808,4 +808,101 @@ fs1_status fs1_apply(const fs1_plan_t* plan, const void* x, void* y, void* works
   return FS1_ERR_UNSUPPORTED;
 }
 
+fs1_status fs1_dual(const fs1_plan_t* plan, const void* a, const void* b, const void* u, const void* v,
+                    void* scratch, double* dual, void* workspace, void* stream) {
+  if (!plan || !a || !b || !u || !v || !scratch || !dual) return FS1_ERR_ARG;
+  if (plan->d.domain == FS1_STABILIZED) return FS1_ERR_UNSUPPORTED;
+  // S = K psi (scaling) / log K e^G (log): the kernel apply of the plan
+  const fs1_status st = fs1_apply(plan, v, scratch, workspace, stream);
+  if (st != FS1_OK) return st;
+  const fs1_desc& d = plan->d;
+  const cudaError_t e = launch_dual(d.dtype == FS1_F64 ? 1 : 0, a, b, u, v, scratch, d.batch, d.n * d.m, d.eps,
+                                    d.domain == FS1_LOG ? 1 : 0, d.domain == FS1_LOG ? d.input_is_log : 0, dual,
+                                    (cudaStream_t)stream);
+  return e == cudaSuccess ? FS1_OK : FS1_ERR_CUDA;
+}
+
+// the eps-scaling schedule: eps_k = max(eps, eps0 factor^k) (oracle/sinkhorn.py eps_schedule)
+static int eps_schedule(double eps, double eps0, double factor, double* out, int cap) {
+  int k = 0;
+  double e = eps0;
+  while (e > eps * (1.0 + 1e-12) && k < cap - 1) {
+    if (out) out[k] = e;
+    ++k;
+    e *= factor;
+  }
+  if (out) out[k] = eps;
+  return k + 1;
+}
+
+static fs1_status eps_scaling_check(const fs1_desc* desc, double eps0, double factor) {
+  if (!desc) return FS1_ERR_ARG;
+  if (desc->domain != FS1_LOG) return FS1_ERR_UNSUPPORTED;
+  if (!(factor > 0.0 && factor < 1.0) || !(eps0 >= desc->eps) || !isfinite(eps0)) return FS1_ERR_ARG;
+  if (eps_schedule(desc->eps, eps0, factor, nullptr, 4096) >= 4096) return FS1_ERR_ARG;
+  return FS1_OK;
+}
+
+fs1_status fs1_eps_scaling_plan(const fs1_desc* desc, int device, double eps0, double factor, int32_t* stages,
+                                size_t* workspace_bytes) {
+  fs1_status st = eps_scaling_check(desc, eps0, factor);
+  if (st != FS1_OK) return st;
+  static thread_local double sched[4096];
+  const int ns = eps_schedule(desc->eps, eps0, factor, sched, 4096);
+  size_t mx = 0;
+  for (int k = 0; k < ns; ++k) {
+    fs1_desc dk = *desc;
+    dk.eps = sched[k];
+    fs1_plan_t* p = nullptr;
+    size_t ws = 0;
+    st = fs1_plan(&dk, device, &p, &ws);
+    if (st != FS1_OK) return st;
+    fs1_plan_destroy(p);
+    mx = std::max(mx, ws);
+  }
+  if (stages) *stages = ns;
+  if (workspace_bytes) *workspace_bytes = mx;
+  return FS1_OK;
+}
+
+fs1_status fs1_solve_eps_scaling(const fs1_desc* desc, int device, double eps0, double factor, int32_t stage_iters,
+                                 const void* a, const void* b, void* u, void* v, int32_t* iters, double* err,
+                                 int32_t* flags, double* cost, void* workspace, size_t workspace_bytes,
+                                 void* stream) {
+  fs1_status st = eps_scaling_check(desc, eps0, factor);
+  if (st != FS1_OK) return st;
+  if (stage_iters < 0 || !a || !b || !u || !v) return FS1_ERR_ARG;
+  static thread_local double sched[4096];
+  const int ns = eps_schedule(desc->eps, eps0, factor, sched, 4096);
+  for (int k = 0; k < ns; ++k) {
+    const bool final = k == ns - 1;
+    fs1_desc dk = *desc;
+    dk.eps = sched[k];
+    dk.itr_max = final ? desc->itr_max : stage_iters;
+    dk.tol = final ? desc->tol : 0.0;
+    dk.warm_start = (k > 0 || desc->warm_start) ? 1 : 0;
+    fs1_plan_t* p = nullptr;
+    size_t ws = 0;
+    st = fs1_plan(&dk, device, &p, &ws);
+    if (st != FS1_OK) return st;
+    if (ws > workspace_bytes || (ws && !workspace)) {
+      fs1_plan_destroy(p);
+      return FS1_ERR_WORKSPACE;
+    }
+    if (k > 0) {
+      // the previous stage's dual potentials f = eps F, g = eps G carried to this eps
+      const cudaError_t e = launch_rescale(desc->dtype == FS1_F64 ? 1 : 0, u, v, desc->batch * desc->n * desc->m,
+                                           sched[k - 1] / sched[k], (cudaStream_t)stream);
+      if (e != cudaSuccess) {
+        fs1_plan_destroy(p);
+        return FS1_ERR_CUDA;
+      }
+    }
+    st = fs1_solve(p, a, b, u, v, iters, err, flags, final ? cost : nullptr, workspace, stream);
+    fs1_plan_destroy(p);  // launches captured their parameters by value
+    if (st != FS1_OK) return st;
+  }
+  return FS1_OK;
+}
+
 }  // extern "C"

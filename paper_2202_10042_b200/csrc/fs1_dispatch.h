@@ -61,6 +61,12 @@ const StabEntry* stab_table(int* count);
 // K5 fp64 scaling-domain 2D solve, one CTA per problem (fs1_sep2d64.cu)
 cudaError_t launch_sep2d64(const Sep2d64Params& P, long long batch, int threads, cudaStream_t st);
 
+// dual objective and eps-scaling warm start (fs1_extra.cu)
+cudaError_t launch_dual(int dtype, const void* a, const void* b, const void* u, const void* v, const void* s,
+                        long long batch, long long size, double eps, int logd, int input_is_log, double* out,
+                        cudaStream_t st);
+cudaError_t launch_rescale(int dtype, void* u, void* v, long long count, double ratio, cudaStream_t st);
+
 // transport-plan materialisation (fs1_tplan.cu)
 cudaError_t launch_tplan(int dtype, const void* u, const void* v, void* g, long long batch, long long n, long long m,
                          double c1, double c2, int logd, cudaStream_t st);

@@ -234,3 +234,73 @@ def transport_plan(u, v, *, h, eps, domain="scaling", shape=None, h2=None):
     if s != L.FS1_OK:
         raise L.FS1Error(s, "fs1_transport_plan")
     return g
+
+
+def dual(a, b, u, v, *, h, eps, domain="scaling", input_is_log=False, shape=None, h2=None, kernel=0):
+    """fs1_dual: the dual objective of Eq. (2.3) at the state (u, v) for every pair ([batch] fp64)."""
+    dev = u.device.index
+    ndim, n, m = (1, u.shape[-1], 1) if shape is None else (2, *shape)
+    size = n * m
+    _check(u, "u", u.dtype, dev, size)
+    for t, nm in ((a, "a"), (b, "b"), (v, "v")):
+        _check(t, nm, u.dtype, dev, size, u.numel())
+    batch = u.numel() // size
+    spec = Spec(ndim=ndim, n=n, m=m, h1=float(h), h2=float(h2 if h2 is not None else (h if ndim == 2 else 0.0)),
+                eps=float(eps), batch=batch, dtype=u.dtype, domain=domain, input_is_log=bool(input_is_log),
+                itr_max=0, kernel=int(kernel))
+    p = plan(spec, dev)
+    scratch = torch.empty_like(u)
+    out = torch.empty(batch, dtype=torch.float64, device=u.device)
+    s = L.lib().fs1_dual(p._h, _ptr(a), _ptr(b), _ptr(u), _ptr(v), _ptr(scratch), _ptr(out),
+                         _ptr(p.workspace()), _stream(dev))
+    if s != L.FS1_OK:
+        raise L.FS1Error(s, "fs1_dual")
+    return out
+
+
+def solve_eps_scaling(a, b, *, h, eps, eps0, factor, stage_iters, itr_max, tol=0.0, input_is_log=False,
+                      check_interval=1, shape=None, h2=None, u0=None, v0=None):
+    """fs1_solve_eps_scaling (log domain): the eps-scaling continuation eps0 -> eps; outputs as
+    solve() for the last stage, plus 'stages'."""
+    dev = a.device.index
+    if shape is None:
+        ndim, n, m = 1, a.shape[-1], 1
+    else:
+        ndim, (n, m) = 2, shape
+    size = n * m
+    _check(a, "a", a.dtype, dev, size)
+    _check(b, "b", a.dtype, dev, size, a.numel())
+    if (u0 is None) != (v0 is None):
+        raise ValueError("warm start needs both u0 and v0 (or neither)")
+    batch = a.numel() // size
+    spec = Spec(ndim=ndim, n=n, m=m, h1=float(h), h2=float(h2 if h2 is not None else (h if ndim == 2 else 0.0)),
+                eps=float(eps), batch=batch, dtype=a.dtype, domain="log", input_is_log=bool(input_is_log),
+                itr_max=int(itr_max), tol=float(tol), check_interval=int(check_interval),
+                warm_start=u0 is not None)
+    d = spec.desc()
+    ns = ctypes.c_int32()
+    wsb = ctypes.c_size_t()
+    s = L.lib().fs1_eps_scaling_plan(ctypes.byref(d), dev, float(eps0), float(factor), ctypes.byref(ns),
+                                     ctypes.byref(wsb))
+    if s != L.FS1_OK:
+        raise L.FS1Error(s, "fs1_eps_scaling_plan")
+    ws = torch.empty(wsb.value + 256, dtype=torch.uint8, device=a.device) if wsb.value else None
+    wsp = None if ws is None else ctypes.c_void_p(ws.data_ptr() + (-ws.data_ptr()) % 256)
+    if u0 is not None:
+        _check(u0, "u0", a.dtype, dev, size, a.numel())
+        _check(v0, "v0", a.dtype, dev, size, a.numel())
+        u = u0.clone(memory_format=torch.contiguous_format)
+        v = v0.clone(memory_format=torch.contiguous_format)
+    else:
+        u, v = torch.empty_like(a), torch.empty_like(b)
+    iters = torch.empty(batch, dtype=torch.int32, device=a.device)
+    err = torch.empty(batch, dtype=torch.float64, device=a.device)
+    flags = torch.empty(batch, dtype=torch.int32, device=a.device)
+    cost = torch.empty(batch, dtype=torch.float64, device=a.device)
+    s = L.lib().fs1_solve_eps_scaling(ctypes.byref(d), dev, float(eps0), float(factor), int(stage_iters),
+                                      _ptr(a), _ptr(b), _ptr(u), _ptr(v), _ptr(iters), _ptr(err), _ptr(flags),
+                                      _ptr(cost), wsp, wsb.value, _stream(dev))
+    if s != L.FS1_OK:
+        raise L.FS1Error(s, "fs1_solve_eps_scaling")
+    # (ws is returned to torch's caching allocator stream-ordered: safe while the launches run)
+    return {"u": u, "v": v, "iters": iters, "err": err, "flags": flags, "cost": cost, "stages": int(ns.value)}
