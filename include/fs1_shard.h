@@ -69,6 +69,20 @@ fs1_status fs1_shard_half(const fs1_shard_t* s, int which, int hs, int check, in
                           int psi_out, const double* all_tot, double* tot4, double* errflag, void* workspace,
                           void* stream);
 
+/* fs1_shard_decide — the loop-top decision of Algorithm 1 line 2 on the
+ * device, from every rank's errflag (all_errflag: device [world][2], the all-gather of the
+ * fs1_shard_half errflag rows in rank order; the same on every rank):
+ *   out4[0] = err = sum of the error partials in rank order,
+ *   out4[1] = 0 continue | 1 CONVERGED (tol > 0, err <= tol) | 2 NONFINITE | 4 ITR_MAX (l >= itr_max),
+ *   out4[2] = the iteration at the stop (NONFINITE: the smallest non-finite record), out4[3] = 0.
+ *   l : the loop-top iteration.  The caller only reads the flag.                     */
+fs1_status fs1_shard_decide(const fs1_shard_t* s, const double* all_errflag, int l, double* out4, void* stream);
+
+/* fs1_shard_sum — out[0] = sum over ranks (rank order) of rows[k * stride + col]
+ * (device [world][stride]; the cost partials of fs1_shard_finish).                    */
+fs1_status fs1_shard_sum(const fs1_shard_t* s, const double* rows, int stride, int col, double* out,
+                         void* stream);
+
 /* fs1_shard_cost_totals — Jordan-block pair totals of psi (buffer `psi`) for the
  * return line (R7): device out tot8 = 8 doubles.          */
 fs1_status fs1_shard_cost_totals(const fs1_shard_t* s, int psi, double* tot8, void* workspace, void* stream);

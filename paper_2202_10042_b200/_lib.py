@@ -23,7 +23,7 @@ EXPORTS = ["fs1_plan", "fs1_solve", "fs1_cost", "fs1_apply", "fs1_transport_plan
            "fs1_shard_plan", "fs1_shard_init", "fs1_shard_half", "fs1_shard_cost_totals",
            "fs1_shard_finish", "fs1_shard_destroy", "fs1_shard_mailbox_bytes", "fs1_shard_mailbox_alloc",
            "fs1_shard_mailbox_open", "fs1_shard_mailbox_close", "fs1_shard_mailbox_free",
-           "fs1_shard_set_mailboxes"]
+           "fs1_shard_set_mailboxes", "fs1_shard_decide", "fs1_shard_sum"]
 
 
 class Desc(ctypes.Structure):
@@ -133,5 +133,9 @@ def lib():
         L.fs1_shard_mailbox_free.restype = st
         L.fs1_shard_set_mailboxes.argtypes = [vp, vp]
         L.fs1_shard_set_mailboxes.restype = st
+        L.fs1_shard_decide.argtypes = [vp, vp, st, vp, vp]
+        L.fs1_shard_decide.restype = st
+        L.fs1_shard_sum.argtypes = [vp, vp, st, st, vp, vp]
+        L.fs1_shard_sum.restype = st
         _lib = L
     return _lib

@@ -322,6 +322,52 @@ fs1_status fs1_shard_set_mailboxes(fs1_shard_t* s, void* const* boxes) {
   return FS1_OK;
 }
 
+// Loop-top decision of Algorithm 1 line 2 over every rank's errflag row
+// ([world][2] in rank order): err = the rank-ordered sum of the error partials (a fixed
+// order, the same on every rank), the first non-finite iteration = the smallest positive
+// record; out = {err, flag (0 continue, 1 CONVERGED, 2 NONFINITE, 4 ITR_MAX), l at stop}.
+__global__ void k_shard_decide(const double* all, int world, int l, int itr_max, double tol, double* out) {
+  double err = 0.0;
+  double bad = 0.0;
+  for (int k = 0; k < world; ++k) {
+    err += all[2 * k];
+    const double f = all[2 * k + 1];
+    if (f > 0.0 && (bad == 0.0 || f < bad)) bad = f;
+  }
+  const bool use_tol = tol > 0.0;
+  double flag = 0.0, lstop = (double)l;
+  if (bad > 0.0) {
+    flag = 2.0;  // "terminates abnormally"
+    lstop = bad;
+  } else if (l >= itr_max || err <= tol) {
+    flag = (use_tol && err <= tol) ? 1.0 : 4.0;
+  }
+  out[0] = err;
+  out[1] = flag;
+  out[2] = lstop;
+  out[3] = 0.0;
+}
+
+// rank-ordered sum of column `col` of a [world][stride] row set (the cost partials)
+__global__ void k_shard_sum(const double* all, int world, int stride, int col, double* out) {
+  double sacc = 0.0;
+  for (int k = 0; k < world; ++k) sacc += all[(size_t)k * stride + col];
+  out[0] = sacc;
+}
+
+fs1_status fs1_shard_decide(const fs1_shard_t* s, const double* all_errflag, int l, double* out4, void* stream) {
+  if (!s || !all_errflag || !out4 || l < 0) return FS1_ERR_ARG;
+  k_shard_decide<<<1, 1, 0, (cudaStream_t)stream>>>(all_errflag, s->P.world, l, s->d.itr_max, s->d.tol, out4);
+  return cudaGetLastError() == cudaSuccess ? FS1_OK : FS1_ERR_CUDA;
+}
+
+fs1_status fs1_shard_sum(const fs1_shard_t* s, const double* rows, int stride, int col, double* out,
+                         void* stream) {
+  if (!s || !rows || !out || stride < 1 || col < 0 || col >= stride) return FS1_ERR_ARG;
+  k_shard_sum<<<1, 1, 0, (cudaStream_t)stream>>>(rows, s->P.world, stride, col, out);
+  return cudaGetLastError() == cudaSuccess ? FS1_OK : FS1_ERR_CUDA;
+}
+
 void fs1_shard_destroy(fs1_shard_t* s) { delete s; }
 
 }  // extern "C"

@@ -61,6 +61,8 @@ class ShardRank:
         self.errflag = torch.zeros(2, dtype=torch.float64, device=dev)
         self.tot8 = torch.zeros(8, dtype=torch.float64, device=dev)
         self.cost = torch.zeros(1, dtype=torch.float64, device=dev)
+        self.decision = torch.zeros(4, dtype=torch.float64, device=dev)
+        self.total = torch.zeros(1, dtype=torch.float64, device=dev)
 
     def set_mailboxes(self, boxes):
         """boxes: every rank's mailbox pointer (int) as seen from this device; None = off."""
@@ -91,6 +93,21 @@ class ShardRank:
                                         _stream(self.device)), "fs1_shard_half")
         return self.tot, self.errflag
 
+    def decide(self, all_errflag, l):
+        """fs1_shard_decide: (err, flag, l at stop) of the loop top, computed on the device
+        from every rank's errflag row; the host reads the result only."""
+        self._ok(L.lib().fs1_shard_decide(self._h, _ptr(all_errflag.contiguous()), l, _ptr(self.decision),
+                                          _stream(self.device)), "fs1_shard_decide")
+        d = self.decision.cpu()  # one host read per check
+        return float(d[0]), int(d[1]), int(d[2])
+
+    def rank_sum(self, rows, col=0):
+        """fs1_shard_sum: the rank-ordered sum of column `col` of [world][k] rows (device)."""
+        rows = rows.contiguous()
+        self._ok(L.lib().fs1_shard_sum(self._h, _ptr(rows), rows.shape[1], col, _ptr(self.total),
+                                       _stream(self.device)), "fs1_shard_sum")
+        return self.total
+
     def cost_totals(self, psi):
         self._ok(L.lib().fs1_shard_cost_totals(self._h, psi, _ptr(self.tot8), _ptr(self.ws),
                                                _stream(self.device)), "fs1_shard_cost_totals")
@@ -118,14 +135,11 @@ def _run(ranks, segs_a, segs_b, gather, itr_max, tol, check_interval, want_cost,
         allT = tgather(tots)
         outs = [r.half(0, hs, check, not last, l + 1, qi, qo, allT) for r in ranks]
         if check:
-            ef = gather([o[1] for o in outs]).cpu()  # one host sync per check
-            err = float(sum(ef[k, 0].item() for k in range(ef.shape[0])))  # fixed rank order
-            bad = [int(ef[k, 1].item()) for k in range(ef.shape[0]) if ef[k, 1].item() > 0]
-            if bad:  # "terminates abnormally": the first non-finite iteration
-                l, flag = min(bad), 2
-                break
-            if last or err <= tol:
-                flag = 1 if (use_tol and err <= tol) else 4
+            # the stop rule of line 2 on the device (rank-ordered error sum, first non-finite
+            # iteration); one host read of the decision per check
+            err, f, lstop = ranks[0].decide(gather([o[1] for o in outs]), l)
+            if f:
+                l, flag = (lstop if f == 2 else l), f
                 break
             qi = qo
         hs += 1
@@ -164,11 +178,9 @@ def _run_graph(ranks, segs_a, segs_b, gather, itr_max, tgather=None):
     # loop top at l = itr_max: the exit check, psi^(l) kept in buffer 0
     allT = tgather([r.tot for r in ranks])
     outs = [r.half(0, 0, True, False, itr_max + 1, 0, 1, allT) for r in ranks]
-    ef = gather([o[1] for o in outs]).cpu()
-    err = float(sum(ef[k, 0].item() for k in range(ef.shape[0])))
-    bad = [int(ef[k, 1].item()) for k in range(ef.shape[0]) if ef[k, 1].item() > 0]
-    if bad:
-        return min(bad), 0, 2, err
+    err, f, lstop = ranks[0].decide(gather([o[1] for o in outs]), itr_max)
+    if f == 2:
+        return lstop, 0, 2, err
     return itr_max, 0, 4, err
 
 
@@ -250,7 +262,7 @@ def solve_segments(a, b, world, *, h, eps, itr_max, tol=0.0, check_interval=1, i
                 r.set_mailboxes(None)
     ok = flag != 2
     us, vs, parts = _finish(ranks, qi, gather, flag, want_cost and ok, lambda r: a.device)
-    cost = float(sum(p.item() for p in parts)) if (want_cost and ok) else float("nan")
+    cost = ranks[0].rank_sum(gather(parts)).item() if (want_cost and ok) else float("nan")
     return {"u": torch.cat(us), "v": torch.cat(vs), "iters": l, "err": err if ok else float("nan"),
             "flags": flag, "cost": cost, "segments": [(r.lo, r.len) for r in ranks]}
 
@@ -297,8 +309,7 @@ def solve_sharded(a_seg, b_seg, n, *, h, eps, itr_max, tol=0.0, check_interval=1
     us, vs, parts = _finish([r], qi, gather, flag, want_cost and ok, lambda _: a_seg.device)
     cost = float("nan")
     if want_cost and ok:
-        allc = gather([parts[0]]).cpu()
-        cost = float(sum(allc[k, 0].item() for k in range(world)))
+        cost = r.rank_sum(gather([parts[0]])).item()
     return {"u": us[0], "v": vs[0], "iters": l, "err": err if ok else float("nan"), "flags": flag,
             "cost": cost, "segment": (r.lo, r.len)}
 

@@ -226,3 +226,26 @@ def test_fused_exchange_oracle_parity_and_repeat():
     r = shard.ShardRank(n, 2, 0, h=1 / n, eps=2e-3, itr_max=1, input_is_log=True)
     with pytest.raises(L.FS1Error):
         r.set_mailboxes([0, 0])  # NULL mailbox
+
+
+def test_shard_decide_and_sum_on_device():
+    """fs1_shard_decide / fs1_shard_sum: the loop-top rule and the rank-ordered sums run on
+    the device; they equal the host-side rank-ordered fp64 sums bitwise."""
+    n = 5000
+    r = shard.ShardRank(n, 3, 0, h=1.0 / n, eps=1e-2, itr_max=10, tol=1e-9, device=0)
+    dev = torch.device("cuda:0")
+    rows = torch.tensor([[0.1, 0.0], [1e-17, 0.0], [0.3, 0.0]], dtype=torch.float64, device=dev)
+    err, f, ls = r.decide(rows, 4)
+    host = 0.0
+    for k in range(3):
+        host += rows[k, 0].item()
+    assert err == host and f == 0 and ls == 4
+    small = torch.tensor([[4e-10, 0.0], [5e-10, 0.0], [0.0, 0.0]], dtype=torch.float64, device=dev)
+    assert r.decide(small, 6)[1] == 1                      # err <= tol: CONVERGED
+    assert r.decide(rows, 10)[1] == 4                      # l >= itr_max: ITR_MAX
+    bad = torch.tensor([[0.1, 0.0], [0.2, 7.0], [0.3, 5.0]], dtype=torch.float64, device=dev)
+    e2, f2, l2 = r.decide(bad, 8)
+    assert f2 == 2 and l2 == 5                             # the first non-finite iteration
+    parts = torch.tensor([[1.0 / 3.0], [1e-20], [2.0 / 7.0]], dtype=torch.float64, device=dev)
+    s = r.rank_sum(parts).item()
+    assert s == (0.0 + 1.0 / 3.0) + 1e-20 + 2.0 / 7.0

@@ -66,10 +66,13 @@ def test_gather_totals_gloo_world2():
 
 
 class FakeRank:
-    """Stands in for ShardRank: records calls; errors follow `errs` (per check)."""
+    """Stands in for ShardRank: records calls; errors follow `errs` (per check).  `decide`
+    stands in for fs1_shard_decide (the device rule, tested on the GPU in
+    tests/test_gpu_shard.py) with the same rule written out here."""
 
-    def __init__(self, rank, errs, bad_at=None, fused=False):
+    def __init__(self, rank, errs, bad_at=None, fused=False, itr_max=None, tol=None):
         self.rank, self.errs, self.bad_at, self.fused = rank, list(errs), bad_at, fused
+        self.itr_max, self.tol = itr_max, tol
         self.calls = []
         self.tot = torch.zeros(4, dtype=torch.float64)
         self.ef = torch.zeros(2, dtype=torch.float64)
@@ -87,13 +90,25 @@ class FakeRank:
             self.ef = torch.tensor([e, float(bad)], dtype=torch.float64)
         return self.tot, self.ef
 
+    def decide(self, all_ef, l):
+        self.calls.append(("decide", l))
+        err = 0.0
+        for k in range(all_ef.shape[0]):       # rank order
+            err += float(all_ef[k, 0])
+        bad = [int(all_ef[k, 1]) for k in range(all_ef.shape[0]) if all_ef[k, 1] > 0]
+        if bad:
+            return err, 2, min(bad)
+        if l >= self.itr_max or err <= self.tol:
+            return err, (1 if (self.tol > 0 and err <= self.tol) else 4), l
+        return err, 0, l
+
 
 def _gather(ts):
     return torch.stack([t.clone() for t in ts])
 
 
 def test_loop_fixed_iterations():
-    ranks = [FakeRank(0, []), FakeRank(1, [])]
+    ranks = [FakeRank(0, [], itr_max=3, tol=0.0), FakeRank(1, [], itr_max=3, tol=0.0)]
     l, qi, flag, err = shard._run(ranks, [None] * 2, [None] * 2, _gather, 3, 0.0, 1, True)
     assert (l, qi, flag) == (3, 0, 4)
     expect = [("init",)]
@@ -102,15 +117,15 @@ def test_loop_fixed_iterations():
         expect += [("half", 0, hs, False, True, it + 1, 0, 0), ("half", 1, hs + 1, False, True, it + 1, 0, 0)]
         hs += 2
     expect += [("half", 0, hs, True, False, 4, 0, 1)]  # exit check at l = itr_max, no write
-    for r in ranks:
-        assert r.calls == expect
+    assert ranks[0].calls == expect + [("decide", 3)]  # the decision is taken once, by rank 0's plan
+    assert ranks[1].calls == expect
     assert err == 2.0  # 1.0 + 1.0 in rank order
 
 
 def test_loop_tolerance_keeps_psi_of_the_stopping_check():
     # rank errors per check at l = 0, 2, 4: sums 3e-9 + ..., stop when <= 1e-9
-    r0 = FakeRank(0, [1.0, 1e-6, 4e-10])
-    r1 = FakeRank(1, [1.0, 1e-6, 5e-10])
+    r0 = FakeRank(0, [1.0, 1e-6, 4e-10], itr_max=100, tol=1e-9)
+    r1 = FakeRank(1, [1.0, 1e-6, 5e-10], itr_max=100, tol=1e-9)
     l, qi, flag, err = shard._run([r0, r1], [None] * 2, [None] * 2, _gather, 100, 1e-9, 2, True)
     assert flag == 1 and l == 4 and err == 4e-10 + 5e-10
     checks = [c for c in r0.calls if c[0] == "half" and c[3]]
@@ -123,8 +138,8 @@ def test_loop_tolerance_keeps_psi_of_the_stopping_check():
 
 
 def test_loop_nonfinite_reports_first_iteration():
-    r0 = FakeRank(0, [1.0] * 10, bad_at=None)
-    r1 = FakeRank(1, [1.0] * 10, bad_at=3)
+    r0 = FakeRank(0, [1.0] * 10, bad_at=None, itr_max=50, tol=1e-12)
+    r1 = FakeRank(1, [1.0] * 10, bad_at=3, itr_max=50, tol=1e-12)
     l, qi, flag, err = shard._run([r0, r1], [None] * 2, [None] * 2, _gather, 50, 1e-12, 5, True)
     assert flag == 2
     assert l == 3  # the device-recorded first non-finite iteration, seen at the check at l = 5
@@ -134,8 +149,9 @@ def test_loop_fused_exchange_same_calls_no_totals():
     """fused exchange: the loop passes no totals (the kernels deliver them) and issues
     exactly the gathered loop's calls; the check-step errors still use `gather`."""
     for tol, errs in ((0.0, []), (1e-9, [1.0, 1e-6, 4e-10])):
-        g = [FakeRank(0, errs), FakeRank(1, errs)]
-        f = [FakeRank(0, errs, fused=True), FakeRank(1, errs, fused=True)]
+        kw = dict(itr_max=6, tol=tol)
+        g = [FakeRank(0, errs, **kw), FakeRank(1, errs, **kw)]
+        f = [FakeRank(0, errs, fused=True, **kw), FakeRank(1, errs, fused=True, **kw)]
         rg = shard._run(g, [None] * 2, [None] * 2, _gather, 6, tol, 2, True)
         rf = shard._run(f, [None] * 2, [None] * 2, _gather, 6, tol, 2, True, tgather=lambda ts: None)
         assert rg == rf
