@@ -25,10 +25,11 @@
  *    never allocates, frees or synchronises inside fs1_solve / fs1_cost /
  *    fs1_apply; every call is asynchronous on `stream` (a cudaStream_t,
  *    passed as void*, NULL = legacy default stream).
- *  - Batched layout: `batch` independent problems, each `n*m` contiguous
- *    values of the plan's dtype, problem-major: x[p*(n*m) + k].
+ *  - Batched layout: `batch` independent problems, each `n*m*l` contiguous
+ *    values of the plan's dtype, problem-major: x[p*(n*m*l) + k].
  *    2D arrays are flattened column-major, k = j*n + i, i along axis 1 (h1),
  *    j along axis 2 (h2)
+ *    3D (the extension of PAPER.md:314): k = (z*m + j)*n + i, z along axis 3 (h3).
  *  - Call-level errors are returned synchronously before any launch (only
  *    argument, shape and support problems are detected; data is not
  *    validated).  Per-problem outcomes go to device arrays.
@@ -87,7 +88,8 @@ typedef enum { FS1_SCALING = 0, FS1_LOG = 1, FS1_STABILIZED = 2 } fs1_domain;
 #define FS1_FLAG_ITR_MAX 4    /* stopped at itr_max                                  */
 
 typedef struct {
-  int32_t ndim;          /* 1 or 2                                                            */
+  int32_t ndim;          /* 1, 2 or 3 (3D: the separable extension PAPER.md:314 names; fp64
+                            scaling domain, the K5 kernel)                                    */
   int64_t n;             /* points along axis 1 (>= 1)                                         */
   int64_t m;             /* points along axis 2 (1 for ndim == 1)                             */
   double h1, h2;         /* grid spacings (> 0); h2 ignored when ndim == 1                   */
@@ -103,6 +105,8 @@ typedef struct {
   int32_t warm_start;    /* 1: u, v hold the initial phi, psi (LOG: F, G); 0: 1/(n m)        */
   double tau;            /* FS1_STABILIZED: absorption threshold (> 1; 0 selects 1e10, the
                             reading of the unstated tau, R30); ignored otherwise   */
+  int64_t l;             /* ndim == 3: points along axis 3 (>= 1); 0 or 1 otherwise         */
+  double h3;             /* ndim == 3: axis-3 spacing (> 0); ignored otherwise              */
 } fs1_desc;
 
 typedef struct fs1_plan_s fs1_plan_t;
@@ -123,9 +127,10 @@ typedef struct {
  *   out       : receives the plan (free with fs1_plan_destroy).
  *   workspace_bytes : receives the device workspace fs1_solve / fs1_cost need
  *               (may be 0; pass a buffer of at least this size, 256-byte aligned).
- * Kernel choice: n*m up to FS1_MAX_PERSIST points per problem ->
- * the persistent one-CTA-per-problem kernel; larger 1D problems -> the
- * multi-CTA HBM-streaming scan kernel; 2D -> the separable kernel.
+ * Kernel choice: 1D problems that fit one CTA -> the persistent
+ * one-CTA-per-problem kernel; larger 1D problems -> the multi-CTA HBM-streaming scan
+ * kernel; 2D fp32 log -> the separable warp-per-line kernel; 2D and 3D fp64 scaling ->
+ * the one-CTA-per-problem line kernel; FS1_STABILIZED -> the stabilised kernel.
  * Log domain range limits: a persistent chunk of E points needs
  * c E <= 40 (fp32) / 300 (fp64) and c 32 E <= 650 with c = h/eps; fs1_solve on a
  * streaming plan (fp64 log) needs c (min(n, 256) - 1) <= 600 and returns FS1_ERR_UNSUPPORTED

@@ -149,10 +149,54 @@ class _Ops2D:
         return np.array(out)
 
 
+class _Ops3D:
+    """The separable extension to three axes ("easily extended to
+    high-dimensional cases"): K = T_L(lambda3) (x) T_M(lambda2) (x) T_N(lambda1) on
+    column-major (N, M, L) arrays flattened as (z M + j) N + i, applied per axis (dense
+    per-axis kernels); cost with the weighted kernel on one axis at a time.  Scaling
+    domain, dense applies only."""
+
+    def __init__(self, n, m, l, h1, h2, h3, eps, apply):
+        assert apply == "dense"
+        self.n, self.m, self.l = n, m, l
+        self.K = [dense.kernel(n, dense.lam(h1, eps)), dense.kernel(m, dense.lam(h2, eps)),
+                  dense.kernel(l, dense.lam(h3, eps))]
+        self.W = [dense.weighted_kernel(n, dense.lam(h1, eps), h1), dense.weighted_kernel(m, dense.lam(h2, eps), h2),
+                  dense.weighted_kernel(l, dense.lam(h3, eps), h3)]
+
+    def _t(self, x):        # flat -> [i, j, z]
+        return x.reshape(self.l, self.m, self.n).transpose(2, 1, 0)
+
+    def _f(self, X):
+        return X.transpose(2, 1, 0).ravel()
+
+    def _app(self, mats, x):
+        # (K1 (x) K2 (x) K3) X, one axis at a time: Y_ijz = sum_abc K1_ia K2_jb K3_zc X_abc
+        X = self._t(x)
+        X = np.einsum("ia,ajz->ijz", mats[0], X)
+        X = np.einsum("jb,ibz->ijz", mats[1], X)
+        X = np.einsum("zc,ijc->ijz", mats[2], X)
+        return self._f(X)
+
+    def K_(self, x):
+        return np.stack([self._app(self.K, x[:, j]) for j in range(x.shape[1])], axis=1)
+
+    def cost(self, phi, psi):
+        out = []
+        for j in range(phi.shape[1]):
+            t = 0.0
+            for w in range(3):
+                mats = [self.W[a] if a == w else self.K[a] for a in range(3)]
+                t += float(phi[:, j] @ self._app(mats, psi[:, j]))
+            out.append(t)
+        return np.array(out)
+
+
 def solve(a, b, *, n, m=1, h1, h2=0.0, eps, itr_max, tol=0.0, domain="scaling",
           input_is_log=False, apply="dense", check_interval=1, u0=None, v0=None,
-          trace=None):
-    """Run Algorithm 1 (m == 1) or Algorithm 2 (m > 1) on one or many pairs.
+          trace=None, l=1, h3=0.0):
+    """Run Algorithm 1 (m == 1) or Algorithm 2 (m > 1; l > 1: its 3D extension) on one
+    or many pairs.
 
     a, b: [size] or [B, size]; promoted to fp64 (R16).
     Returns dict with F, G (log scalings, [B, size]), iters, err, flags, cost ([B]).
@@ -161,8 +205,12 @@ def solve(a, b, *, n, m=1, h1, h2=0.0, eps, itr_max, tol=0.0, domain="scaling",
     a = np.atleast_2d(np.asarray(a, dtype=np.float64))
     b = np.atleast_2d(np.asarray(b, dtype=np.float64))
     B, size = a.shape
-    assert size == n * m
-    ops = _Ops1D(n, h1, eps, apply) if m == 1 else _Ops2D(n, m, h1, h2, eps, apply)
+    assert size == n * m * l
+    if l > 1:
+        assert domain == "scaling", "3D: scaling domain only"
+        ops = _Ops3D(n, m, l, h1, h2, h3, eps, apply)
+    else:
+        ops = _Ops1D(n, h1, eps, apply) if m == 1 else _Ops2D(n, m, h1, h2, eps, apply)
     # work on [size, B] (pairs as columns; BLAS-friendly)
     a, b = a.T.copy(), b.T.copy()
     log_dom = domain == "log"

@@ -43,6 +43,8 @@ class Desc(ctypes.Structure):
         ("check_interval", ctypes.c_int32),
         ("warm_start", ctypes.c_int32),
         ("tau", ctypes.c_double),
+        ("l", ctypes.c_int64),
+        ("h3", ctypes.c_double),
     ]
 
 

@@ -394,7 +394,9 @@ static fs1_status plan_impl(const fs1_desc* desc, int device, int force, fs1_pla
   if (!desc || !out) return FS1_ERR_ARG;
   *out = nullptr;
   const fs1_desc& d = *desc;
-  if (d.ndim != 1 && d.ndim != 2) return FS1_ERR_ARG;
+  if (d.ndim != 1 && d.ndim != 2 && d.ndim != 3) return FS1_ERR_ARG;
+  if (d.ndim == 3 ? d.l < 1 : (d.l != 0 && d.l != 1)) return FS1_ERR_ARG;
+  if (d.ndim == 3 && (!(d.h3 > 0.0) || !isfinite(d.h3))) return FS1_ERR_EPS;
   if (d.n < 1 || d.m < 1 || d.batch < 1 || d.itr_max < 0 || d.check_interval < 1) return FS1_ERR_ARG;
   if (!(d.tol >= 0.0) || !isfinite(d.tol)) return FS1_ERR_ARG;
   if (d.ndim == 1 && d.m != 1) return FS1_ERR_ARG;
@@ -402,7 +404,7 @@ static fs1_status plan_impl(const fs1_desc* desc, int device, int force, fs1_pla
   if (d.domain != FS1_SCALING && d.domain != FS1_LOG && d.domain != FS1_STABILIZED) return FS1_ERR_ARG;
   if (d.domain == FS1_STABILIZED && !(d.tau == 0.0 || (d.tau > 1.0 && isfinite(d.tau)))) return FS1_ERR_ARG;
   if (!(d.eps > 0.0) || !isfinite(d.eps) || !(d.h1 > 0.0) || !isfinite(d.h1)) return FS1_ERR_EPS;
-  if (d.ndim == 2 && (!(d.h2 > 0.0) || !isfinite(d.h2))) return FS1_ERR_EPS;
+  if (d.ndim >= 2 && (!(d.h2 > 0.0) || !isfinite(d.h2))) return FS1_ERR_EPS;
   if (d.batch > 0x7fffffffLL) return FS1_ERR_UNSUPPORTED;
 
   fs1_plan_s* p = new (std::nothrow) fs1_plan_s();
@@ -457,27 +459,38 @@ static fs1_status plan_impl(const fs1_desc* desc, int device, int force, fs1_pla
     p->info.grid = d.batch;
     p->info.smem_bytes = p->smem;
     p->info.workspace_bytes = p->ws;
-  } else if (d.ndim == 2 && d.dtype == FS1_F64) {
-    // K5: Algorithm 2 in fp64 (scaling domain), one CTA per problem, a thread per line
-    if (d.domain != FS1_SCALING || d.n > 1024 || d.m > 1024) { delete p; return FS1_ERR_UNSUPPORTED; }
+  } else if (d.ndim == 3 || (d.ndim == 2 && d.dtype == FS1_F64)) {
+    // K5: Algorithm 2 (and its 3D extension) in fp64 (scaling domain), one CTA per
+    // problem, a thread per line
+    const long long L3 = d.ndim == 3 ? d.l : 1;
+    if (d.dtype != FS1_F64 || d.domain != FS1_SCALING || d.n * d.m * L3 > (1LL << 28)) {
+      delete p;
+      return FS1_ERR_UNSUPPORTED;
+    }
     p->kind = KIND_SEP64;
     Sep2d64Params& D = p->dbase;
     memset(&D, 0, sizeof(D));
     D.n = (int)d.n;
     D.m = (int)d.m;
+    D.l = (int)L3;
     D.lam1 = exp(-d.h1 / d.eps);
     D.lam2 = exp(-d.h2 / d.eps);
+    D.lam3 = d.ndim == 3 ? exp(-d.h3 / d.eps) : 0.0;
     D.h1 = d.h1;
     D.h2 = d.h2;
+    D.h3 = d.ndim == 3 ? d.h3 : 0.0;
     D.tol = d.tol;
     D.itr_max = d.itr_max;
     D.check_interval = d.check_interval;
     D.warm = d.warm_start;
-    const long long lines = std::max(d.n, d.m);
-    p->threads = (int)std::min<long long>(1024, ((lines + 31) / 32) * 32);
-    p->ws = al256((size_t)d.batch * 2 * (size_t)d.n * (size_t)d.m * 8);
+    // a thread per line of the busiest axis (2D: max(n, m); 3D: max(m l, n l, n m)), at most
+    // 512 (the kernel's launch bound)
+    const long long lines = d.ndim == 3 ? std::max<long long>(std::max<long long>(d.m * L3, d.n * L3), d.n * d.m)
+                                        : std::max<long long>(d.n, d.m);
+    p->threads = (int)std::min<long long>(512, ((lines + 31) / 32) * 32);
+    p->ws = al256((size_t)d.batch * 3 * (size_t)d.n * (size_t)d.m * (size_t)L3 * 8);
     p->smem = 0;
-    snprintf(p->info.kernel, sizeof(p->info.kernel), "sep2d64_f64_scaling");
+    snprintf(p->info.kernel, sizeof(p->info.kernel), d.ndim == 3 ? "sep3d64_f64_scaling" : "sep2d64_f64_scaling");
     p->info.chunk = 1;
     p->info.threads = p->threads;
     p->info.ctas_per_problem = 1;
@@ -761,7 +774,7 @@ fs1_status fs1_cost(const fs1_plan_t* plan, const void* u, const void* v, double
 fs1_status fs1_transport_plan(const fs1_plan_t* plan, const void* u, const void* v, void* gamma, void* stream) {
   if (!plan || !u || !v || !gamma) return FS1_ERR_ARG;
   const fs1_desc& d = plan->d;
-  if (d.n * d.m > FS1_MAX_TPLAN) return FS1_ERR_UNSUPPORTED;
+  if (d.ndim == 3 || d.n * d.m > FS1_MAX_TPLAN) return FS1_ERR_UNSUPPORTED;
   const double c1 = d.h1 / d.eps, c2 = d.ndim == 2 ? d.h2 / d.eps : 0.0;
   const cudaError_t e = launch_tplan(d.dtype == FS1_F64 ? 1 : 0, u, v, gamma, d.batch, d.n, d.m, c1, c2,
                                      d.domain != FS1_SCALING ? 1 : 0, (cudaStream_t)stream);
@@ -816,7 +829,8 @@ fs1_status fs1_dual(const fs1_plan_t* plan, const void* a, const void* b, const 
   const fs1_status st = fs1_apply(plan, v, scratch, workspace, stream);
   if (st != FS1_OK) return st;
   const fs1_desc& d = plan->d;
-  const cudaError_t e = launch_dual(d.dtype == FS1_F64 ? 1 : 0, a, b, u, v, scratch, d.batch, d.n * d.m, d.eps,
+  const long long size = d.n * d.m * (d.ndim == 3 ? d.l : 1);
+  const cudaError_t e = launch_dual(d.dtype == FS1_F64 ? 1 : 0, a, b, u, v, scratch, d.batch, size, d.eps,
                                     d.domain == FS1_LOG ? 1 : 0, d.domain == FS1_LOG ? d.input_is_log : 0, dual,
                                     (cudaStream_t)stream);
   return e == cudaSuccess ? FS1_OK : FS1_ERR_CUDA;

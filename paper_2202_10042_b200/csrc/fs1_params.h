@@ -188,7 +188,8 @@ struct StabParams {
 
 namespace fs1 {
 
-// K5: Algorithm 2 in fp64, scaling domain, one CTA per 2D problem (fs1_sep2d64.cu).
+// K5: Algorithm 2 (and its 3D extension) in fp64, scaling domain, one CTA per problem
+// (fs1_sep2d64.cu).
 struct Sep2d64Params {
   const double* a;   // [batch][n m] column-major histograms
   const double* b;
@@ -200,9 +201,9 @@ struct Sep2d64Params {
   double* cost;
   const double* x;   // apply: input / output
   double* y;
-  double* ws;        // [batch][2][n m]
-  int n, m;
-  double lam1, lam2, h1, h2, tol;
+  double* ws;        // [batch][3][n m l]
+  int n, m, l;       // l = 1 in 2D
+  double lam1, lam2, lam3, h1, h2, h3, tol;
   int itr_max, check_interval, warm;
   int mode;          // 0 solve, 1 cost, 2 apply
 };

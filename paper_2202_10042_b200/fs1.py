@@ -44,6 +44,8 @@ class Spec:
     warm_start: bool = False
     tau: float = 0.0         # "stabilized": absorption threshold (0 = the library default 1e10)
     kernel: int = 0          # 0 auto; test-only overrides (fs1__plan_kind in fs1_api.cu)
+    l: int = 1               # 3D: points along axis 3
+    h3: float = 0.0          # 3D: axis-3 spacing
 
     def desc(self) -> L.Desc:
         return L.Desc(ndim=self.ndim, n=self.n, m=self.m, h1=self.h1, h2=self.h2, eps=self.eps,
@@ -51,7 +53,8 @@ class Spec:
                       domain=_DOMAIN[self.domain],
                       input_is_log=int(self.input_is_log), itr_max=self.itr_max, tol=self.tol,
                       check_interval=self.check_interval, warm_start=int(self.warm_start),
-                      tau=float(self.tau))
+                      tau=float(self.tau), l=int(self.l) if self.ndim == 3 else 1,
+                      h3=float(self.h3) if self.ndim == 3 else 0.0)
 
 
 class Plan:
@@ -151,18 +154,36 @@ def _check(t, name, dtype, device, size, numel=None):
         raise ValueError(f"{name}: numel {t.numel()} != {numel} (one row per pair of a)")
 
 
+def _geom(t, shape, h, h2, h3):
+    """(ndim, n, m, l, size, h1, h2, h3) from a tensor's last axis (1D) or shape=(n, m) /
+    (n, m, l) (2D / 3D, column-major flat index (z m + j) n + i); h2, h3 default to h."""
+    if shape is None:
+        return 1, t.shape[-1], 1, 1, t.shape[-1], float(h), 0.0, 0.0
+    shape = tuple(int(x) for x in shape)
+    if len(shape) == 2:
+        n, m = shape
+        return 2, n, m, 1, n * m, float(h), float(h if h2 is None else h2), 0.0
+    if len(shape) == 3:
+        n, m, l = shape
+        return (3, n, m, l, n * m * l, float(h), float(h if h2 is None else h2),
+                float(h if h3 is None else h3))
+    raise ValueError(f"shape must have 2 or 3 axes, got {shape}")
+
+
+def _spec(t, shape, h, h2, h3, eps, batch, **kw):
+    ndim, n, m, l, size, h1, hh2, hh3 = _geom(t, shape, h, h2, h3)
+    return Spec(ndim=ndim, n=n, m=m, h1=h1, h2=hh2, eps=float(eps), batch=batch, dtype=t.dtype, l=l, h3=hh3, **kw)
+
+
 def solve(a, b, *, h, eps, itr_max, tol=0.0, domain="scaling", input_is_log=False,
-          check_interval=1, u0=None, v0=None, shape=None, h2=None, want_cost=True, kernel=0, tau=0.0):
-    """Batched FS-1 solve.  a, b: CUDA tensors [batch, n] (1D) or [batch, n*m] with
-    shape=(n, m) (2D, column-major).  domain: "scaling" | "log" | "stabilized" (the
-    paper's Remark 2.1 / 3.2 stabilisation, absorption threshold tau).
+          check_interval=1, u0=None, v0=None, shape=None, h2=None, h3=None, want_cost=True, kernel=0,
+          tau=0.0):
+    """Batched FS-1 solve.  a, b: CUDA tensors [batch, n] (1D) or [batch, n*m(*l)] with
+    shape=(n, m) / (n, m, l) (2D / 3D, column-major).  domain: "scaling" | "log" |
+    "stabilized" (the paper's Remark 2.1 / 3.2 stabilisation, absorption threshold tau).
     Returns dict u, v, iters, err, flags, cost."""
     dev = a.device.index
-    if shape is None:
-        ndim, n, m = 1, a.shape[-1], 1
-    else:
-        ndim, (n, m) = 2, shape
-    size = n * m
+    size = _geom(a, shape, h, h2, h3)[4]
     _check(a, "a", a.dtype, dev, size)
     _check(b, "b", a.dtype, dev, size, a.numel())
     if (u0 is None) != (v0 is None):
@@ -171,11 +192,9 @@ def solve(a, b, *, h, eps, itr_max, tol=0.0, domain="scaling", input_is_log=Fals
         _check(u0, "u0", a.dtype, dev, size, a.numel())
         _check(v0, "v0", a.dtype, dev, size, a.numel())
     batch = a.numel() // size
-    spec = Spec(ndim=ndim, n=n, m=m, h1=float(h), h2=float(h2 if h2 is not None else (h if ndim == 2 else 0.0)),
-                eps=float(eps), batch=batch, dtype=a.dtype, domain=domain,
-                input_is_log=bool(input_is_log), itr_max=int(itr_max), tol=float(tol),
-                check_interval=int(check_interval), warm_start=u0 is not None, kernel=int(kernel),
-                tau=float(tau))
+    spec = _spec(a, shape, h, h2, h3, eps, batch, domain=domain, input_is_log=bool(input_is_log),
+                 itr_max=int(itr_max), tol=float(tol), check_interval=int(check_interval),
+                 warm_start=u0 is not None, kernel=int(kernel), tau=float(tau))
     p = plan(spec, dev)
     if u0 is not None:
         u = u0.clone(memory_format=torch.contiguous_format)
@@ -190,29 +209,26 @@ def solve(a, b, *, h, eps, itr_max, tol=0.0, domain="scaling", input_is_log=Fals
     return {"u": u, "v": v, "iters": iters, "err": err, "flags": flags, "cost": cost}
 
 
-def cost(u, v, *, h, eps, domain="scaling", shape=None, h2=None, kernel=0):
+def cost(u, v, *, h, eps, domain="scaling", shape=None, h2=None, h3=None, kernel=0):
+    """The return line (PAPER.md:163 / 339) on a given state."""
     dev = u.device.index
-    ndim, n, m = (1, u.shape[-1], 1) if shape is None else (2, *shape)
-    size = n * m
+    size = _geom(u, shape, h, h2, h3)[4]
     _check(u, "u", u.dtype, dev, size)
     _check(v, "v", u.dtype, dev, size, u.numel())
     batch = u.numel() // size
-    spec = Spec(ndim=ndim, n=n, m=m, h1=float(h), h2=float(h2 if h2 is not None else (h if ndim == 2 else 0.0)),
-                eps=float(eps), batch=batch, dtype=u.dtype, domain=domain, itr_max=0, kernel=int(kernel))
+    spec = _spec(u, shape, h, h2, h3, eps, batch, domain=domain, itr_max=0, kernel=int(kernel))
     out = torch.empty(batch, dtype=torch.float64, device=u.device)
     plan(spec, dev).cost_into(u, v, out)
     return out
 
 
-def apply(x, *, h, eps, domain="scaling", shape=None, h2=None, kernel=0):
+def apply(x, *, h, eps, domain="scaling", shape=None, h2=None, h3=None, kernel=0):
     """y = K x (scaling) or log K e^x (log) for every vector of x."""
     dev = x.device.index
-    ndim, n, m = (1, x.shape[-1], 1) if shape is None else (2, *shape)
-    size = n * m
+    size = _geom(x, shape, h, h2, h3)[4]
     _check(x, "x", x.dtype, dev, size)
     batch = x.numel() // size
-    spec = Spec(ndim=ndim, n=n, m=m, h1=float(h), h2=float(h2 if h2 is not None else (h if ndim == 2 else 0.0)),
-                eps=float(eps), batch=batch, dtype=x.dtype, domain=domain, itr_max=0, kernel=int(kernel))
+    spec = _spec(x, shape, h, h2, h3, eps, batch, domain=domain, itr_max=0, kernel=int(kernel))
     y = torch.empty_like(x)
     plan(spec, dev).apply_into(x, y)
     return y
@@ -221,13 +237,11 @@ def apply(x, *, h, eps, domain="scaling", shape=None, h2=None, kernel=0):
 def transport_plan(u, v, *, h, eps, domain="scaling", shape=None, h2=None):
     """gamma = diag(phi) K diag(psi) per problem: [batch, n*m, n*m] (fs1_transport_plan)."""
     dev = u.device.index
-    ndim, n, m = (1, u.shape[-1], 1) if shape is None else (2, *shape)
-    size = n * m
+    size = _geom(u, shape, h, h2, None)[4]
     _check(u, "u", u.dtype, dev, size)
     _check(v, "v", u.dtype, dev, size, u.numel())
     batch = u.numel() // size
-    spec = Spec(ndim=ndim, n=n, m=m, h1=float(h), h2=float(h2 if h2 is not None else (h if ndim == 2 else 0.0)),
-                eps=float(eps), batch=batch, dtype=u.dtype, domain=domain, itr_max=0)
+    spec = _spec(u, shape, h, h2, None, eps, batch, domain=domain, itr_max=0)
     g = torch.empty(batch, size, size, dtype=u.dtype, device=u.device)
     p = plan(spec, dev)
     s = L.lib().fs1_transport_plan(p._h, _ptr(u), _ptr(v), _ptr(g), _stream(dev))
@@ -236,18 +250,16 @@ def transport_plan(u, v, *, h, eps, domain="scaling", shape=None, h2=None):
     return g
 
 
-def dual(a, b, u, v, *, h, eps, domain="scaling", input_is_log=False, shape=None, h2=None, kernel=0):
+def dual(a, b, u, v, *, h, eps, domain="scaling", input_is_log=False, shape=None, h2=None, h3=None, kernel=0):
     """fs1_dual: the dual objective of Eq. (2.3) at the state (u, v) for every pair ([batch] fp64)."""
     dev = u.device.index
-    ndim, n, m = (1, u.shape[-1], 1) if shape is None else (2, *shape)
-    size = n * m
+    size = _geom(u, shape, h, h2, h3)[4]
     _check(u, "u", u.dtype, dev, size)
     for t, nm in ((a, "a"), (b, "b"), (v, "v")):
         _check(t, nm, u.dtype, dev, size, u.numel())
     batch = u.numel() // size
-    spec = Spec(ndim=ndim, n=n, m=m, h1=float(h), h2=float(h2 if h2 is not None else (h if ndim == 2 else 0.0)),
-                eps=float(eps), batch=batch, dtype=u.dtype, domain=domain, input_is_log=bool(input_is_log),
-                itr_max=0, kernel=int(kernel))
+    spec = _spec(u, shape, h, h2, h3, eps, batch, domain=domain, input_is_log=bool(input_is_log), itr_max=0,
+                 kernel=int(kernel))
     p = plan(spec, dev)
     scratch = torch.empty_like(u)
     out = torch.empty(batch, dtype=torch.float64, device=u.device)
@@ -263,20 +275,15 @@ def solve_eps_scaling(a, b, *, h, eps, eps0, factor, stage_iters, itr_max, tol=0
     """fs1_solve_eps_scaling (log domain): the eps-scaling continuation eps0 -> eps; outputs as
     solve() for the last stage, plus 'stages'."""
     dev = a.device.index
-    if shape is None:
-        ndim, n, m = 1, a.shape[-1], 1
-    else:
-        ndim, (n, m) = 2, shape
-    size = n * m
+    size = _geom(a, shape, h, h2, None)[4]
     _check(a, "a", a.dtype, dev, size)
     _check(b, "b", a.dtype, dev, size, a.numel())
     if (u0 is None) != (v0 is None):
         raise ValueError("warm start needs both u0 and v0 (or neither)")
     batch = a.numel() // size
-    spec = Spec(ndim=ndim, n=n, m=m, h1=float(h), h2=float(h2 if h2 is not None else (h if ndim == 2 else 0.0)),
-                eps=float(eps), batch=batch, dtype=a.dtype, domain="log", input_is_log=bool(input_is_log),
-                itr_max=int(itr_max), tol=float(tol), check_interval=int(check_interval),
-                warm_start=u0 is not None)
+    spec = _spec(a, shape, h, h2, None, eps, batch, domain="log", input_is_log=bool(input_is_log),
+                 itr_max=int(itr_max), tol=float(tol), check_interval=int(check_interval),
+                 warm_start=u0 is not None)
     d = spec.desc()
     ns = ctypes.c_int32()
     wsb = ctypes.c_size_t()
