@@ -61,7 +61,12 @@ template <class T, int E, int WARPS, bool LOGD> struct Persist {
   static constexpr size_t OFF_XE = OFF_XM + 4 * WARPS * sizeof(double);  // [2][2][WARPS] int
   static constexpr size_t OFF_RED = OFF_XE + 4 * WARPS * sizeof(int);    // [2][WARPS] double
   static constexpr size_t OFF_INT = OFF_RED + 2 * WARPS * sizeof(double);  // [2][WARPS] int
-  static constexpr size_t SMEM = OFF_INT + 2 * WARPS * sizeof(int);
+  static constexpr size_t OFF_LPM = (OFF_INT + 2 * WARPS * sizeof(int) + 15) & ~(size_t)15;  // [32] double
+  static constexpr size_t OFF_LPE = OFF_LPM + 32 * sizeof(double);                          // [32] int
+  // log domain, multi-warp CTAs: the lane powers lambda^{E l} (ER) live in shared memory,
+  // read lane-indexed where the cross-warp carries use them (held in registers they were
+  // re-read from the parameter bank with lane-divergent addresses on every half-step)
+  static constexpr size_t SMEM = OFF_LPE + 32 * sizeof(int);
 
   // vector j of thread t at s[j * NT + t]: consecutive threads read consecutive 16-byte
   // words (conflict-free) and every access is one base register plus an immediate offset
@@ -196,6 +201,18 @@ template <class T, int E, int WARPS, bool LOGD> struct Persist {
       cb = er_add(cb, er_mul(CG, rP));
     }
   }
+  // the same with the lane powers read from a lane-indexed shared table where they are
+  // used (K1: held in registers they were re-read from the parameter bank with
+  // lane-divergent addresses on every half-step)
+  __device__ __forceinline__ static void carries_er(T f, T g, int xe, ER<double>& cf, ER<double>& cb,
+                                                    const PersistParams& P, double* xm, int* xi, int par,
+                                                    int lane, int warp, const double* lpm, const int* lpe) {
+    if constexpr (WARPS > 1)
+      carries_er(f, g, xe, cf, cb, P, xm, xi, par, lane, warp, ER<double>{lpm[lane], lpe[lane]},
+                 ER<double>{lpm[31 - lane], lpe[31 - lane]});
+    else
+      carries_er(f, g, xe, cf, cb, P, xm, xi, par, lane, warp, er_zero<double>(), er_zero<double>());
+  }
 };
 
 // ---------------------------------------------------------------------------------------
@@ -212,7 +229,8 @@ template <class T, int E, int WARPS, bool LOGD> struct Half {
     int tid, lane, warp, nv;
     T lam, lamS;  // lambda, lambda^S (S = E / NCH: one sub-chain run)
     T lA, lB, rA, rB;        // scaling: lane powers
-    ER<double> lP, rP;       // log: lane powers
+    const double* lpm;       // log: lane powers lambda^{E l} (shared memory)
+    const int* lpe;
     double* xm;
     int* xi;
   };
@@ -384,7 +402,7 @@ template <class T, int E, int WARPS, bool LOGD> struct Half {
       }
     } else {
       ER<double> CF, CB;
-      PS::carries_er(f, g, xe, CF, CB, P, c.xm, c.xi, par, c.lane, c.warp, c.lP, c.rP);
+      PS::carries_er(f, g, xe, CF, CB, P, c.xm, c.xi, par, c.lane, c.warp, c.lpm, c.lpe);
       const int xeff = (f > T(0)) ? xe : ZE;
       R = xeff;
       slow = (CF.e - xeff > Tt::LIM) || (CB.e - xeff > Tt::LIM);
@@ -647,8 +665,14 @@ __global__ void __launch_bounds__(32 * WARPS, (persist_minb<T, E, WARPS>())) fs1
     c.lA = (T)P.laneA[c.lane]; c.lB = (T)P.laneB[c.lane];
     c.rA = (T)P.laneA[31 - c.lane]; c.rB = (T)P.laneB[31 - c.lane];
   } else {
-    c.lP = ER<double>{P.lanem[c.lane], P.lanee[c.lane]};
-    c.rP = ER<double>{P.lanem[31 - c.lane], P.lanee[31 - c.lane]};
+    double* lpm = reinterpret_cast<double*>(smem + PS::OFF_LPM);
+    int* lpe = reinterpret_cast<int*>(smem + PS::OFF_LPE);
+    if (c.tid < 32) {
+      lpm[c.tid] = P.lanem[c.tid];
+      lpe[c.tid] = P.lanee[c.tid];
+    }
+    c.lpm = lpm;
+    c.lpe = lpe;
   }
   // warp-uniform: the masked and unmasked paths contain different barriers
   const bool full = __all_sync(FULL, c.nv == E);
@@ -794,9 +818,14 @@ __global__ void __launch_bounds__(32 * WARPS) fs1_persist_apply(const PersistPar
                     (T)P.laneA[31 - lane], (T)P.laneB[31 - lane]);
   } else {
     ER<double> CF, CB;
-    PS::carries_er(f, g, ve, CF, CB, P, xm, xi, 0, lane, warp,
-                   ER<double>{P.lanem[lane], P.lanee[lane]},
-                   ER<double>{P.lanem[31 - lane], P.lanee[31 - lane]});
+    double* lpm = reinterpret_cast<double*>(smem + PS::OFF_LPM);
+    int* lpe = reinterpret_cast<int*>(smem + PS::OFF_LPE);
+    if (tid < 32) {
+      lpm[tid] = P.lanem[tid];
+      lpe[tid] = P.lanee[tid];
+    }
+    __syncthreads();
+    PS::carries_er(f, g, ve, CF, CB, P, xm, xi, 0, lane, warp, lpm, lpe);
     const int xeff = (f > T(0)) ? ve : ZE;
     R = max(xeff, max(CF.e, CB.e));
     s = Tt::pow2(max(ve - R, -1000));
