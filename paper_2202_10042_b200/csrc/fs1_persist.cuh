@@ -62,8 +62,9 @@ template <class T, int E, int WARPS, bool LOGD> struct Persist {
   static constexpr size_t OFF_RED = OFF_XE + 4 * WARPS * sizeof(int);    // [2][WARPS] double
   static constexpr size_t OFF_INT = OFF_RED + 2 * WARPS * sizeof(double);  // [2][WARPS] int
   static constexpr size_t OFF_LPM = (OFF_INT + 2 * WARPS * sizeof(int) + 15) & ~(size_t)15;  // [32] double
-  static constexpr size_t OFF_LPE = OFF_LPM + 32 * sizeof(double);                          // [32] int
-  // log domain, multi-warp CTAs: the lane powers lambda^{E l} (ER) live in shared memory,
+  static constexpr size_t OFF_LPE = OFF_LPM + 64 * sizeof(double);                          // [32] int
+  // multi-warp CTAs: the lane powers lambda^{E l} (log: ER; scaling: the two factors
+  // laneA, laneB at [0, 32) and [32, 64)) live in shared memory,
   // read lane-indexed where the cross-warp carries use them (held in registers they were
   // re-read from the parameter bank with lane-divergent addresses on every half-step)
   static constexpr size_t SMEM = OFF_LPE + 32 * sizeof(int);
@@ -228,7 +229,7 @@ template <class T, int E, int WARPS, bool LOGD> struct Half {
   struct Ctx {
     int tid, lane, warp, nv;
     T lam, lamS;  // lambda, lambda^S (S = E / NCH: one sub-chain run)
-    T lA, lB, rA, rB;        // scaling: lane powers
+    const double* lab;       // scaling: lane powers laneA[32], laneB[32] (shared memory)
     const double* lpm;       // log: lane powers lambda^{E l} (shared memory)
     const int* lpe;
     double* xm;
@@ -371,7 +372,8 @@ template <class T, int E, int WARPS, bool LOGD> struct Half {
     int R = 0;
     bool slow = false;
     if constexpr (!LOGD) {
-      PS::carries_lin(f, g, cf, cb, P, c.xm, par, c.lane, c.warp, c.lA, c.lB, c.rA, c.rB);
+      PS::carries_lin(f, g, cf, cb, P, c.xm, par, c.lane, c.warp, (T)c.lab[c.lane], (T)c.lab[32 + c.lane],
+                      (T)c.lab[31 - c.lane], (T)c.lab[63 - c.lane]);
     } else if constexpr (WARPS == 1) {
       // one warp: the ER carries of carries_er() in plain doubles relative to the warp's
       // largest chunk exponent Rw; exact exponents only where the slow-path test needs them
@@ -662,8 +664,12 @@ __global__ void __launch_bounds__(32 * WARPS, (persist_minb<T, E, WARPS>())) fs1
   c.xm = xm;
   c.xi = xi;
   if constexpr (!LOGD) {
-    c.lA = (T)P.laneA[c.lane]; c.lB = (T)P.laneB[c.lane];
-    c.rA = (T)P.laneA[31 - c.lane]; c.rB = (T)P.laneB[31 - c.lane];
+    double* lab = reinterpret_cast<double*>(smem + PS::OFF_LPM);
+    if (c.tid < 32) {
+      lab[c.tid] = P.laneA[c.tid];
+      lab[32 + c.tid] = P.laneB[c.tid];
+    }
+    c.lab = lab;
   } else {
     double* lpm = reinterpret_cast<double*>(smem + PS::OFF_LPM);
     int* lpe = reinterpret_cast<int*>(smem + PS::OFF_LPE);
