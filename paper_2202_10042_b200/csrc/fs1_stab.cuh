@@ -68,6 +68,7 @@ __device__ __forceinline__ Aff compose(Aff L, Aff E) {  // L after E
 }
 __device__ __forceinline__ Aff shfl_up_m(Aff x, int d) { return Aff{shfl_up_er(x.M, d), shfl_up_er(x.C, d)}; }
 __device__ __forceinline__ Aff shfl_down_m(Aff x, int d) { return Aff{shfl_down_er(x.M, d), shfl_down_er(x.C, d)}; }
+__device__ __forceinline__ Aff shfl_idx_m(Aff x, int s) { return Aff{shfl_idx_er(x.M, s), shfl_idx_er(x.C, s)}; }
 
 // (p, P) -> (a p + c1, b p + a P + c2): the Jordan-block maps of the cost scan
 struct Jor {
@@ -110,6 +111,46 @@ __device__ __forceinline__ Map block_scan_excl(Map x, Map* sm) {
   return compose(ex, cw);
 }
 
+// Both directions of the half-step's affine-map scan with one block barrier: warp
+// inclusive scans (forward up, backward down), the warp totals through shared memory,
+// then every warp scans the W totals across its lanes (lane j <-> warp j, shuffle
+// levels instead of a serial fold) and takes the composite of the warps before /
+// after it.  Returns the exclusive maps of this thread's chunk.  Deterministic.
+template <int W>
+__device__ __forceinline__ void block_scan2(Aff xf, Aff xb, Aff* sm, Aff& ef, Aff& eb) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const Aff yf = shfl_up_m(xf, d);
+    const Aff yb = shfl_down_m(xb, d);
+    if (lane >= d) xf = compose(xf, yf);
+    if (lane + d < 32) xb = compose(xb, yb);
+  }
+  if (lane == 31) sm[warp] = xf;
+  if (lane == 0) sm[W + warp] = xb;
+  __syncthreads();
+  // lanes j < W hold warp j's totals; inclusive scans across them
+  Aff wf = lane < W ? sm[lane] : ident((Aff*)nullptr);
+  Aff wb = lane < W ? sm[W + lane] : ident((Aff*)nullptr);
+#pragma unroll
+  for (int d = 1; d < W; d <<= 1) {
+    const Aff yf = shfl_up_m(wf, d);
+    const Aff yb = shfl_down_m(wb, d);
+    if (lane >= d) wf = compose(wf, yf);
+    if (lane + d < W) wb = compose(wb, yb);
+  }
+  // composite of the warps before (after) this one: lane warp-1 (warp+1) of the scans
+  Aff cwf = shfl_idx_m(wf, warp > 0 ? warp - 1 : 0);
+  Aff cwb = shfl_idx_m(wb, warp + 1 < W ? warp + 1 : 0);
+  if (warp == 0) cwf = ident((Aff*)nullptr);
+  if (warp == W - 1) cwb = ident((Aff*)nullptr);
+  Aff xef = shfl_up_m(xf, 1), xeb = shfl_down_m(xb, 1);
+  if (lane == 0) xef = ident((Aff*)nullptr);
+  if (lane == 31) xeb = ident((Aff*)nullptr);
+  ef = compose(xef, cwf);
+  eb = compose(xeb, cwb);
+}
+
 __device__ __forceinline__ double block_sum(double v, double* red, int W) {
   v = warp_sum(v);
   __syncthreads();
@@ -140,27 +181,39 @@ __device__ __forceinline__ void half(long long n, const double* xs, double* ys, 
                                      double& errp) {
   constexpr int T = 32 * W;
   const int t = threadIdx.x;
-  // pass 1: the chunk's forward / backward maps
-  ER<double> Mf = er1(), Mb = er1();
+  // pass 1: the chunk's forward / backward maps.  The products M of the chunk's E
+  // coefficients are formed in plain fp64 (no extended-range step per point) unless one
+  // leaves [2^-960, 2^960] — then the chunk recomputes them in extended range, so no
+  // product of many coefficients ever under/overflows on its own (Remark 3.3).
+  double mf = 1.0, mb = 1.0;
   double Cf = 0.0, Cb = 0.0;
 #pragma unroll 4
   for (int e = 0; e < E; ++e) {
     const int i = e * T + t;
-    const double f = ld_(fv + i);
-    Cf = fma(f, Cf, ld_(wv + i) * xs[i]);
-    Mf = er_mul(Mf, erd(f));
+    const double f = ld_(fv + i), g = ld_(gv + E * T - T - e * T + t);
+    const double xf = ld_(wv + i) * xs[i];
+    const int j = (E - 1 - e) * T + t;
+    Cf = fma(f, Cf, xf);
+    Cb = fma(g, Cb, ld_(wv + j) * xs[j]);
+    mf *= f;
+    mb *= g;
   }
-#pragma unroll 4
-  for (int e = E - 1; e >= 0; --e) {
-    const int i = e * T + t;
-    const double g = ld_(gv + i);
-    Cb = fma(g, Cb, ld_(wv + i) * xs[i]);
-    Mb = er_mul(Mb, erd(g));
+  ER<double> Mf, Mb;
+  const double LO = 0x1p-960, HI = 0x1p960;
+  if ((mf == 0.0 || (mf >= LO && mf <= HI)) && (mb == 0.0 || (mb >= LO && mb <= HI))) {
+    Mf = erd(mf);
+    Mb = erd(mb);
+  } else {
+    Mf = er1();
+    Mb = er1();
+    for (int e = 0; e < E; ++e) {
+      Mf = er_mul(Mf, erd(ld_(fv + e * T + t)));
+      Mb = er_mul(Mb, erd(ld_(gv + e * T + t)));
+    }
   }
   // carries: r just before this chunk, u just after it (both from zero at the ends)
-  const Aff cf = block_scan_excl<Aff, W, true>(Aff{Mf, er_norm<double>(fabs(Cf), 0)}, sm);
-  __syncthreads();
-  const Aff cb = block_scan_excl<Aff, W, false>(Aff{Mb, er_norm<double>(fabs(Cb), 0)}, sm);
+  Aff cf, cb;
+  block_scan2<W>(Aff{Mf, er_norm<double>(fabs(Cf), 0)}, Aff{Mb, er_norm<double>(fabs(Cb), 0)}, sm, cf, cb);
   double r = er_val(cf.C);
   double u = er_val(cb.C);
   // pass 2: the forward recursion r_k
