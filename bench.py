@@ -127,10 +127,10 @@ DFMA_PER_UPDATE = 16
 
 
 def launches_per_solve(info, batch):
-    """Library kernels one fs1_solve launches: K1 one launch for the whole batch; K2 and
-    K3w / K3 one cooperative launch per problem (each preceded by a cudaMemsetAsync of
-    its grid-barrier counter, which is not a kernel)."""
-    return 1 if info["kernel"].startswith(("persist", "stab")) else batch
+    """Library kernels one fs1_solve launches: K1, K4, K5 one launch for the whole batch;
+    K2 and K3w / K3 one cooperative launch per problem (each preceded by a
+    cudaMemsetAsync of its grid-barrier counter, which is not a kernel)."""
+    return 1 if info["kernel"].startswith(("persist", "stab", "sep2d64", "sep3d64")) else batch
 
 
 def roofline(cfg, info, updates, it_run, batch, kern_s, peaks, src, props):
@@ -144,7 +144,7 @@ def roofline(cfg, info, updates, it_run, batch, kern_s, peaks, src, props):
     wb = 8 if cfg.dtype == "f64" else 4
     sms = props.multi_processor_count
     clk = peaks.get("sm_max_mhz", 1965.0)
-    onchip = kern.startswith(("persist", "stab", "sep2d64"))   # one CTA per problem (K1, K4, K5)
+    onchip = kern.startswith(("persist", "stab", "sep2d64", "sep3d64"))   # one CTA per problem (K1, K4, K5)
     if onchip:
         alg = 4 * wb * cfg.size * batch
     else:
