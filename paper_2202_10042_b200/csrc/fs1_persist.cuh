@@ -240,7 +240,8 @@ template <class T, int E, int WARPS, bool LOGD> struct Half {
   // points whose recursions run interleaved; run c enters with the carry
   // lam^S (carry of run c-1) + (run c-1's aggregate).  S stays a multiple of the
   // shared-memory vector width.
-  static constexpr int NCH = (E / PS::VEC >= 4 && FS1_NCH >= 4) ? 4 : ((E / PS::VEC >= 2 && FS1_NCH >= 2) ? 2 : 1);
+  static constexpr int NCH = (E / PS::VEC >= 8 && FS1_NCH >= 8) ? 8
+                             : (E / PS::VEC >= 4 && FS1_NCH >= 4) ? 4 : ((E / PS::VEC >= 2 && FS1_NCH >= 2) ? 2 : 1);
   static constexpr int S = E / NCH;
 
   // 3. the recursions from the exact carries (fq: forward run aggregates, gq: backward)
