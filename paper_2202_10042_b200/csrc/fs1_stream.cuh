@@ -599,15 +599,25 @@ __device__ __forceinline__ void warp_step_in(Ctx& c, const StreamParams& P, int 
   const ER<double> CFx = warp_er_sum(xf), CBx = warp_er_sum(xb);
   err = warp_sum(xs);
   flag = __reduce_or_sync(FULL, (unsigned)xl);
+  // full carries of this warp's tiles: lambda^{256 i} CFx + local exclusive carry (and
+  // the backward mirror), formed directly relative to the tile's reference exponent R
+  // in plain fp64 (integer exponent arithmetic, no extended-range normalisation): the
+  // two terms are m 2^e with m < 4; R = the tile exponent X unless an upper bound of a
+  // carry's exponent exceeds X + LIM (then R = that bound).
+  const bool fz = !(CFx.m > 0.0), bz = !(CBx.m > 0.0);
   for (int i = c.warp + c.lane * c.NW; i < c.nt; i += 32 * c.NW) {
-    const ER<double> CF = er_fma(pw(c, i), CFx, ER<double>{Fm[i], Fe[i]});
-    const ER<double> CB = er_fma(pw(c, c.nt - 1 - i), CBx, ER<double>{Bm[i], Be[i]});
+    const int j = c.nt - 1 - i;
+    const double fa = c.pwm[i] * CFx.m, ba = c.pwm[j] * CBx.m;
+    const int efa = fz ? ZE : c.pwe[i] + CFx.e, eba = bz ? ZE : c.pwe[j] + CBx.e;
+    const double fb = Fm[i], bb = Bm[i];
+    const int efb = fb > 0.0 ? Fe[i] : ZE, ebb = bb > 0.0 ? Be[i] : ZE;
+    const int EF = max(efa, efb), EB = max(eba, ebb);
     const int X = Xx[i];
     int R = X;
-    if (X == ZE || CF.e - X > LIM || CB.e - X > LIM) R = max(CF.e, CB.e);
-    if (R == ZE) R = 0;
-    c.cfr[i] = er_rel(CF, R);
-    c.cbr[i] = er_rel(CB, R);
+    if (X == ZE || EF + 2 - X > LIM || EB + 2 - X > LIM) R = max(EF, EB) + 2;
+    if (R <= ZE + 2) R = 0;
+    c.cfr[i] = fa * pow2d(max(efa - R, -1100)) + fb * pow2d(max(efb - R, -1100));
+    c.cbr[i] = ba * pow2d(max(eba - R, -1100)) + bb * pow2d(max(ebb - R, -1100));
     c.Rr[i] = R;
   }
   __syncwarp();
@@ -1309,6 +1319,7 @@ __global__ void __launch_bounds__(32 * NW, 1) fs1_stream_kernel(const __grid_con
     {
       ER<double> tF = er_zero<double>(), tB = er_zero<double>();
       if (!last) block_tile_scan(c, c.QFm, c.QFe, c.QBm, c.QBe, tF, tB);
+      if (td) td[5] = gtimer();
       double es = 0.0;
       if (check) {
         // deterministic per-range error sum
@@ -1324,9 +1335,11 @@ __global__ void __launch_bounds__(32 * NW, 1) fs1_stream_kernel(const __grid_con
         __syncthreads();
       }
       const int nf = __syncthreads_or(nonfinite);
+      if (td) td[6] = gtimer();
       publish(c, P, par ^ 1, tF, tB, es, nf);
       if (td) td[3] = gtimer();
       grid_barrier(P.bar, P.G, c.gen);
+      if (td) td[7] = gtimer();
       par ^= 1;
     }
     {

@@ -32,3 +32,10 @@ print(f"CTAs {G}; psi half-step (us): stream med {med(stream):.2f} max {med(stre
       f"min {med(stream.min(0)):.2f} | tile scan+publish {med(scan):.2f} | barrier+fold {med(wait_fold):.2f} "
       f"| iteration {med(step):.2f}")
 print("  per-CTA stream (us): p10 %.2f p50 %.2f p90 %.2f" % tuple(np.percentile(stream, [10, 50, 90]) / 1e3))
+scan_only = t[:, :, 5] - t[:, :, 1]
+sync_or = t[:, :, 6] - t[:, :, 5]
+pub = t[:, :, 3] - t[:, :, 6]
+bar = t[:, :, 7] - t[:, :, 3]
+fold = t[:, :, 4] - t[:, :, 7]
+print(f"  tile scan {med(scan_only):.2f} | sync_or {med(sync_or):.2f} | publish {med(pub):.2f} | barrier wait "
+      f"{med(bar):.2f} (slowest-arriving CTA: {np.median(bar.min(0))/1e3:.2f}) | fold+carries {med(fold):.2f}")
