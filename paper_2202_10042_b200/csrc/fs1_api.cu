@@ -488,6 +488,18 @@ static fs1_status plan_impl(const fs1_desc* desc, int device, int force, fs1_pla
     const long long lines = d.ndim == 3 ? std::max<long long>(std::max<long long>(d.m * L3, d.n * L3), d.n * d.m)
                                         : std::max<long long>(d.n, d.m);
     p->threads = (int)std::min<long long>(512, ((lines + 31) / 32) * 32);
+    // small 2D problems: the intermediate in shared memory (fs1_sep2d64.cu)
+    const size_t ssm = sep2d64_smem(d.n, d.m, d.ndim);
+    if (ssm) {
+      std::lock_guard<std::mutex> lk(g_attr_mu);
+      int cur = 0;
+      if (cudaGetDevice(&cur) != cudaSuccess) { delete p; return FS1_ERR_CUDA; }
+      if (cur != device && cudaSetDevice(device) != cudaSuccess) { delete p; return FS1_ERR_CUDA; }
+      const cudaError_t e = cudaFuncSetAttribute(sep2d64_fn(), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
+      if (cur != device) cudaSetDevice(cur);
+      if (e != cudaSuccess) { delete p; return FS1_ERR_CUDA; }
+      D.staged = 1;
+    }
     p->ws = al256((size_t)d.batch * 3 * (size_t)d.n * (size_t)d.m * (size_t)L3 * 8);
     p->smem = 0;
     snprintf(p->info.kernel, sizeof(p->info.kernel), d.ndim == 3 ? "sep3d64_f64_scaling" : "sep2d64_f64_scaling");

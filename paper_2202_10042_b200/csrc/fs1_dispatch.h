@@ -60,6 +60,8 @@ const StabEntry* stab_table(int* count);
 
 // K5 fp64 scaling-domain 2D solve, one CTA per problem (fs1_sep2d64.cu)
 cudaError_t launch_sep2d64(const Sep2d64Params& P, long long batch, int threads, cudaStream_t st);
+size_t sep2d64_smem(long long n, long long m, int ndim);  // dynamic shared memory of the staged 2D path (0: none)
+const void* sep2d64_fn();
 
 // dual objective and eps-scaling warm start (fs1_extra.cu)
 cudaError_t launch_dual(int dtype, const void* a, const void* b, const void* u, const void* v, const void* s,

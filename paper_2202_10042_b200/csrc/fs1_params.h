@@ -206,6 +206,7 @@ struct Sep2d64Params {
   double lam1, lam2, lam3, h1, h2, h3, tol;
   int itr_max, check_interval, warm;
   int mode;          // 0 solve, 1 cost, 2 apply
+  int staged;        // 2D with n m <= SMEM_NM: the intermediate lives in shared memory
 };
 
 }  // namespace fs1

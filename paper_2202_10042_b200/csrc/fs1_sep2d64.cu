@@ -150,6 +150,87 @@ __device__ __forceinline__ void line_pass(const Geo& g, int ax, const double* __
   }
 }
 
+// ---- 2D problems whose intermediate fits shared memory (n m <= SMEM_NM): the axis-1
+// result T lives in shared memory (columns padded to n + 1 doubles: the column pass's
+// threads hit distinct banks) and the axis-2 pass stages its forward values there too,
+// so both sweeps run at shared-memory latency; only x, the targets and y touch global
+// memory (loads issued 8 deep ahead).
+constexpr int SMEM_NM = 13600;  // (n + 1) m + n m doubles <= 227 KB
+
+// axis 1: T[j (n+1) + i] = (K1 x[:, j])_i, thread per column j (x from global memory,
+// loads issued 8 deep; copying x into shared memory first measured slower)
+__device__ __forceinline__ void col_pass_s(const double* __restrict__ x, double* T, int n, int m, double lam) {
+  for (int j = threadIdx.x; j < m; j += blockDim.x) {
+    const double* xc = x + (size_t)j * n;
+    double* tc = T + (size_t)j * (n + 1);
+    double r = 0.0;
+    for (int k0 = 0; k0 < n; k0 += U8) {
+      double xv[U8];
+#pragma unroll
+      for (int u = 0; u < U8; ++u) xv[u] = (k0 + u < n) ? xc[k0 + u] : 0.0;
+#pragma unroll
+      for (int u = 0; u < U8; ++u)
+        if (k0 + u < n) {
+          r = (k0 + u == 0) ? xv[u] : fma(lam, r, xv[u]);
+          tc[k0 + u] = r;
+        }
+    }
+    double s = 0.0, xn = 0.0;
+    for (int k1 = n - 1; k1 >= 0; k1 -= U8) {
+      double xv[U8];
+#pragma unroll
+      for (int u = 0; u < U8; ++u) xv[u] = (k1 - u >= 0) ? xc[k1 - u] : 0.0;
+#pragma unroll
+      for (int u = 0; u < U8; ++u) {
+        const int k = k1 - u;
+        if (k < 0) break;
+        if (k < n - 1) s = lam * (s + xn);
+        xn = xv[u];
+        tc[k] += s;
+      }
+    }
+  }
+}
+
+// axis 2 fused with the update: y[:, ] = tgt / (K2 T[i, :]) per row i (thread per row);
+// forward values staged in Rs[j n + i]; CHECK: acc += |yold k - tgt|
+template <bool CHECK>
+__device__ __forceinline__ void row_pass_s(const double* T, double* Rs, const double* __restrict__ tgt,
+                                           const double* __restrict__ yold, double* __restrict__ y, int n, int m,
+                                           double lam, double& acc, int& bad) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    double r = 0.0;
+    for (int j = 0; j < m; ++j) {
+      const double t = T[(size_t)j * (n + 1) + i];
+      r = (j == 0) ? t : fma(lam, r, t);
+      Rs[(size_t)j * n + i] = r;
+    }
+    double s = 0.0;
+    for (int j1 = m - 1; j1 >= 0; j1 -= U8) {
+      double gv[U8], ov[U8];
+#pragma unroll
+      for (int u = 0; u < U8; ++u) {
+        const int j = j1 - u;
+        const size_t o = (size_t)(j >= 0 ? j : 0) * n + i;
+        gv[u] = j >= 0 ? tgt[o] : 0.0;
+        ov[u] = (CHECK && j >= 0) ? yold[o] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U8; ++u) {
+        const int j = j1 - u;
+        if (j < 0) break;
+        const size_t o = (size_t)j * n + i;
+        if (j < m - 1) s = lam * (s + T[(size_t)(j + 1) * (n + 1) + i]);
+        const double kx = Rs[o] + s;
+        const double out = gv[u] / kx;
+        if (CHECK) acc += fabs(ov[u] * kx - gv[u]);
+        bad |= !isfinite(out);
+        y[o] = out;
+      }
+    }
+  }
+}
+
 __device__ __forceinline__ double block_sum(double v, double* red) {
   v = warp_sum(v);
   __syncthreads();
@@ -235,9 +316,45 @@ __global__ void __launch_bounds__(512) fs1_sep2d64_kernel(const __grid_constant_
     const bool use_tol = P.tol > 0.0;
     int it = 0, flag = 0;
     double errv = NAN;
+    extern __shared__ double sst[];
+    const bool staged = nax == 2 && P.staged;
+    double* sT = sst;                                      // [(n + 1) m]
+    double* sR = sst + (size_t)(P.n + 1) * P.m;             // [n m]: the axis-2 staging
     while (true) {
       const bool check = (it >= P.itr_max) || (use_tol && (it % P.check_interval) == 0);
       bad = 0;
+      if (staged) {
+        // lines 2-7 and 8-12 with the intermediate in shared memory
+        col_pass_s(U, sT, P.n, P.m, P.lam1);
+        __syncthreads();
+        if (check) {
+          double e = 0.0;
+          row_pass_s<true>(sT, sR, b, V, Y, P.n, P.m, P.lam2, e, bad);
+          errv = block_sum(e, red);
+          if (it >= P.itr_max || errv <= P.tol) {
+            flag = (use_tol && errv <= P.tol) ? FLAG_CONVERGED : FLAG_ITR_MAX;
+            break;
+          }
+          for (size_t k = threadIdx.x; k < nm; k += blockDim.x) V[k] = Y[k];
+        } else {
+          double e = 0.0;
+          row_pass_s<false>(sT, sR, b, nullptr, V, P.n, P.m, P.lam2, e, bad);
+        }
+        __syncthreads();
+        col_pass_s(V, sT, P.n, P.m, P.lam1);
+        __syncthreads();
+        {
+          double e = 0.0;
+          row_pass_s<false>(sT, sR, a, nullptr, U, P.n, P.m, P.lam2, e, bad);
+        }
+        ++it;
+        if (__syncthreads_or(bad)) {
+          flag = FLAG_NONFINITE;
+          errv = NAN;
+          break;
+        }
+        continue;
+      }
       // lines 2-7: psi = b ./ (K phi)  (K symmetric: K^T phi = K phi)
       if (check) {
         double e = 0.0;
@@ -279,8 +396,16 @@ __global__ void __launch_bounds__(512) fs1_sep2d64_kernel(const __grid_constant_
 
 }  // namespace s64
 
+size_t sep2d64_smem(long long n, long long m, int ndim) {
+  if (ndim != 2 || (n + 1) * m > s64::SMEM_NM) return 0;
+  return (size_t)((n + 1) * m + n * m) * sizeof(double);
+}
+
+const void* sep2d64_fn() { return (const void*)&s64::fs1_sep2d64_kernel; }
+
 cudaError_t launch_sep2d64(const Sep2d64Params& P, long long batch, int threads, cudaStream_t st) {
-  s64::fs1_sep2d64_kernel<<<(unsigned)batch, threads, 0, st>>>(P);
+  const size_t smem = P.staged ? sep2d64_smem(P.n, P.m, P.l > 1 ? 3 : 2) : 0;
+  s64::fs1_sep2d64_kernel<<<(unsigned)batch, threads, smem, st>>>(P);
   return cudaGetLastError();
 }
 
