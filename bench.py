@@ -208,7 +208,8 @@ def profile_traffic(cfg_name):
 # ----------------------------------------------------------------------------- oracle legs
 def oracle_sample(cfg, pairs, iters, n=None):
     """Time the oracle (as it stands) on a bounded sample; returns (updates, seconds).
-    ``n`` shrinks the grid (same recipe) for untimed warm-up calls."""
+    ``n`` shrinks the grid (same recipe): the large single problems' samples and the
+    untimed warm-up calls."""
     from oracle import sinkhorn
     if n is not None:
         cfg = dataclasses.replace(cfg, n=n, m=(n if cfg.ndim == 2 else 1))
@@ -219,8 +220,8 @@ def oracle_sample(cfg, pairs, iters, n=None):
         from oracle import stabilized
         for p in range(len(pairs)):
             stabilized.solve_stab(A64[p], B64[p], n=cfg.n, h=cfg.h1, eps=cfg.eps, itr_max=iters)
-    elif cfg.ndim == 1 and cfg.n <= 8192:
-        sinkhorn.solve(A64, B64, n=cfg.n, h1=cfg.h1, eps=cfg.eps, itr_max=iters,
+    elif cfg.domain == "scaling" or (cfg.ndim == 1 and cfg.n <= 8192):
+        sinkhorn.solve(A64, B64, n=cfg.n, m=cfg.m, h1=cfg.h1, h2=cfg.h2, eps=cfg.eps, itr_max=iters,
                        domain="scaling", input_is_log=cfg.input_is_log)
     else:
         sinkhorn.solve(A64, B64, n=cfg.n, m=cfg.m, h1=cfg.h1, h2=cfg.h2, eps=cfg.eps, itr_max=iters,
@@ -238,21 +239,31 @@ def oracle_cores():
 
 
 def sample_plan(cfg):
-    """Bounded oracle sample (about 10-30 s of CPU work) for the config (C3: one
-    iteration of the plain-C LSE recursion over all 2^24 points, ~7 s)."""
+    """Bounded oracle sample (seconds of CPU work) for the config: (pairs, iterations,
+    grid size or None for the config's, description).  The large single problems run the
+    same recipe on a shorter grid (the oracle's cost per update does not depend on N)."""
     if cfg.name == "c2":
-        return list(range(256)), cfg.itr_max, "256 of 4096 pairs, all 500 iterations, dense fp64 (BLAS)"
+        return list(range(256)), cfg.itr_max, None, "256 of 4096 pairs, all 500 iterations, dense fp64 (BLAS)"
     if cfg.name == "c5":
-        return list(range(8)), 200, "8 pairs, 200 of 1000 iterations, dense fp64 (BLAS)"
+        return list(range(8)), 200, None, "8 pairs, 200 of 1000 iterations, dense fp64 (BLAS)"
     if cfg.name == "c1":
-        return [0], 700, "1 pair, 700 iterations, dense fp64"
+        return [0], 700, None, "1 pair, 700 iterations, dense fp64"
+    if cfg.name == "c3":
+        return [0], 1, 1 << 21, ("1 pair of C3's recipe on 2^21 of its 2^24 points, 1 of 1000 iterations + exit "
+                                 "check + cost, plain-C LSE recursion (x87)")
+    if cfg.name == "c4":
+        return [0], 2, 512, "1 pair of C4's recipe on 512^2 of its 2048^2 points, 2 of 300 iterations, plain-C LSE"
     if cfg.name.startswith("e2s_"):
         it = {500: 2000, 2000: 1000, 8000: 300}.get(cfg.n, 100)
-        return [0], it, f"1 of 100 pairs, {it} of {cfg.itr_max} iterations, the stabilised oracle (plain C recursions)"
+        return [0], it, None, (f"1 of 100 pairs, {it} of {cfg.itr_max} iterations, the stabilised oracle "
+                               "(plain C recursions)")
     if cfg.name.startswith(("e1_", "e2_")):
         it = {500: 500, 2000: 50, 8000: 20}.get(cfg.n, 20)
-        return [0], it, f"1 of 100 pairs, {it} of {cfg.itr_max} iterations, dense fp64"
-    return [0], 1, "1 pair, 1 iteration, plain-C LSE recursion"
+        return [0], it, None, f"1 of 100 pairs, {it} of {cfg.itr_max} iterations, dense fp64"
+    if cfg.name.startswith("e3_"):
+        it = {10: 1000, 20: 1000, 40: 300, 80: 100, 160: 30}.get(cfg.n, 30)
+        return [0], it, None, f"1 of 100 trials, {it} of {cfg.itr_max} iterations, dense fp64 per axis"
+    return [0], 1, None, "1 pair, 1 iteration, plain-C LSE recursion"
 
 
 def host_threads():
@@ -270,7 +281,7 @@ def run_reference(args, cfg):
     if rank != 0:
         return
     _limits = host_threads()  # noqa: F841 (kept alive for the run)
-    pairs, iters, what = sample_plan(cfg)
+    pairs, iters, sn, what = sample_plan(cfg)
     # warm-up steps: the same oracle on a short prefix of the workload (builds the C
     # oracle, starts the BLAS / OpenMP threads); the large configs' full sample would
     # cost seconds per untimed step
@@ -279,7 +290,7 @@ def run_reference(args, cfg):
     times = []
     ups = 0
     for _ in range(args.steps):
-        u, t = oracle_sample(cfg, pairs, iters)
+        u, t = oracle_sample(cfg, pairs, iters, n=sn)
         ups, times = u, times + [t]
     T = sum(times)
     value = ups * len(times) / T
@@ -453,9 +464,9 @@ def run_fs1(args, cfg):
                                                      kern_avg_s, peaks, src, props)
         line["e2e"] = e2e
         if not args.no_cpu_baseline:
-            pairs, it, what = sample_plan(cfg)
+            pairs, it, sn, what = sample_plan(cfg)
             oracle_sample(cfg, pairs[:1], 1, n=None if cfg.size <= 65536 else 256)   # warm-up
-            u_, t_ = oracle_sample(cfg, pairs, it)
+            u_, t_ = oracle_sample(cfg, pairs, it, n=sn)
             line["cpu_baseline"] = {"value": u_ / t_, "unit": UNIT, "cores": oracle_cores(),
                                     "kind": "oracle", "sample": what, "seconds": t_}
         print(json.dumps(line), flush=True)

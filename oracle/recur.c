@@ -118,26 +118,57 @@ void fs1o_sweep_log(const double* X, long n, long stride, long lines, long lstri
   }
 }
 
+/* The weighted sweeps of one line: (p, P') forward and (t, Q') backward are independent
+ * of each other; for a single line (config 3's cost) they run on two threads, each
+ * still sequential with unchanged arithmetic. */
+static void wfwd_log(const double* xl, long n, long stride, ld C, ld* p, ld* P) {
+  p[0] = xl[0];
+  for (long i = 1; i < n; ++i) p[i] = lae(p[i - 1] - C, (ld)xl[i * stride]);
+  P[0] = -INFINITY;
+  for (long i = 1; i < n; ++i) P[i] = -C + lae(P[i - 1], p[i - 1]);
+}
+
+static void wbwd_log(const double* xl, long n, long stride, ld C, ld* t, ld* Q) {
+  t[n - 1] = xl[(n - 1) * stride];
+  for (long i = n - 2; i >= 0; --i) t[i] = lae(t[i + 1] - C, (ld)xl[i * stride]);
+  Q[n - 1] = -INFINITY;
+  for (long i = n - 2; i >= 0; --i) Q[i] = -C + lae(Q[i + 1], t[i + 1]);
+}
+
 void fs1o_wsweep_log(const double* X, long n, long stride, long lines, long lstride,
                      double c, double h, double* Y) {
-#pragma omp parallel for schedule(static)
-  for (long l = 0; l < lines; ++l) {
-    const double* xl = X + l * lstride;
-    double* yl = Y + l * lstride;
+  const ld C = (ld)c;
+  const ld lh = logl((ld)h);
+  if (lines == 1) {
     ld* p = (ld*)malloc(sizeof(ld) * n);   /* log inclusive forward sums  */
     ld* t = (ld*)malloc(sizeof(ld) * n);   /* log inclusive backward sums */
     ld* P = (ld*)malloc(sizeof(ld) * n);   /* log P'                       */
     ld* Q = (ld*)malloc(sizeof(ld) * n);   /* log Q'                       */
-    const ld C = (ld)c;
-    p[0] = xl[0];
-    for (long i = 1; i < n; ++i) p[i] = lae(p[i - 1] - C, (ld)xl[i * stride]);
-    t[n - 1] = xl[(n - 1) * stride];
-    for (long i = n - 2; i >= 0; --i) t[i] = lae(t[i + 1] - C, (ld)xl[i * stride]);
-    P[0] = -INFINITY;
-    for (long i = 1; i < n; ++i) P[i] = -C + lae(P[i - 1], p[i - 1]);
-    Q[n - 1] = -INFINITY;
-    for (long i = n - 2; i >= 0; --i) Q[i] = -C + lae(Q[i + 1], t[i + 1]);
-    ld lh = logl((ld)h);
+#pragma omp parallel sections num_threads(2)
+    {
+#pragma omp section
+      wfwd_log(X, n, stride, C, p, P);
+#pragma omp section
+      wbwd_log(X, n, stride, C, t, Q);
+    }
+#pragma omp parallel for schedule(static)
+    for (long i = 0; i < n; ++i) Y[i * stride] = (double)(lh + lae(P[i], Q[i]));
+    free(p);
+    free(t);
+    free(P);
+    free(Q);
+    return;
+  }
+#pragma omp parallel for schedule(static)
+  for (long l = 0; l < lines; ++l) {
+    const double* xl = X + l * lstride;
+    double* yl = Y + l * lstride;
+    ld* p = (ld*)malloc(sizeof(ld) * n);
+    ld* t = (ld*)malloc(sizeof(ld) * n);
+    ld* P = (ld*)malloc(sizeof(ld) * n);
+    ld* Q = (ld*)malloc(sizeof(ld) * n);
+    wfwd_log(xl, n, stride, C, p, P);
+    wbwd_log(xl, n, stride, C, t, Q);
     for (long i = 0; i < n; ++i) yl[i * stride] = (double)(lh + lae(P[i], Q[i]));
     free(p);
     free(t);
