@@ -436,6 +436,7 @@ __device__ __forceinline__ void block_tile_scan(Ctx& c, double* Fm, int* Fe, dou
   if (lane < c.NW) { xF = wF[lane]; xsF = wFs[lane]; xG = wG[lane]; xsG = wGs[lane]; }
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
+    if (d >= c.NW) break;
     const double uf = __shfl_up_sync(FULL, xF, d);
     const int us = __shfl_up_sync(FULL, xsF, d);
     const double dg = __shfl_down_sync(FULL, xG, d);
