@@ -488,6 +488,21 @@ static fs1_status plan_impl(const fs1_desc* desc, int device, int force, fs1_pla
     const long long lines = d.ndim == 3 ? std::max<long long>(std::max<long long>(d.m * L3, d.n * L3), d.n * d.m)
                                         : std::max<long long>(d.n, d.m);
     p->threads = (int)std::min<long long>(512, ((lines + 31) / 32) * 32);
+    // 2D problems whose lines fit one warp (32 E points, E <= 8): K5w, one warp per line
+    // with a chunked scan (test-only kind 5 keeps the thread-per-line kernel)
+    const int wE = d.ndim == 2 && force != 5 ? sep2d64w_chunk(d.n, d.m) : 0;
+    if (wE) {
+      D.wE = wE;
+      const long double cc[2] = {(long double)d.h1 / (long double)d.eps, (long double)d.h2 / (long double)d.eps};
+      for (int k = 0; k < 5; ++k) {
+        const long double L = (long double)wE * (long double)(1 << k);
+        const long double La = ceill(L / 2), Lb = floorl(L / 2);
+        D.wA1[k] = (double)expl(-cc[0] * La);
+        D.wB1[k] = (double)expl(-cc[0] * Lb);
+        D.wA2[k] = (double)expl(-cc[1] * La);
+        D.wB2[k] = (double)expl(-cc[1] * Lb);
+      }
+    }
     // small 2D problems: the intermediate in shared memory (fs1_sep2d64.cu)
     const size_t ssm = sep2d64_smem(d.n, d.m, d.ndim);
     if (ssm) {
@@ -502,7 +517,8 @@ static fs1_status plan_impl(const fs1_desc* desc, int device, int force, fs1_pla
     }
     p->ws = al256((size_t)d.batch * 3 * (size_t)d.n * (size_t)d.m * (size_t)L3 * 8);
     p->smem = 0;
-    snprintf(p->info.kernel, sizeof(p->info.kernel), d.ndim == 3 ? "sep3d64_f64_scaling" : "sep2d64_f64_scaling");
+    if (wE) snprintf(p->info.kernel, sizeof(p->info.kernel), "sep2d64w_f64_scaling_E%d", wE);
+    else snprintf(p->info.kernel, sizeof(p->info.kernel), d.ndim == 3 ? "sep3d64_f64_scaling" : "sep2d64_f64_scaling");
     p->info.chunk = 1;
     p->info.threads = p->threads;
     p->info.ctas_per_problem = 1;
@@ -619,7 +635,8 @@ fs1_status fs1_plan(const fs1_desc* desc, int device, fs1_plan_t** out, size_t* 
 
 // test-only (not in include/fs1.h): plan with a forced kernel family so the parity
 // tests reach every kernel at small sizes and the benchmarks can compare
-// instantiations.  kind: 1 persistent (K1); 2 streaming (K2); 10 + i streaming
+// instantiations.  kind: 1 persistent (K1); 2 streaming (K2); 5 the 2D fp64 kernel K5
+// with a thread per line (not its warp-per-line variant K5w); 10 + i streaming
 // instantiation i; 3 2D CTA-line kernel (K3); 20 + i 2D warp-line instantiation i
 // (K3w); 30 + W persistent with W warps per CTA; 100 + E persistent with chunk E.
 fs1_status fs1__plan_kind(const fs1_desc* desc, int device, int kind, fs1_plan_t** out,
@@ -670,8 +687,9 @@ fs1_status fs1_solve(const fs1_plan_t* plan, const void* a, const void* b, void*
     P.iters = iters; P.err = err; P.flags = flags; P.cost = cost;
     P.ws = (double*)workspace;
     P.mode = 0;
-    return launch_sep2d64(P, plan->d.batch, plan->threads, (cudaStream_t)stream) == cudaSuccess ? FS1_OK
-                                                                                            : FS1_ERR_CUDA;
+    const cudaError_t e = P.wE ? launch_sep2d64w(P, plan->d.batch, P.wE, (cudaStream_t)stream)
+                               : launch_sep2d64(P, plan->d.batch, plan->threads, (cudaStream_t)stream);
+    return e == cudaSuccess ? FS1_OK : FS1_ERR_CUDA;
   }
   if (plan->kind == KIND_STAB) {
     StabParams P = plan->kbase;

@@ -207,6 +207,8 @@ struct Sep2d64Params {
   int itr_max, check_interval, warm;
   int mode;          // 0 solve, 1 cost, 2 apply
   int staged;        // 2D with n m <= SMEM_NM: the intermediate lives in shared memory
+  int wE;            // > 0: the warp-per-line variant K5w with chunk E (2D, max(n, m) <= 32 E)
+  double wA1[5], wB1[5], wA2[5], wB2[5];  // K5w: lambda^{E 2^k} per axis as two factors
 };
 
 }  // namespace fs1

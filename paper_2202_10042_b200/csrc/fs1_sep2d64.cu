@@ -394,7 +394,212 @@ __global__ void __launch_bounds__(512) fs1_sep2d64_kernel(const __grid_constant_
   if (threadIdx.x == 0) P.cost[pb] = cost;
 }
 
+// ---------------------------------------------------------------------------------
+// K5w: the same 2D solve with ONE WARP per line: lane l owns the E contiguous points
+// [l E, l E + E) of a line of up to 32 E, the line apply is a chunked scan (lane Horner
+// aggregates, a 5-level warp scan of the affine maps y -> lambda^L y + c, both recursions
+// from the exact carries) instead of one thread walking the whole line.  The scan
+// multipliers lambda^{E 2^k} are formed on the host as two factors (each >= sqrt of
+// the power) so that an underflow of the power alone cannot zero a carry that is still
+// representable (Remark 3.3; lambda = e^{-100} at E3).  The axis-1
+// result goes through the workspace (L1/L2); the axis-2 pass is fused with the update.
+
+template <int E>
+__device__ __forceinline__ void warp_line_apply(const double (&x)[E], double (&y)[E], double lam,
+                                                const double* lvA, const double* lvB, int lane) {
+  double f = 0.0, g = 0.0;
+#pragma unroll
+  for (int e = 0; e < E; ++e) f = fma(lam, f, x[e]);           // forward value at the chunk end
+#pragma unroll
+  for (int e = E - 1; e >= 0; --e) g = fma(lam, g, x[e]);      // backward value at the chunk start
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    const int d = 1 << k;
+    const double up = __shfl_up_sync(FULL, f, d), dn = __shfl_down_sync(FULL, g, d);
+    if (lane >= d) f = fma(up * lvA[k], lvB[k], f);
+    if (lane + d < 32) g = fma(dn * lvA[k], lvB[k], g);
+  }
+  double cf = __shfl_up_sync(FULL, f, 1), cb = __shfl_down_sync(FULL, g, 1);
+  if (lane == 0) cf = 0.0;
+  if (lane == 31) cb = 0.0;
+  // forward recursion r_k = lam r_{k-1} + x_k from the exact carry
+  double p = cf;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    p = fma(lam, p, x[e]);
+    y[e] = p;
+  }
+  // backward: t_k = x_k + lam t_{k+1} (inclusive), K x = r_k + lam t_{k+1}
+  double t = cb;
+#pragma unroll
+  for (int e = E - 1; e >= 0; --e) {
+    const double kx = fma(lam, t, y[e]);
+    t = fma(lam, t, x[e]);
+    y[e] = kx;
+  }
+}
+
+// axis 1: T = K1 x on every column (warp per column); the next column's loads are in
+// flight while this one is scanned
+template <int E>
+__device__ __forceinline__ void colw(const double* __restrict__ x, double* __restrict__ T, int n, int m,
+                                     const Sep2d64Params& P, int warp, int nw, int lane) {
+  double v[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int k = lane * E + e;
+    v[e] = (warp < m && k < n) ? x[(size_t)warp * n + k] : 0.0;
+  }
+  for (int j = warp; j < m; j += nw) {
+    double nv[E], y[E];
+    const int jn = j + nw;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int k = lane * E + e;
+      nv[e] = (jn < m && k < n) ? x[(size_t)jn * n + k] : 0.0;
+    }
+    warp_line_apply<E>(v, y, P.lam1, P.wA1, P.wB1, lane);
+    double* tc = T + (size_t)j * n;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int k = lane * E + e;
+      if (k < n) tc[k] = y[e];
+      v[e] = nv[e];
+    }
+  }
+}
+
+// axis 2 fused with the update: y = tgt / (K2 T) on every row (warp per row); CHECK: the
+// marginal error against yold.  The row's targets (and old values) are loaded with the row
+// itself and the next row's T is in flight during the scan: the loads are strided (a row
+// is not contiguous), so their latency, not their bytes, is what this pass waits on.
+template <int E, bool CHECK>
+__device__ __forceinline__ void roww(const double* __restrict__ T, const double* __restrict__ tgt,
+                                     const double* __restrict__ yold, double* __restrict__ y, int n, int m,
+                                     const Sep2d64Params& P, int warp, int nw, int lane, double& acc, int& bad) {
+  double v[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int j = lane * E + e;
+    v[e] = (warp < n && j < m) ? T[(size_t)j * n + warp] : 0.0;
+  }
+  for (int i = warp; i < n; i += nw) {
+    double tg[E], yo[E], nv[E], k2[E];
+    const int in = i + nw;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int j = lane * E + e;
+      const size_t o = (size_t)j * n + i;
+      tg[e] = j < m ? tgt[o] : 1.0;
+      if (CHECK) yo[e] = j < m ? yold[o] : 0.0;
+      nv[e] = (in < n && j < m) ? T[(size_t)j * n + in] : 0.0;
+    }
+    warp_line_apply<E>(v, k2, P.lam2, P.wA2, P.wB2, lane);
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int j = lane * E + e;
+      if (j < m) {
+        const size_t o = (size_t)j * n + i;
+        const double out = tg[e] / k2[e];
+        if (CHECK) acc += fabs(yo[e] * k2[e] - tg[e]);
+        bad |= !isfinite(out);
+        y[o] = out;
+      }
+      v[e] = nv[e];
+    }
+  }
+}
+
+template <int E>
+__global__ void __launch_bounds__(512) fs1_sep2d64w_kernel(const __grid_constant__ Sep2d64Params P) {
+  __shared__ double red[32];
+  const int n = P.n, m = P.m;
+  const size_t nm = (size_t)n * m;
+  const long long pb = blockIdx.x;
+  double* T = P.ws + (size_t)pb * 3 * nm;
+  double* Y = T + 2 * nm;
+  const double* a = P.a + pb * nm;
+  const double* b = P.b + pb * nm;
+  double* U = P.u + pb * nm;
+  double* V = P.v + pb * nm;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (!P.warm) {
+    const double init = 1.0 / (double)nm;
+    for (size_t k = threadIdx.x; k < nm; k += blockDim.x) {
+      U[k] = init;
+      V[k] = init;
+    }
+  }
+  __syncthreads();
+  const bool use_tol = P.tol > 0.0;
+  int it = 0, flag = 0, bad = 0;
+  double errv = NAN;
+  while (true) {
+    const bool check = (it >= P.itr_max) || (use_tol && (it % P.check_interval) == 0);
+    bad = 0;
+    colw<E>(U, T, n, m, P, warp, nw, lane);                      // lines 3-6: K phi, axis 1
+    __syncthreads();
+    if (check) {
+      double e = 0.0;
+      roww<E, true>(T, b, V, Y, n, m, P, warp, nw, lane, e, bad);  // axis 2 + line 7 + line 2
+      errv = block_sum(e, red);
+      if (it >= P.itr_max || errv <= P.tol) {
+        flag = (use_tol && errv <= P.tol) ? FLAG_CONVERGED : FLAG_ITR_MAX;
+        break;
+      }
+      for (size_t k = threadIdx.x; k < nm; k += blockDim.x) V[k] = Y[k];
+    } else {
+      double e = 0.0;
+      roww<E, false>(T, b, nullptr, V, n, m, P, warp, nw, lane, e, bad);
+    }
+    __syncthreads();
+    colw<E>(V, T, n, m, P, warp, nw, lane);                      // lines 8-11
+    __syncthreads();
+    {
+      double e = 0.0;
+      roww<E, false>(T, a, nullptr, U, n, m, P, warp, nw, lane, e, bad);  // line 12
+    }
+    ++it;  // line 13
+    if (__syncthreads_or(bad)) {
+      flag = FLAG_NONFINITE;
+      errv = NAN;
+      break;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (P.iters) P.iters[pb] = it;
+    if (P.err) P.err[pb] = errv;
+    if (P.flags) P.flags[pb] = flag;
+  }
+  if (flag == FLAG_NONFINITE) {
+    if (threadIdx.x == 0 && P.cost) P.cost[pb] = NAN;
+    return;
+  }
+  if (!P.cost) return;
+  const Geo g{P.n, P.m, 1};
+  const double cost = cost_all(g, 2, P, U, V, T, T + nm, red);
+  if (threadIdx.x == 0) P.cost[pb] = cost;
+}
+
 }  // namespace s64
+
+int sep2d64w_chunk(long long n, long long m) {
+  const long long L = n > m ? n : m;
+  for (int E : {2, 4, 8})
+    if (32LL * E >= L) return E;
+  return 0;
+}
+
+cudaError_t launch_sep2d64w(const Sep2d64Params& P, long long batch, int E, cudaStream_t st) {
+  switch (E) {
+    case 2: s64::fs1_sep2d64w_kernel<2><<<(unsigned)batch, 512, 0, st>>>(P); break;
+    case 4: s64::fs1_sep2d64w_kernel<4><<<(unsigned)batch, 512, 0, st>>>(P); break;
+    case 8: s64::fs1_sep2d64w_kernel<8><<<(unsigned)batch, 512, 0, st>>>(P); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
 
 size_t sep2d64_smem(long long n, long long m, int ndim) {
   if (ndim != 2 || (n + 1) * m > s64::SMEM_NM) return 0;

@@ -92,3 +92,23 @@ def test_ragged_shapes(shape):
     out = fs1.solve(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), **kw)
     ref = sinkhorn.solve(A, B, n=n, m=m, h1=1.0 / n, h2=1.0 / m, eps=0.03, itr_max=60)
     assert_solve_parity(out, ref, "scaling", "f64")
+
+
+@pytest.mark.parametrize("shape", [(10, 10), (33, 64), (160, 160), (64, 200), (1, 256), (256, 3)])
+def test_warp_line_variant_equals_thread_line_kernel(shape):
+    """K5w (one warp per line, chunked scan with two-factor multipliers) against K5's
+    sequential thread-per-line recursion (test-only kind 5) and the oracle, at E3's
+    lambda = e^{-100} and at a moderate lambda."""
+    n, m = shape
+    rng = np.random.default_rng(n + 7 * m)
+    A, B = gi.random_positive(rng, (2, n * m)), gi.random_positive(rng, (2, n * m))
+    for h, eps, itr in ((1.0, 0.01, 200), (1.0 / max(n, m), 0.05, 60)):
+        kw = dict(h=h, h2=h, shape=(n, m), eps=eps, itr_max=itr, domain="scaling")
+        w = fs1.solve(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), **kw)
+        t = fs1.solve(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), kernel=5, **kw)
+        ref = sinkhorn.solve(A, B, n=n, m=m, h1=h, h2=h, eps=eps, itr_max=itr)
+        assert_solve_parity(w, ref, "scaling", "f64")
+        assert_solve_parity(t, ref, "scaling", "f64")
+    info = fs1.plan(fs1.Spec(ndim=2, n=n, m=m, h1=h, h2=h, eps=eps, batch=2, dtype=torch.float64,
+                             itr_max=itr)).info()
+    assert info["kernel"].startswith("sep2d64w")
