@@ -515,7 +515,7 @@ static fs1_status plan_impl(const fs1_desc* desc, int device, int force, fs1_pla
       if (e != cudaSuccess) { delete p; return FS1_ERR_CUDA; }
       D.staged = 1;
     }
-    p->ws = al256((size_t)d.batch * 3 * (size_t)d.n * (size_t)d.m * (size_t)L3 * 8);
+    p->ws = al256((size_t)d.batch * (wE ? 5 : 3) * (size_t)d.n * (size_t)d.m * (size_t)L3 * 8);
     p->smem = 0;
     if (wE) snprintf(p->info.kernel, sizeof(p->info.kernel), "sep2d64w_f64_scaling_E%d", wE);
     else snprintf(p->info.kernel, sizeof(p->info.kernel), d.ndim == 3 ? "sep3d64_f64_scaling" : "sep2d64_f64_scaling");

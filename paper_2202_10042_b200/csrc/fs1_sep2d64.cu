@@ -439,73 +439,64 @@ __device__ __forceinline__ void warp_line_apply(const double (&x)[E], double (&y
   }
 }
 
-// axis 1: T = K1 x on every column (warp per column); the next column's loads are in
-// flight while this one is scanned
+// A line of length len at base + k * stride (k = 0..len-1), lane l holding k = l E + e;
+// zero beyond the end (a zero tail leaves both recursions of the line unchanged).
 template <int E>
-__device__ __forceinline__ void colw(const double* __restrict__ x, double* __restrict__ T, int n, int m,
-                                     const Sep2d64Params& P, int warp, int nw, int lane) {
-  double v[E];
+__device__ __forceinline__ void load_line(double (&x)[E], const double* __restrict__ base, int len, size_t stride,
+                                          int lane, bool valid) {
 #pragma unroll
   for (int e = 0; e < E; ++e) {
     const int k = lane * E + e;
-    v[e] = (warp < m && k < n) ? x[(size_t)warp * n + k] : 0.0;
-  }
-  for (int j = warp; j < m; j += nw) {
-    double nv[E], y[E];
-    const int jn = j + nw;
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-      const int k = lane * E + e;
-      nv[e] = (jn < m && k < n) ? x[(size_t)jn * n + k] : 0.0;
-    }
-    warp_line_apply<E>(v, y, P.lam1, P.wA1, P.wB1, lane);
-    double* tc = T + (size_t)j * n;
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-      const int k = lane * E + e;
-      if (k < n) tc[k] = y[e];
-      v[e] = nv[e];
-    }
+    x[e] = (valid && k < len) ? base[(size_t)k * stride] : 0.0;
   }
 }
 
-// axis 2 fused with the update: y = tgt / (K2 T) on every row (warp per row); CHECK: the
-// marginal error against yold.  The row's targets (and old values) are loaded with the row
-// itself and the next row's T is in flight during the scan: the loads are strided (a row
-// is not contiguous), so their latency, not their bytes, is what this pass waits on.
+// One half of Algorithm 2 on lines of one axis, fused with the first axis of the next
+// half (K = K1 (x) K2 is separable and the two axes commute):
+//   K_this z   = lam-recursions of the line Tin (Tin already holds K_other of the other
+//                potential),
+//   y_new      = tgt / K z                              (line 7 / line 12),
+//   Tout line  = K_this y_new                           (the next half's first axis),
+//   CHECK:     acc += |y_old * K z - tgt|               (line 2's marginal error).
+// Every line read (Tin, tgt, y_old) and the potential written are contiguous in the
+// layout of this axis; Tout is written transposed (strided stores, no wait), which is
+// what makes the next half's reads contiguous.  The next line's Tin loads are in flight
+// while this line is scanned.
 template <int E, bool CHECK>
-__device__ __forceinline__ void roww(const double* __restrict__ T, const double* __restrict__ tgt,
-                                     const double* __restrict__ yold, double* __restrict__ y, int n, int m,
-                                     const Sep2d64Params& P, int warp, int nw, int lane, double& acc, int& bad) {
+__device__ __forceinline__ void half_pass(const double* __restrict__ Tin, const double* __restrict__ tgt,
+                                          const double* __restrict__ yold, double* __restrict__ ynew,
+                                          double* __restrict__ Tout, int len, int count, double lam,
+                                          const double* lvA, const double* lvB, int warp, int nw, int lane,
+                                          double& acc, int& bad) {
   double v[E];
+  load_line<E>(v, Tin + (size_t)warp * len, len, 1, lane, warp < count);
+  for (int r = warp; r < count; r += nw) {
+    const size_t base = (size_t)r * len;
+    double tg[E], nv[E], kz[E];
+    load_line<E>(tg, tgt + base, len, 1, lane, true);
+    load_line<E>(nv, Tin + base + (size_t)nw * len, len, 1, lane, r + nw < count);
+    warp_line_apply<E>(v, kz, lam, lvA, lvB, lane);
+    if (CHECK) {
+      double yo[E];
+      load_line<E>(yo, yold + base, len, 1, lane, true);
 #pragma unroll
-  for (int e = 0; e < E; ++e) {
-    const int j = lane * E + e;
-    v[e] = (warp < n && j < m) ? T[(size_t)j * n + warp] : 0.0;
-  }
-  for (int i = warp; i < n; i += nw) {
-    double tg[E], yo[E], nv[E], k2[E];
-    const int in = i + nw;
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-      const int j = lane * E + e;
-      const size_t o = (size_t)j * n + i;
-      tg[e] = j < m ? tgt[o] : 1.0;
-      if (CHECK) yo[e] = j < m ? yold[o] : 0.0;
-      nv[e] = (in < n && j < m) ? T[(size_t)j * n + in] : 0.0;
+      for (int e = 0; e < E; ++e)
+        if (lane * E + e < len) acc += fabs(yo[e] * kz[e] - tg[e]);
     }
-    warp_line_apply<E>(v, k2, P.lam2, P.wA2, P.wB2, lane);
 #pragma unroll
     for (int e = 0; e < E; ++e) {
-      const int j = lane * E + e;
-      if (j < m) {
-        const size_t o = (size_t)j * n + i;
-        const double out = tg[e] / k2[e];
-        if (CHECK) acc += fabs(yo[e] * k2[e] - tg[e]);
-        bad |= !isfinite(out);
-        y[o] = out;
-      }
+      const int k = lane * E + e;
+      const double out = k < len ? tg[e] / kz[e] : 0.0;
+      bad |= !isfinite(out);
+      if (k < len) ynew[base + k] = out;
+      tg[e] = out;
       v[e] = nv[e];
+    }
+    warp_line_apply<E>(tg, kz, lam, lvA, lvB, lane);
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int k = lane * E + e;
+      if (k < len) Tout[(size_t)k * count + r] = kz[e];
     }
   }
 }
@@ -516,18 +507,36 @@ __global__ void __launch_bounds__(512) fs1_sep2d64w_kernel(const __grid_constant
   const int n = P.n, m = P.m;
   const size_t nm = (size_t)n * m;
   const long long pb = blockIdx.x;
-  double* T = P.ws + (size_t)pb * 3 * nm;
-  double* Y = T + 2 * nm;
+  // workspace (5 n m per problem): TR and TC, the intermediates in row layout (axis 2
+  // contiguous, [i m + j]) and column layout (axis 1 contiguous, [j n + i], the layout of
+  // u, v, a, b); psi in row layout, ping-pong; b in row layout
+  double* TR = P.ws + (size_t)pb * 5 * nm;
+  double* TC = TR + nm;
+  double* Vc = TC + nm;      // psi of the last completed iteration
+  double* Vn = TC + 2 * nm;  // psi being formed
+  double* bR = TC + 3 * nm;
   const double* a = P.a + pb * nm;
   const double* b = P.b + pb * nm;
   double* U = P.u + pb * nm;
   double* V = P.v + pb * nm;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  if (!P.warm) {
-    const double init = 1.0 / (double)nm;
-    for (size_t k = threadIdx.x; k < nm; k += blockDim.x) {
-      U[k] = init;
-      V[k] = init;
+  const double init = 1.0 / (double)nm;
+  for (size_t k = threadIdx.x; k < nm; k += blockDim.x) {
+    const size_t j = k / n, i = k - j * n;  // column layout index k = j n + i
+    if (!P.warm) U[k] = init;
+    Vc[i * m + j] = P.warm ? V[k] : init;
+    bR[i * m + j] = b[k];
+  }
+  __syncthreads();
+  // prologue: TR = K1 phi (axis 1 on the columns of phi, stored transposed)
+  for (int j = warp; j < m; j += nw) {
+    double x[E], y[E];
+    load_line<E>(x, U + (size_t)j * n, n, 1, lane, true);
+    warp_line_apply<E>(x, y, P.lam1, P.wA1, P.wB1, lane);
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int k = lane * E + e;
+      if (k < n) TR[(size_t)k * m + j] = y[e];
     }
   }
   __syncthreads();
@@ -537,27 +546,29 @@ __global__ void __launch_bounds__(512) fs1_sep2d64w_kernel(const __grid_constant
   while (true) {
     const bool check = (it >= P.itr_max) || (use_tol && (it % P.check_interval) == 0);
     bad = 0;
-    colw<E>(U, T, n, m, P, warp, nw, lane);                      // lines 3-6: K phi, axis 1
-    __syncthreads();
+    // lines 2-7 on the rows: psi = b / K2 TR, TC = K2 psi
     if (check) {
       double e = 0.0;
-      roww<E, true>(T, b, V, Y, n, m, P, warp, nw, lane, e, bad);  // axis 2 + line 7 + line 2
+      half_pass<E, true>(TR, bR, Vc, Vn, TC, m, n, P.lam2, P.wA2, P.wB2, warp, nw, lane, e, bad);
       errv = block_sum(e, red);
       if (it >= P.itr_max || errv <= P.tol) {
         flag = (use_tol && errv <= P.tol) ? FLAG_CONVERGED : FLAG_ITR_MAX;
-        break;
+        break;  // psi stays Vc: the result of the last completed iteration
       }
-      for (size_t k = threadIdx.x; k < nm; k += blockDim.x) V[k] = Y[k];
     } else {
       double e = 0.0;
-      roww<E, false>(T, b, nullptr, V, n, m, P, warp, nw, lane, e, bad);
+      half_pass<E, false>(TR, bR, nullptr, Vn, TC, m, n, P.lam2, P.wA2, P.wB2, warp, nw, lane, e, bad);
+    }
+    {
+      double* t = Vc;
+      Vc = Vn;
+      Vn = t;
     }
     __syncthreads();
-    colw<E>(V, T, n, m, P, warp, nw, lane);                      // lines 8-11
-    __syncthreads();
+    // lines 8-12 on the columns: phi = a / K1 TC, TR = K1 phi
     {
       double e = 0.0;
-      roww<E, false>(T, a, nullptr, U, n, m, P, warp, nw, lane, e, bad);  // line 12
+      half_pass<E, false>(TC, a, nullptr, U, TR, n, m, P.lam1, P.wA1, P.wB1, warp, nw, lane, e, bad);
     }
     ++it;  // line 13
     if (__syncthreads_or(bad)) {
@@ -565,6 +576,12 @@ __global__ void __launch_bounds__(512) fs1_sep2d64w_kernel(const __grid_constant
       errv = NAN;
       break;
     }
+  }
+  __syncthreads();
+  // psi back to the column layout of the interface
+  for (size_t k = threadIdx.x; k < nm; k += blockDim.x) {
+    const size_t j = k / n, i = k - j * n;
+    V[k] = Vc[i * m + j];
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -578,7 +595,7 @@ __global__ void __launch_bounds__(512) fs1_sep2d64w_kernel(const __grid_constant
   }
   if (!P.cost) return;
   const Geo g{P.n, P.m, 1};
-  const double cost = cost_all(g, 2, P, U, V, T, T + nm, red);
+  const double cost = cost_all(g, 2, P, U, V, TR, TC, red);
   if (threadIdx.x == 0) P.cost[pb] = cost;
 }
 
