@@ -503,19 +503,22 @@ static fs1_status plan_impl(const fs1_desc* desc, int device, int force, fs1_pla
         D.wB2[k] = (double)expl(-cc[1] * Lb);
       }
     }
-    // small 2D problems: the intermediate in shared memory (fs1_sep2d64.cu)
-    const size_t ssm = sep2d64_smem(d.n, d.m, d.ndim);
-    if (ssm) {
+    // K5w's transposition stage (fs1_sep2d64.cu); else small 2D problems: the
+    // intermediate in shared memory
+    const size_t ssm = wE ? sep2d64w_smem(d.n, d.m, wE) : sep2d64_smem(d.n, d.m, d.ndim);
+    if (ssm > (wE ? 48 * 1024 : 0)) {
       std::lock_guard<std::mutex> lk(g_attr_mu);
       int cur = 0;
       if (cudaGetDevice(&cur) != cudaSuccess) { delete p; return FS1_ERR_CUDA; }
       if (cur != device && cudaSetDevice(device) != cudaSuccess) { delete p; return FS1_ERR_CUDA; }
-      const cudaError_t e = cudaFuncSetAttribute(sep2d64_fn(), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
+      const cudaError_t e = cudaFuncSetAttribute(wE ? sep2d64w_fn(wE) : sep2d64_fn(),
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
       if (cur != device) cudaSetDevice(cur);
       if (e != cudaSuccess) { delete p; return FS1_ERR_CUDA; }
-      D.staged = 1;
+      if (!wE) D.staged = 1;
     }
-    p->ws = al256((size_t)d.batch * (wE ? 5 : 3) * (size_t)d.n * (size_t)d.m * (size_t)L3 * 8);
+    p->ws = al256(wE ? (size_t)d.batch * sep2d64w_workspace(d.n, d.m, wE)
+                     : (size_t)d.batch * 3 * (size_t)d.n * (size_t)d.m * (size_t)L3 * 8);
     p->smem = 0;
     if (wE) snprintf(p->info.kernel, sizeof(p->info.kernel), "sep2d64w_f64_scaling_E%d", wE);
     else snprintf(p->info.kernel, sizeof(p->info.kernel), d.ndim == 3 ? "sep3d64_f64_scaling" : "sep2d64_f64_scaling");

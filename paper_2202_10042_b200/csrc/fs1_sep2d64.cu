@@ -439,109 +439,182 @@ __device__ __forceinline__ void warp_line_apply(const double (&x)[E], double (&y
   }
 }
 
-// A line of length len at base + k * stride (k = 0..len-1), lane l holding k = l E + e;
-// zero beyond the end (a zero tail leaves both recursions of the line unchanged).
+// Internal layouts of K5w (workspace): every line padded to a multiple of PADW doubles
+// (>= E), so that a lane's E points are one aligned 16 / 32-byte vector and a line's
+// loads are a single contiguous, coalesced request.  Row layout: [i ldm + j]
+// (axis 2 contiguous); column layout: [j ldn + i] (axis 1 contiguous, the layout of the
+// interface's u, v, a, b).
+__host__ __device__ constexpr int w_pad(int E) { return E > 4 ? E : 4; }
+__host__ __device__ inline int w_ld(int len, int E) { return (len + w_pad(E) - 1) / w_pad(E) * w_pad(E); }
+// shared-memory stage of one round of transposed line results: NW lines x SP points,
+// SP = w_ld(L) + 2 (holds a lane's whole chunk; even: 16-byte aligned rows; = 2 mod 4:
+// the column-wise readout of NW rows spreads over the banks)
+__host__ __device__ inline int w_sp(int L, int E) { return w_ld(L, E) + 2; }
+
+// lane's chunk of a padded line (ld doubles; only lanes whose chunk starts before ld
+// load), zero at and beyond len
 template <int E>
-__device__ __forceinline__ void load_line(double (&x)[E], const double* __restrict__ base, int len, size_t stride,
-                                          int lane, bool valid) {
+__device__ __forceinline__ void vload_line(double (&x)[E], const double* __restrict__ line, int len, int ld,
+                                           int lane, bool valid) {
+  const int k0 = lane * E;
 #pragma unroll
-  for (int e = 0; e < E; ++e) {
-    const int k = lane * E + e;
-    x[e] = (valid && k < len) ? base[(size_t)k * stride] : 0.0;
+  for (int e = 0; e < E; ++e) x[e] = 0.0;
+  if (valid && k0 < ld) {
+    const double* p = line + k0;
+    if constexpr (E == 2) {
+      asm volatile("ld.global.v2.f64 {%0,%1}, [%2];" : "=d"(x[0]), "=d"(x[1]) : "l"(p));
+    } else {
+#pragma unroll
+      for (int q = 0; q < E / 4; ++q)
+        asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];"
+                     : "=d"(x[4 * q]), "=d"(x[4 * q + 1]), "=d"(x[4 * q + 2]), "=d"(x[4 * q + 3])
+                     : "l"(p + 4 * q));
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < E; ++e)
+    if (k0 + e >= len) x[e] = 0.0;
+}
+
+template <int E>
+__device__ __forceinline__ void vstore_line(double* __restrict__ line, const double (&x)[E], int ld, int lane) {
+  const int k0 = lane * E;
+  if (k0 >= ld) return;
+  double* p = line + k0;
+  if constexpr (E == 2) {
+    asm volatile("st.global.v2.f64 [%0], {%1,%2};" ::"l"(p), "d"(x[0]), "d"(x[1]) : "memory");
+  } else {
+#pragma unroll
+    for (int q = 0; q < E / 4; ++q)
+      asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p + 4 * q), "d"(x[4 * q]), "d"(x[4 * q + 1]),
+                   "d"(x[4 * q + 2]), "d"(x[4 * q + 3])
+                   : "memory");
   }
 }
 
-// One half of Algorithm 2 on lines of one axis, fused with the first axis of the next
-// half (K = K1 (x) K2 is separable and the two axes commute):
-//   K_this z   = lam-recursions of the line Tin (Tin already holds K_other of the other
-//                potential),
-//   y_new      = tgt / K z                              (line 7 / line 12),
-//   Tout line  = K_this y_new                           (the next half's first axis),
-//   CHECK:     acc += |y_old * K z - tgt|               (line 2's marginal error).
-// Every line read (Tin, tgt, y_old) and the potential written are contiguous in the
-// layout of this axis; Tout is written transposed (strided stores, no wait), which is
-// what makes the next half's reads contiguous.  The next line's Tin loads are in flight
-// while this line is scanned.
-template <int E, bool CHECK>
+// line 7 / 12: t / k as a reciprocal estimate, one Newton step and a residual correction
+// (< 1 ulp).  The IEEE '/' takes its slow path whenever any lane's operands leave a
+// narrow exponent window, which E3's potentials (2^-925 .. 2^908 at 160^2) do in every
+// warp; it remains for denominators outside 2^-1000 .. 2^1000 (and zero / non-finite
+// ones), where the estimate's flush to zero would differ.
+__device__ __forceinline__ double upd_div(double t, double k) {
+  const double ak = fabs(k);
+  return (ak > 0x1p-1000 && ak < 0x1p1000) ? Tr<double>::div<true>(t, k) : t / k;
+}
+
+// One half of Algorithm 2 on the `count` lines (length len, padded ld) of one axis,
+// fused with the first axis of the next half (K = K1 (x) K2 is separable and the two
+// axes commute):
+//   kz         = K_this z    (the lambda-recursions of line r of Tin, which already
+//                             holds K_other of the other potential),
+//   y_new      = tgt / kz                               (line 7 / line 12),
+//   Tout       = K_this y_new, transposed                (the next half's first axis),
+//   MODE CHECK: acc += |y_old kz - tgt|                  (line 2's marginal error).
+// MODE PRO (prologue): Tout = K_this Tin, transposed, nothing else.
+// Lines go in rounds of NW (one per warp); a round's Tout lines are staged in shared
+// memory and written out column-wise by the whole CTA (NW consecutive doubles per
+// point: coalesced), one barrier per round with the stage double-buffered.  The next
+// line's Tin loads are in flight while this one is scanned.
+constexpr int W_PRO = 0, W_UPD = 1, W_CHECK = 2;
+
+template <int E, int MODE>
 __device__ __forceinline__ void half_pass(const double* __restrict__ Tin, const double* __restrict__ tgt,
                                           const double* __restrict__ yold, double* __restrict__ ynew,
-                                          double* __restrict__ Tout, int len, int count, double lam,
-                                          const double* lvA, const double* lvB, int warp, int nw, int lane,
-                                          double& acc, int& bad) {
+                                          double* __restrict__ Tout, int len, int ld, int count, int ldo,
+                                          double lam, const double* lvA, const double* lvB, double* stage, int sp,
+                                          int warp, int nw, int lane, double& acc, int& bad) {
   double v[E];
-  load_line<E>(v, Tin + (size_t)warp * len, len, 1, lane, warp < count);
-  for (int r = warp; r < count; r += nw) {
-    const size_t base = (size_t)r * len;
-    double tg[E], nv[E], kz[E];
-    load_line<E>(tg, tgt + base, len, 1, lane, true);
-    load_line<E>(nv, Tin + base + (size_t)nw * len, len, 1, lane, r + nw < count);
-    warp_line_apply<E>(v, kz, lam, lvA, lvB, lane);
-    if (CHECK) {
-      double yo[E];
-      load_line<E>(yo, yold + base, len, 1, lane, true);
+  vload_line<E>(v, Tin + (size_t)warp * ld, len, ld, lane, warp < count);
+  int buf = 0;
+  for (int r0 = 0; r0 < count; r0 += nw, buf ^= 1) {
+    const int r = r0 + warp;
+    double* st = stage + (size_t)buf * nw * sp;
+    if (r < count) {
+      const size_t base = (size_t)r * ld;
+      double nv[E], kz[E];
+      double tg[E];
+      if (MODE != W_PRO) vload_line<E>(tg, tgt + base, len, ld, lane, true);
+      vload_line<E>(nv, Tin + base + (size_t)nw * ld, len, ld, lane, r + nw < count);
+      warp_line_apply<E>(v, kz, lam, lvA, lvB, lane);
+      if (MODE != W_PRO) {
+        if (MODE == W_CHECK) {
+          double yo[E];
+          vload_line<E>(yo, yold + base, len, ld, lane, true);
 #pragma unroll
-      for (int e = 0; e < E; ++e)
-        if (lane * E + e < len) acc += fabs(yo[e] * kz[e] - tg[e]);
+          for (int e = 0; e < E; ++e) acc += fabs(yo[e] * kz[e] - tg[e]);  // zero beyond len
+        }
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const bool live = lane * E + e < len;
+          const double out = live ? upd_div(tg[e], kz[e]) : 0.0;
+          bad |= !isfinite(out);
+          tg[e] = out;
+        }
+        vstore_line<E>(ynew + base, tg, ld, lane);
+        warp_line_apply<E>(tg, kz, lam, lvA, lvB, lane);
+      }
+      // stage row `warp`: this line's Tout values, lane chunk as 16-byte vectors
+      if (lane * E < len) {
+        double2* srow = reinterpret_cast<double2*>(st + (size_t)warp * sp + lane * E);
+#pragma unroll
+        for (int q = 0; q < E / 2; ++q) srow[q] = make_double2(kz[2 * q], kz[2 * q + 1]);
+      }
+#pragma unroll
+      for (int e = 0; e < E; ++e) v[e] = nv[e];
     }
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-      const int k = lane * E + e;
-      const double out = k < len ? tg[e] / kz[e] : 0.0;
-      bad |= !isfinite(out);
-      if (k < len) ynew[base + k] = out;
-      tg[e] = out;
-      v[e] = nv[e];
-    }
-    warp_line_apply<E>(tg, kz, lam, lvA, lvB, lane);
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-      const int k = lane * E + e;
-      if (k < len) Tout[(size_t)k * count + r] = kz[e];
+    __syncthreads();
+    // write-out: Tout[k ldo + r0 + w] = stage[w][k], NW consecutive doubles per point k
+    const int nr = count - r0 < nw ? count - r0 : nw;
+    for (int t = threadIdx.x; t < len * nw; t += blockDim.x) {
+      const int k = t / nw, w = t - k * nw;
+      if (w < nr) Tout[(size_t)k * ldo + r0 + w] = st[(size_t)w * sp + k];
     }
   }
 }
 
-template <int E>
-__global__ void __launch_bounds__(512) fs1_sep2d64w_kernel(const __grid_constant__ Sep2d64Params P) {
+template <int E, int NT>
+__global__ void __launch_bounds__(NT) fs1_sep2d64w_kernel(const __grid_constant__ Sep2d64Params P) {
   __shared__ double red[32];
+  extern __shared__ __align__(16) double stage[];
   const int n = P.n, m = P.m;
+  const int ldn = w_ld(n, E), ldm = w_ld(m, E);
   const size_t nm = (size_t)n * m;
+  const size_t szR = (size_t)n * ldm, szC = (size_t)m * ldn;
   const long long pb = blockIdx.x;
-  // workspace (5 n m per problem): TR and TC, the intermediates in row layout (axis 2
-  // contiguous, [i m + j]) and column layout (axis 1 contiguous, [j n + i], the layout of
-  // u, v, a, b); psi in row layout, ping-pong; b in row layout
-  double* TR = P.ws + (size_t)pb * 5 * nm;
-  double* TC = TR + nm;
-  double* Vc = TC + nm;      // psi of the last completed iteration
-  double* Vn = TC + 2 * nm;  // psi being formed
-  double* bR = TC + 3 * nm;
+  // workspace (4 row-layout + 3 column-layout buffers per problem): TR, TC the
+  // intermediates; psi in row layout (ping-pong: a check iteration that stops keeps
+  // the psi of the last completed iteration); b in row layout; a and phi in column
+  // layout (padded copies of the interface's arrays)
+  double* TR = P.ws + (size_t)pb * (4 * szR + 3 * szC);
+  double* Vc = TR + szR;
+  double* Vn = Vc + szR;
+  double* bR = Vn + szR;
+  double* TC = bR + szR;
+  double* aC = TC + szC;
+  double* UC = aC + szC;
   const double* a = P.a + pb * nm;
   const double* b = P.b + pb * nm;
   double* U = P.u + pb * nm;
   double* V = P.v + pb * nm;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = NT / 32;
+  const int sp = w_sp(n > m ? n : m, E);
   const double init = 1.0 / (double)nm;
-  for (size_t k = threadIdx.x; k < nm; k += blockDim.x) {
-    const size_t j = k / n, i = k - j * n;  // column layout index k = j n + i
-    if (!P.warm) U[k] = init;
-    Vc[i * m + j] = P.warm ? V[k] : init;
-    bR[i * m + j] = b[k];
+  for (size_t k = threadIdx.x; k < nm; k += NT) {
+    const size_t j = k / n, i = k - j * n;  // interface index k = j n + i
+    UC[j * ldn + i] = P.warm ? U[k] : init;
+    aC[j * ldn + i] = a[k];
+    Vc[i * ldm + j] = P.warm ? V[k] : init;
+    bR[i * ldm + j] = b[k];
   }
   __syncthreads();
+  double e0 = 0.0;
+  int bad = 0;
   // prologue: TR = K1 phi (axis 1 on the columns of phi, stored transposed)
-  for (int j = warp; j < m; j += nw) {
-    double x[E], y[E];
-    load_line<E>(x, U + (size_t)j * n, n, 1, lane, true);
-    warp_line_apply<E>(x, y, P.lam1, P.wA1, P.wB1, lane);
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-      const int k = lane * E + e;
-      if (k < n) TR[(size_t)k * m + j] = y[e];
-    }
-  }
+  half_pass<E, W_PRO>(UC, nullptr, nullptr, nullptr, TR, n, ldn, m, ldm, P.lam1, P.wA1, P.wB1, stage, sp, warp,
+                      nw, lane, e0, bad);
   __syncthreads();
   const bool use_tol = P.tol > 0.0;
-  int it = 0, flag = 0, bad = 0;
+  int it = 0, flag = 0;
   double errv = NAN;
   while (true) {
     const bool check = (it >= P.itr_max) || (use_tol && (it % P.check_interval) == 0);
@@ -549,7 +622,8 @@ __global__ void __launch_bounds__(512) fs1_sep2d64w_kernel(const __grid_constant
     // lines 2-7 on the rows: psi = b / K2 TR, TC = K2 psi
     if (check) {
       double e = 0.0;
-      half_pass<E, true>(TR, bR, Vc, Vn, TC, m, n, P.lam2, P.wA2, P.wB2, warp, nw, lane, e, bad);
+      half_pass<E, W_CHECK>(TR, bR, Vc, Vn, TC, m, ldm, n, ldn, P.lam2, P.wA2, P.wB2, stage, sp, warp, nw, lane,
+                            e, bad);
       errv = block_sum(e, red);
       if (it >= P.itr_max || errv <= P.tol) {
         flag = (use_tol && errv <= P.tol) ? FLAG_CONVERGED : FLAG_ITR_MAX;
@@ -557,7 +631,8 @@ __global__ void __launch_bounds__(512) fs1_sep2d64w_kernel(const __grid_constant
       }
     } else {
       double e = 0.0;
-      half_pass<E, false>(TR, bR, nullptr, Vn, TC, m, n, P.lam2, P.wA2, P.wB2, warp, nw, lane, e, bad);
+      half_pass<E, W_UPD>(TR, bR, nullptr, Vn, TC, m, ldm, n, ldn, P.lam2, P.wA2, P.wB2, stage, sp, warp, nw,
+                          lane, e, bad);
     }
     {
       double* t = Vc;
@@ -568,7 +643,8 @@ __global__ void __launch_bounds__(512) fs1_sep2d64w_kernel(const __grid_constant
     // lines 8-12 on the columns: phi = a / K1 TC, TR = K1 phi
     {
       double e = 0.0;
-      half_pass<E, false>(TC, a, nullptr, U, TR, n, m, P.lam1, P.wA1, P.wB1, warp, nw, lane, e, bad);
+      half_pass<E, W_UPD>(TC, aC, nullptr, UC, TR, n, ldn, m, ldm, P.lam1, P.wA1, P.wB1, stage, sp, warp, nw,
+                          lane, e, bad);
     }
     ++it;  // line 13
     if (__syncthreads_or(bad)) {
@@ -578,10 +654,11 @@ __global__ void __launch_bounds__(512) fs1_sep2d64w_kernel(const __grid_constant
     }
   }
   __syncthreads();
-  // psi back to the column layout of the interface
-  for (size_t k = threadIdx.x; k < nm; k += blockDim.x) {
+  // phi and psi back to the interface layout
+  for (size_t k = threadIdx.x; k < nm; k += NT) {
     const size_t j = k / n, i = k - j * n;
-    V[k] = Vc[i * m + j];
+    U[k] = UC[j * ldn + i];
+    V[k] = Vc[i * ldm + j];
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -601,6 +678,10 @@ __global__ void __launch_bounds__(512) fs1_sep2d64w_kernel(const __grid_constant
 
 }  // namespace s64
 
+#ifndef W8NT
+#define W8NT 512
+#endif
+
 int sep2d64w_chunk(long long n, long long m) {
   const long long L = n > m ? n : m;
   for (int E : {2, 4, 8})
@@ -608,11 +689,32 @@ int sep2d64w_chunk(long long n, long long m) {
   return 0;
 }
 
-cudaError_t launch_sep2d64w(const Sep2d64Params& P, long long batch, int E, cudaStream_t st) {
+static int w_threads(int E) { return E == 8 ? W8NT : 512; }
+
+size_t sep2d64w_workspace(long long n, long long m, int E) {
+  const size_t ldn = (size_t)s64::w_ld((int)n, E), ldm = (size_t)s64::w_ld((int)m, E);
+  return (4 * (size_t)n * ldm + 3 * (size_t)m * ldn) * sizeof(double);
+}
+
+size_t sep2d64w_smem(long long n, long long m, int E) {
+  return (size_t)2 * (w_threads(E) / 32) * s64::w_sp((int)(n > m ? n : m), E) * sizeof(double);
+}
+
+const void* sep2d64w_fn(int E) {
   switch (E) {
-    case 2: s64::fs1_sep2d64w_kernel<2><<<(unsigned)batch, 512, 0, st>>>(P); break;
-    case 4: s64::fs1_sep2d64w_kernel<4><<<(unsigned)batch, 512, 0, st>>>(P); break;
-    case 8: s64::fs1_sep2d64w_kernel<8><<<(unsigned)batch, 512, 0, st>>>(P); break;
+    case 2: return (const void*)&s64::fs1_sep2d64w_kernel<2, 512>;
+    case 4: return (const void*)&s64::fs1_sep2d64w_kernel<4, 512>;
+    case 8: return (const void*)&s64::fs1_sep2d64w_kernel<8, W8NT>;
+    default: return nullptr;
+  }
+}
+
+cudaError_t launch_sep2d64w(const Sep2d64Params& P, long long batch, int E, cudaStream_t st) {
+  const size_t smem = sep2d64w_smem(P.n, P.m, E);
+  switch (E) {
+    case 2: s64::fs1_sep2d64w_kernel<2, 512><<<(unsigned)batch, 512, smem, st>>>(P); break;
+    case 4: s64::fs1_sep2d64w_kernel<4, 512><<<(unsigned)batch, 512, smem, st>>>(P); break;
+    case 8: s64::fs1_sep2d64w_kernel<8, W8NT><<<(unsigned)batch, W8NT, smem, st>>>(P); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
