@@ -452,10 +452,12 @@ __host__ __device__ inline int w_ld(int len, int E) { return (len + w_pad(E) - 1
 __host__ __device__ inline int w_sp(int L, int E) { return w_ld(L, E) + 2; }
 
 // lane's chunk of a padded line (ld doubles; only lanes whose chunk starts before ld
-// load), zero at and beyond len
+// load).  The pads of every internal line hold zeros (written once, never overwritten
+// by anything else), so the chunk needs no masking and nothing waits on the load
+// until the recursion consumes it.
 template <int E>
-__device__ __forceinline__ void vload_line(double (&x)[E], const double* __restrict__ line, int len, int ld,
-                                           int lane, bool valid) {
+__device__ __forceinline__ void vload_line(double (&x)[E], const double* __restrict__ line, int ld, int lane,
+                                           bool valid) {
   const int k0 = lane * E;
 #pragma unroll
   for (int e = 0; e < E; ++e) x[e] = 0.0;
@@ -471,9 +473,6 @@ __device__ __forceinline__ void vload_line(double (&x)[E], const double* __restr
                      : "l"(p + 4 * q));
     }
   }
-#pragma unroll
-  for (int e = 0; e < E; ++e)
-    if (k0 + e >= len) x[e] = 0.0;
 }
 
 template <int E>
@@ -510,38 +509,39 @@ __device__ __forceinline__ double upd_div(double t, double k) {
 //   y_new      = tgt / kz                               (line 7 / line 12),
 //   Tout       = K_this y_new, transposed                (the next half's first axis),
 //   MODE CHECK: acc += |y_old kz - tgt|                  (line 2's marginal error).
-// MODE PRO (prologue): Tout = K_this Tin, transposed, nothing else.
+// MODE PRO (prologue): Tout = K_this Tin, transposed, nothing else.  y_new is stored
+// only when `store` (the state is needed: before a check, see the kernel).
 // Lines go in rounds of NW (one per warp); a round's Tout lines are staged in shared
 // memory and written out column-wise by the whole CTA (NW consecutive doubles per
 // point: coalesced), one barrier per round with the stage double-buffered.  The next
 // line's Tin loads are in flight while this one is scanned.
 constexpr int W_PRO = 0, W_UPD = 1, W_CHECK = 2;
 
-template <int E, int MODE>
+template <int E, int NW, int MODE>
 __device__ __forceinline__ void half_pass(const double* __restrict__ Tin, const double* __restrict__ tgt,
-                                          const double* __restrict__ yold, double* __restrict__ ynew,
+                                          const double* __restrict__ yold, double* __restrict__ ynew, bool store,
                                           double* __restrict__ Tout, int len, int ld, int count, int ldo,
                                           double lam, const double* lvA, const double* lvB, double* stage, int sp,
-                                          int warp, int nw, int lane, double& acc, int& bad) {
+                                          int warp, int lane, double& acc, int& bad) {
   double v[E];
-  vload_line<E>(v, Tin + (size_t)warp * ld, len, ld, lane, warp < count);
+  vload_line<E>(v, Tin + (size_t)warp * ld, ld, lane, warp < count);
   int buf = 0;
-  for (int r0 = 0; r0 < count; r0 += nw, buf ^= 1) {
+  for (int r0 = 0; r0 < count; r0 += NW, buf ^= 1) {
     const int r = r0 + warp;
-    double* st = stage + (size_t)buf * nw * sp;
+    double* st = stage + (size_t)buf * NW * sp;
     if (r < count) {
       const size_t base = (size_t)r * ld;
       double nv[E], kz[E];
       double tg[E];
-      if (MODE != W_PRO) vload_line<E>(tg, tgt + base, len, ld, lane, true);
-      vload_line<E>(nv, Tin + base + (size_t)nw * ld, len, ld, lane, r + nw < count);
+      if (MODE != W_PRO) vload_line<E>(tg, tgt + base, ld, lane, true);
+      vload_line<E>(nv, Tin + base + (size_t)NW * ld, ld, lane, r + NW < count);
       warp_line_apply<E>(v, kz, lam, lvA, lvB, lane);
       if (MODE != W_PRO) {
         if (MODE == W_CHECK) {
           double yo[E];
-          vload_line<E>(yo, yold + base, len, ld, lane, true);
+          vload_line<E>(yo, yold + base, ld, lane, true);
 #pragma unroll
-          for (int e = 0; e < E; ++e) acc += fabs(yo[e] * kz[e] - tg[e]);  // zero beyond len
+          for (int e = 0; e < E; ++e) acc += fabs(yo[e] * kz[e] - tg[e]);  // pads: 0 kz - 0
         }
 #pragma unroll
         for (int e = 0; e < E; ++e) {
@@ -550,7 +550,7 @@ __device__ __forceinline__ void half_pass(const double* __restrict__ Tin, const 
           bad |= !isfinite(out);
           tg[e] = out;
         }
-        vstore_line<E>(ynew + base, tg, ld, lane);
+        if (store) vstore_line<E>(ynew + base, tg, ld, lane);
         warp_line_apply<E>(tg, kz, lam, lvA, lvB, lane);
       }
       // stage row `warp`: this line's Tout values, lane chunk as 16-byte vectors
@@ -564,16 +564,23 @@ __device__ __forceinline__ void half_pass(const double* __restrict__ Tin, const 
     }
     __syncthreads();
     // write-out: Tout[k ldo + r0 + w] = stage[w][k], NW consecutive doubles per point k
-    const int nr = count - r0 < nw ? count - r0 : nw;
-    for (int t = threadIdx.x; t < len * nw; t += blockDim.x) {
-      const int k = t / nw, w = t - k * nw;
+    const int nr = count - r0 < NW ? count - r0 : NW;
+    for (int t = threadIdx.x; t < len * NW; t += NW * 32) {
+      const int k = t / NW, w = t % NW;
       if (w < nr) Tout[(size_t)k * ldo + r0 + w] = st[(size_t)w * sp + k];
     }
   }
 }
 
+// 2D fp64 solve, one CTA per problem, one warp per line (K5w).  The loop keeps only the
+// two intermediates (TR, TC) and the targets live; phi and psi are stored only on the
+// iterations whose state a check can return (the iteration before every check, i.e.
+// before l = itr_max and, with tol > 0, before every check_interval-th one).  A problem
+// that turns non-finite replays from the last stored state with every iteration
+// stored, so it too returns the state at which it stopped (fs1.h).
 template <int E, int NT>
 __global__ void __launch_bounds__(NT) fs1_sep2d64w_kernel(const __grid_constant__ Sep2d64Params P) {
+  constexpr int NW = NT / 32;
   __shared__ double red[32];
   extern __shared__ __align__(16) double stage[];
   const int n = P.n, m = P.m;
@@ -596,8 +603,15 @@ __global__ void __launch_bounds__(NT) fs1_sep2d64w_kernel(const __grid_constant_
   const double* b = P.b + pb * nm;
   double* U = P.u + pb * nm;
   double* V = P.v + pb * nm;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = NT / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int sp = w_sp(n > m ? n : m, E);
+  {
+    // zero the pads (and everything else) of all seven buffers, then fill
+    double2* z = reinterpret_cast<double2*>(TR);
+    const size_t nz = (4 * szR + 3 * szC) / 2;
+    for (size_t k = threadIdx.x; k < nz; k += NT) z[k] = make_double2(0.0, 0.0);
+  }
+  __syncthreads();
   const double init = 1.0 / (double)nm;
   for (size_t k = threadIdx.x; k < nm; k += NT) {
     const size_t j = k / n, i = k - j * n;  // interface index k = j n + i
@@ -607,34 +621,40 @@ __global__ void __launch_bounds__(NT) fs1_sep2d64w_kernel(const __grid_constant_
     bR[i * ldm + j] = b[k];
   }
   __syncthreads();
-  double e0 = 0.0;
-  int bad = 0;
-  // prologue: TR = K1 phi (axis 1 on the columns of phi, stored transposed)
-  half_pass<E, W_PRO>(UC, nullptr, nullptr, nullptr, TR, n, ldn, m, ldm, P.lam1, P.wA1, P.wB1, stage, sp, warp,
-                      nw, lane, e0, bad);
-  __syncthreads();
   const bool use_tol = P.tol > 0.0;
-  int it = 0, flag = 0;
+  auto is_check = [&](int l) { return l >= P.itr_max || (use_tol && (l % P.check_interval) == 0); };
+  int it = 0, flag = 0, last = 0, bad = 0;
+  bool store_all = false;
   double errv = NAN;
+  bool prologue = true;
   while (true) {
-    const bool check = (it >= P.itr_max) || (use_tol && (it % P.check_interval) == 0);
+    if (prologue) {
+      // TR = K1 phi (axis 1 on the columns of phi, stored transposed)
+      double e0 = 0.0;
+      half_pass<E, NW, W_PRO>(UC, nullptr, nullptr, nullptr, false, TR, n, ldn, m, ldm, P.lam1, P.wA1, P.wB1,
+                              stage, sp, warp, lane, e0, bad);
+      __syncthreads();
+      prologue = false;
+    }
+    const bool check = is_check(it);
+    const bool store = store_all || is_check(it + 1);
     bad = 0;
     // lines 2-7 on the rows: psi = b / K2 TR, TC = K2 psi
     if (check) {
       double e = 0.0;
-      half_pass<E, W_CHECK>(TR, bR, Vc, Vn, TC, m, ldm, n, ldn, P.lam2, P.wA2, P.wB2, stage, sp, warp, nw, lane,
-                            e, bad);
+      half_pass<E, NW, W_CHECK>(TR, bR, Vc, Vn, store, TC, m, ldm, n, ldn, P.lam2, P.wA2, P.wB2, stage, sp, warp,
+                                lane, e, bad);
       errv = block_sum(e, red);
       if (it >= P.itr_max || errv <= P.tol) {
         flag = (use_tol && errv <= P.tol) ? FLAG_CONVERGED : FLAG_ITR_MAX;
-        break;  // psi stays Vc: the result of the last completed iteration
+        break;  // phi, psi in UC, Vc: the state of the last completed iteration
       }
     } else {
       double e = 0.0;
-      half_pass<E, W_UPD>(TR, bR, nullptr, Vn, TC, m, ldm, n, ldn, P.lam2, P.wA2, P.wB2, stage, sp, warp, nw,
-                          lane, e, bad);
+      half_pass<E, NW, W_UPD>(TR, bR, nullptr, Vn, store, TC, m, ldm, n, ldn, P.lam2, P.wA2, P.wB2, stage, sp,
+                              warp, lane, e, bad);
     }
-    {
+    if (store) {
       double* t = Vc;
       Vc = Vn;
       Vn = t;
@@ -643,15 +663,23 @@ __global__ void __launch_bounds__(NT) fs1_sep2d64w_kernel(const __grid_constant_
     // lines 8-12 on the columns: phi = a / K1 TC, TR = K1 phi
     {
       double e = 0.0;
-      half_pass<E, W_UPD>(TC, aC, nullptr, UC, TR, n, ldn, m, ldm, P.lam1, P.wA1, P.wB1, stage, sp, warp, nw,
-                          lane, e, bad);
+      half_pass<E, NW, W_UPD>(TC, aC, nullptr, UC, store, TR, n, ldn, m, ldm, P.lam1, P.wA1, P.wB1, stage, sp,
+                              warp, lane, e, bad);
     }
     ++it;  // line 13
     if (__syncthreads_or(bad)) {
+      if (!store_all) {
+        // replay from the stored state of iteration `last`, storing every iteration
+        store_all = true;
+        it = last;
+        prologue = true;
+        continue;
+      }
       flag = FLAG_NONFINITE;
       errv = NAN;
       break;
     }
+    if (store) last = it;
   }
   __syncthreads();
   // phi and psi back to the interface layout

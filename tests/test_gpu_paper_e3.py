@@ -13,7 +13,7 @@ import pytest
 
 import fs1_inputs as gi
 from oracle import dense, sinkhorn
-from tests.gpu_util import assert_solve_parity, rel
+from tests.gpu_util import assert_solve_parity, rel, rel_norm
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -112,3 +112,55 @@ def test_warp_line_variant_equals_thread_line_kernel(shape):
     info = fs1.plan(fs1.Spec(ndim=2, n=n, m=m, h1=h, h2=h, eps=eps, batch=2, dtype=torch.float64,
                              itr_max=itr)).info()
     assert info["kernel"].startswith("sep2d64w")
+
+
+def test_nonfinite_returns_the_stopping_state():
+    """K5w stores phi, psi only before checks; a problem that overflows replays from the
+    last stored state so that u, v still hold the state at which it stopped (fs1.h).
+    h = 1, eps = 2e-3: the unstabilised iteration overflows after a few hundred
+    iterations; NONFINITE at the oracle's iteration (as the thread-per-line kernel), and
+    the returned state is the one that tripped the check: a non-finite phi or psi entry
+    in every problem (the last state stored before the replay, the initial one, is
+    finite).  Which entries are inf and which NaN is not compared: past an overflow the
+    chunked scan forms inf * 0 (an underflowed lambda^L) where the sequential
+    recursion keeps inf, and the dense oracle 0 * inf for every lambda^|i-j| that
+    underflows."""
+    n, m = 24, 40
+    rng = np.random.default_rng(11)
+    A, B = gi.random_positive(rng, (2, n * m)), gi.random_positive(rng, (2, n * m))
+    kw = dict(h=1.0, h2=1.0, shape=(n, m), eps=0.002, itr_max=3000, domain="scaling")
+    ref = sinkhorn.solve(A, B, n=n, m=m, h1=1.0, h2=1.0, eps=0.002, itr_max=3000)
+    assert np.all(ref["flags"] == 2)
+    w = fs1.solve(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), **kw)
+    t = fs1.solve(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), kernel=5, **kw)
+    assert np.all(w["flags"].cpu().numpy() == 2)
+    np.testing.assert_array_equal(w["iters"].cpu().numpy(), ref["iters"])
+    np.testing.assert_array_equal(t["iters"].cpu().numpy(), ref["iters"])
+    assert np.isnan(w["cost"].cpu().numpy()).all() and np.isnan(w["err"].cpu().numpy()).all()
+    u, v = w["u"].cpu().numpy(), w["v"].cpu().numpy()
+    assert np.all((~np.isfinite(u)).any(1) | (~np.isfinite(v)).any(1))
+
+
+@pytest.mark.parametrize("ci", [1, 7])
+def test_check_interval_stop_state(ci):
+    """tol-stopped run with checks every ci iterations: the stored state at the stopping
+    check is the oracle's (the kernel stores phi, psi only before checks)."""
+    n, m = 24, 40
+    rng = np.random.default_rng(11)
+    A, B = gi.random_positive(rng, (2, n * m)), gi.random_positive(rng, (2, n * m))
+    h1, h2, eps = 1.0 / n, 1.0 / m, 0.05
+    kw = dict(h=h1, h2=h2, shape=(n, m), eps=eps, domain="scaling")
+    ref = sinkhorn.solve(A, B, n=n, m=m, h1=h1, h2=h2, eps=eps, itr_max=20000, tol=1e-9, check_interval=ci)
+    out = fs1.solve(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), itr_max=20000, tol=1e-9,
+                    check_interval=ci, **kw)
+    assert fs1.plan(fs1.Spec(ndim=2, n=n, m=m, h1=h1, h2=h2, eps=eps, batch=2, dtype=torch.float64,
+                             itr_max=20000, tol=1e-9, check_interval=ci)).info()["kernel"].startswith("sep2d64w")
+    it = out["iters"].cpu().numpy()
+    assert np.all(out["flags"].cpu().numpy() == 1) and np.all(it % ci == 0)
+    assert np.all(np.abs(it - ref["iters"]) <= ci)
+    for p in range(2):
+        fixed = sinkhorn.solve(A[p:p + 1], B[p:p + 1], n=n, m=m, h1=h1, h2=h2, eps=eps, itr_max=int(it[p]))
+        one = {k: out[k][p:p + 1] for k in ("u", "v", "cost")}
+        assert rel_norm(np.log(one["u"].cpu().numpy()[0]), fixed["F"][0]) <= 1e-10
+        assert rel_norm(np.log(one["v"].cpu().numpy()[0]), fixed["G"][0]) <= 1e-10
+        assert rel(one["cost"].item(), fixed["cost"][0]) <= 1e-10
