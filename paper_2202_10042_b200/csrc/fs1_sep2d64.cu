@@ -543,13 +543,27 @@ __device__ __forceinline__ void half_pass(const double* __restrict__ Tin, const 
 #pragma unroll
           for (int e = 0; e < E; ++e) acc += fabs(yo[e] * kz[e] - tg[e]);  // pads: 0 kz - 0
         }
+        // line 7 / 12 (upd_div) with the range test hoisted: one warp-uniform branch per
+        // line; pads divide 0 / 1.  Non-finite test on sum(out) / 8 (positive terms: any
+        // inf or NaN survives, finite ones cannot overflow)
+        bool inr = true;
 #pragma unroll
         for (int e = 0; e < E; ++e) {
-          const bool live = lane * E + e < len;
-          const double out = live ? upd_div(tg[e], kz[e]) : 0.0;
-          bad |= !isfinite(out);
-          tg[e] = out;
+          if (lane * E + e >= len) kz[e] = 1.0;
+          const double ak = fabs(kz[e]);
+          inr &= ak > 0x1p-1000 && ak < 0x1p1000;
         }
+        double chk = 0.0;
+        if (__all_sync(FULL, inr)) {
+#pragma unroll
+          for (int e = 0; e < E; ++e) tg[e] = Tr<double>::div<true>(tg[e], kz[e]);
+        } else {
+#pragma unroll
+          for (int e = 0; e < E; ++e) tg[e] = upd_div(tg[e], kz[e]);
+        }
+#pragma unroll
+        for (int e = 0; e < E; ++e) chk = fma(tg[e], 0.125, chk);
+        bad |= !isfinite(chk);
         if (store) vstore_line<E>(ynew + base, tg, ld, lane);
         warp_line_apply<E>(tg, kz, lam, lvA, lvB, lane);
       }
@@ -563,11 +577,21 @@ __device__ __forceinline__ void half_pass(const double* __restrict__ Tin, const 
       for (int e = 0; e < E; ++e) v[e] = nv[e];
     }
     __syncthreads();
-    // write-out: Tout[k ldo + r0 + w] = stage[w][k], NW consecutive doubles per point k
+    // write-out: Tout[k ldo + r0 + w] = stage[w][k], NW consecutive doubles per point k,
+    // four per thread as one 32-byte store (ldo and r0 are multiples of 4)
     const int nr = count - r0 < NW ? count - r0 : NW;
-    for (int t = threadIdx.x; t < len * NW; t += NW * 32) {
-      const int k = t / NW, w = t % NW;
-      if (w < nr) Tout[(size_t)k * ldo + r0 + w] = st[(size_t)w * sp + k];
+    for (int t = threadIdx.x; t < len * (NW / 4); t += NW * 32) {
+      const int k = t / (NW / 4), w = 4 * (t % (NW / 4));
+      if (w >= nr) continue;
+      const double* sc = st + (size_t)w * sp + k;
+      double* o = Tout + (size_t)k * ldo + r0 + w;
+      if (w + 4 <= nr) {
+        asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(o), "d"(sc[0]), "d"(sc[sp]), "d"(sc[2 * sp]),
+                     "d"(sc[3 * sp])
+                     : "memory");
+      } else {
+        for (int q = 0; w + q < nr; ++q) o[q] = sc[(size_t)q * sp];
+      }
     }
   }
 }
