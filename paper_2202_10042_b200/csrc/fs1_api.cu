@@ -488,14 +488,16 @@ static fs1_status plan_impl(const fs1_desc* desc, int device, int force, fs1_pla
     const long long lines = d.ndim == 3 ? std::max<long long>(std::max<long long>(d.m * L3, d.n * L3), d.n * d.m)
                                         : std::max<long long>(d.n, d.m);
     p->threads = (int)std::min<long long>(512, ((lines + 31) / 32) * 32);
-    // 2D problems whose lines fit one warp (32 E points, E <= 8): K5w, one warp per line
-    // with a chunked scan (test-only kind 5 keeps the thread-per-line kernel)
+    // 2D problems whose lines fit a warp (G E <= 256 points): K5w, G lanes per line with
+    // a chunked scan (test-only kind 5 keeps the thread-per-line kernel)
     const int wE = d.ndim == 2 && force != 5 ? sep2d64w_chunk(d.n, d.m) : 0;
+    int wG = 0, wEp = 0;
     if (wE) {
       D.wE = wE;
+      sep2d64w_geom(wE, &wG, &wEp);
       const long double cc[2] = {(long double)d.h1 / (long double)d.eps, (long double)d.h2 / (long double)d.eps};
       for (int k = 0; k < 5; ++k) {
-        const long double L = (long double)wE * (long double)(1 << k);
+        const long double L = (long double)wEp * (long double)(1 << k);
         const long double La = ceill(L / 2), Lb = floorl(L / 2);
         D.wA1[k] = (double)expl(-cc[0] * La);
         D.wB1[k] = (double)expl(-cc[0] * Lb);
@@ -505,7 +507,8 @@ static fs1_status plan_impl(const fs1_desc* desc, int device, int force, fs1_pla
     }
     // K5w's transposition stage (fs1_sep2d64.cu); else small 2D problems: the
     // intermediate in shared memory
-    const size_t ssm = wE ? sep2d64w_smem(d.n, d.m, wE) : sep2d64_smem(d.n, d.m, d.ndim);
+    if (wE) p->threads = sep2d64w_threads(d.n, d.m, wE);
+    const size_t ssm = wE ? sep2d64w_smem(d.n, d.m, wE, p->threads) : sep2d64_smem(d.n, d.m, d.ndim);
     if (ssm > (wE ? 48 * 1024 : 0)) {
       std::lock_guard<std::mutex> lk(g_attr_mu);
       int cur = 0;
@@ -520,7 +523,7 @@ static fs1_status plan_impl(const fs1_desc* desc, int device, int force, fs1_pla
     p->ws = al256(wE ? (size_t)d.batch * sep2d64w_workspace(d.n, d.m, wE)
                      : (size_t)d.batch * 3 * (size_t)d.n * (size_t)d.m * (size_t)L3 * 8);
     p->smem = 0;
-    if (wE) snprintf(p->info.kernel, sizeof(p->info.kernel), "sep2d64w_f64_scaling_E%d", wE);
+    if (wE) snprintf(p->info.kernel, sizeof(p->info.kernel), "sep2d64w_f64_scaling_G%dE%d", wG, wEp);
     else snprintf(p->info.kernel, sizeof(p->info.kernel), d.ndim == 3 ? "sep3d64_f64_scaling" : "sep2d64_f64_scaling");
     p->info.chunk = 1;
     p->info.threads = p->threads;
@@ -690,7 +693,7 @@ fs1_status fs1_solve(const fs1_plan_t* plan, const void* a, const void* b, void*
     P.iters = iters; P.err = err; P.flags = flags; P.cost = cost;
     P.ws = (double*)workspace;
     P.mode = 0;
-    const cudaError_t e = P.wE ? launch_sep2d64w(P, plan->d.batch, P.wE, (cudaStream_t)stream)
+    const cudaError_t e = P.wE ? launch_sep2d64w(P, plan->d.batch, P.wE, plan->threads, (cudaStream_t)stream)
                                : launch_sep2d64(P, plan->d.batch, plan->threads, (cudaStream_t)stream);
     return e == cudaSuccess ? FS1_OK : FS1_ERR_CUDA;
   }

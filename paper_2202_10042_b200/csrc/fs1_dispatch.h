@@ -61,11 +61,13 @@ const StabEntry* stab_table(int* count);
 // K5 fp64 scaling-domain 2D solve, one CTA per problem (fs1_sep2d64.cu)
 cudaError_t launch_sep2d64(const Sep2d64Params& P, long long batch, int threads, cudaStream_t st);
 size_t sep2d64_smem(long long n, long long m, int ndim);  // dynamic shared memory of the staged 2D path (0: none)
-int sep2d64w_chunk(long long n, long long m);             // K5w chunk E for a 2D problem (0: not applicable)
-cudaError_t launch_sep2d64w(const Sep2d64Params& P, long long batch, int E, cudaStream_t st);
-size_t sep2d64w_workspace(long long n, long long m, int E);  // K5w workspace bytes per problem
-size_t sep2d64w_smem(long long n, long long m, int E);       // K5w dynamic shared memory
-const void* sep2d64w_fn(int E);
+int sep2d64w_chunk(long long n, long long m);             // K5w variant for a 2D problem (0: none)
+void sep2d64w_geom(int var, int* G, int* E);               // lanes per line, points per lane
+cudaError_t launch_sep2d64w(const Sep2d64Params& P, long long batch, int var, int threads, cudaStream_t st);
+int sep2d64w_threads(long long n, long long m, int var);       // K5w block size
+size_t sep2d64w_workspace(long long n, long long m, int var);  // K5w workspace bytes per problem
+size_t sep2d64w_smem(long long n, long long m, int var, int threads);  // K5w dynamic shared memory
+const void* sep2d64w_fn(int var);
 const void* sep2d64_fn();
 
 // dual objective and eps-scaling warm start (fs1_extra.cu)

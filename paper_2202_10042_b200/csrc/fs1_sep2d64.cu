@@ -395,33 +395,37 @@ __global__ void __launch_bounds__(512) fs1_sep2d64_kernel(const __grid_constant_
 }
 
 // ---------------------------------------------------------------------------------
-// K5w: the same 2D solve with ONE WARP per line: lane l owns the E contiguous points
-// [l E, l E + E) of a line of up to 32 E, the line apply is a chunked scan (lane Horner
-// aggregates, a 5-level warp scan of the affine maps y -> lambda^L y + c, both recursions
-// from the exact carries) instead of one thread walking the whole line.  The scan
+// K5w: the same 2D solve with G LANES per line (G = 1 .. 32, 32 / G lines per warp): lane
+// q of a segment owns the E contiguous points [q E, q E + E) of a line of up to G E,
+// and the line apply is a chunked scan (lane Horner aggregates, a log2(G)-level segment
+// scan of the affine maps y -> lambda^L y + c, both recursions from the exact carries)
+// instead of one thread walking the whole line (G = 1: exactly that).  The scan
 // multipliers lambda^{E 2^k} are formed on the host as two factors (each >= sqrt of
 // the power) so that an underflow of the power alone cannot zero a carry that is still
-// representable (Remark 3.3; lambda = e^{-100} at E3).  The axis-1
-// result goes through the workspace (L1/L2); the axis-2 pass is fused with the update.
+// representable (Remark 3.3; lambda = e^{-100} at E3).
 
-template <int E>
-__device__ __forceinline__ void warp_line_apply(const double (&x)[E], double (&y)[E], double lam,
-                                                const double* lvA, const double* lvB, int lane) {
+template <int G, int E>
+__device__ __forceinline__ void seg_line_apply(const double (&x)[E], double (&y)[E], double lam,
+                                               const double* lvA, const double* lvB, int q) {
   double f = 0.0, g = 0.0;
 #pragma unroll
   for (int e = 0; e < E; ++e) f = fma(lam, f, x[e]);           // forward value at the chunk end
 #pragma unroll
   for (int e = E - 1; e >= 0; --e) g = fma(lam, g, x[e]);      // backward value at the chunk start
+  double cf = 0.0, cb = 0.0;
+  if constexpr (G > 1) {
 #pragma unroll
-  for (int k = 0; k < 5; ++k) {
-    const int d = 1 << k;
-    const double up = __shfl_up_sync(FULL, f, d), dn = __shfl_down_sync(FULL, g, d);
-    if (lane >= d) f = fma(up * lvA[k], lvB[k], f);
-    if (lane + d < 32) g = fma(dn * lvA[k], lvB[k], g);
+    for (int k = 0; (1 << k) < G; ++k) {
+      const int d = 1 << k;
+      const double up = __shfl_up_sync(FULL, f, d, G), dn = __shfl_down_sync(FULL, g, d, G);
+      if (q >= d) f = fma(up * lvA[k], lvB[k], f);
+      if (q + d < G) g = fma(dn * lvA[k], lvB[k], g);
+    }
+    cf = __shfl_up_sync(FULL, f, 1, G);
+    cb = __shfl_down_sync(FULL, g, 1, G);
+    if (q == 0) cf = 0.0;
+    if (q == G - 1) cb = 0.0;
   }
-  double cf = __shfl_up_sync(FULL, f, 1), cb = __shfl_down_sync(FULL, g, 1);
-  if (lane == 0) cf = 0.0;
-  if (lane == 31) cb = 0.0;
   // forward recursion r_k = lam r_{k-1} + x_k from the exact carry
   double p = cf;
 #pragma unroll
@@ -439,55 +443,54 @@ __device__ __forceinline__ void warp_line_apply(const double (&x)[E], double (&y
   }
 }
 
-// Internal layouts of K5w (workspace): every line padded to a multiple of PADW doubles
-// (>= E), so that a lane's E points are one aligned 16 / 32-byte vector and a line's
-// loads are a single contiguous, coalesced request.  Row layout: [i ldm + j]
-// (axis 2 contiguous); column layout: [j ldn + i] (axis 1 contiguous, the layout of the
-// interface's u, v, a, b).
-__host__ __device__ constexpr int w_pad(int E) { return E > 4 ? E : 4; }
-__host__ __device__ inline int w_ld(int len, int E) { return (len + w_pad(E) - 1) / w_pad(E) * w_pad(E); }
-// shared-memory stage of one round of transposed line results: NW lines x SP points,
-// SP = w_ld(L) + 2 (holds a lane's whole chunk; even: 16-byte aligned rows; = 2 mod 4:
-// the column-wise readout of NW rows spreads over the banks)
-__host__ __device__ inline int w_sp(int L, int E) { return w_ld(L, E) + 2; }
+// Internal layouts of K5w (workspace): every line padded to a multiple of lcm(E, 4)
+// doubles, so that a lane's E points are aligned 16 / 32-byte vectors inside the line
+// and rows start 32-byte aligned.  Row layout: [i ldm + j] (axis 2 contiguous); column
+// layout: [j ldn + i] (axis 1 contiguous, the layout of the interface's u, v, a, b).
+__host__ __device__ constexpr int w_padw(int E) { return E % 4 == 0 ? E : (E % 2 == 0 ? 2 * E : 4 * E); }
+__host__ __device__ inline int w_ld(int len, int E) { return (len + w_padw(E) - 1) / w_padw(E) * w_padw(E); }
+// shared-memory stage of one round of transposed line results: RL lines x SP points,
+// SP = ld + 2 or + 4 (>= a whole chunk row; even: 16-byte aligned rows; = 2 mod 4: the
+// column-wise readout of consecutive rows spreads over the banks)
+__host__ __device__ inline int w_sp(int L, int E) {
+  const int ld = w_ld(L, E);
+  return ld % 4 == 0 ? ld + 2 : ld + 4;
+}
 
-// lane's chunk of a padded line (ld doubles; only lanes whose chunk starts before ld
-// load).  The pads of every internal line hold zeros (written once, never overwritten
-// by anything else), so the chunk needs no masking and nothing waits on the load
-// until the recursion consumes it.
+// lane's chunk (E doubles from `line`; all inside the padded line).  The pads of
+// every internal line hold zeros (written once, never overwritten), so nothing masks
+// the chunk and nothing waits on the load until the recursion consumes it.
 template <int E>
-__device__ __forceinline__ void vload_line(double (&x)[E], const double* __restrict__ line, int ld, int lane,
-                                           bool valid) {
-  const int k0 = lane * E;
+__device__ __forceinline__ void vload(double (&x)[E], const double* __restrict__ p, bool valid) {
 #pragma unroll
   for (int e = 0; e < E; ++e) x[e] = 0.0;
-  if (valid && k0 < ld) {
-    const double* p = line + k0;
-    if constexpr (E == 2) {
-      asm volatile("ld.global.v2.f64 {%0,%1}, [%2];" : "=d"(x[0]), "=d"(x[1]) : "l"(p));
-    } else {
+  if (valid) {
+    if constexpr (E % 4 == 0) {
 #pragma unroll
       for (int q = 0; q < E / 4; ++q)
         asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];"
                      : "=d"(x[4 * q]), "=d"(x[4 * q + 1]), "=d"(x[4 * q + 2]), "=d"(x[4 * q + 3])
                      : "l"(p + 4 * q));
+    } else {
+#pragma unroll
+      for (int q = 0; q < E / 2; ++q)
+        asm volatile("ld.global.v2.f64 {%0,%1}, [%2];" : "=d"(x[2 * q]), "=d"(x[2 * q + 1]) : "l"(p + 2 * q));
     }
   }
 }
 
 template <int E>
-__device__ __forceinline__ void vstore_line(double* __restrict__ line, const double (&x)[E], int ld, int lane) {
-  const int k0 = lane * E;
-  if (k0 >= ld) return;
-  double* p = line + k0;
-  if constexpr (E == 2) {
-    asm volatile("st.global.v2.f64 [%0], {%1,%2};" ::"l"(p), "d"(x[0]), "d"(x[1]) : "memory");
-  } else {
+__device__ __forceinline__ void vstore(double* __restrict__ p, const double (&x)[E]) {
+  if constexpr (E % 4 == 0) {
 #pragma unroll
     for (int q = 0; q < E / 4; ++q)
       asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p + 4 * q), "d"(x[4 * q]), "d"(x[4 * q + 1]),
                    "d"(x[4 * q + 2]), "d"(x[4 * q + 3])
                    : "memory");
+  } else {
+#pragma unroll
+    for (int q = 0; q < E / 2; ++q)
+      asm volatile("st.global.v2.f64 [%0], {%1,%2};" ::"l"(p + 2 * q), "d"(x[2 * q]), "d"(x[2 * q + 1]) : "memory");
   }
 }
 
@@ -511,78 +514,88 @@ __device__ __forceinline__ double upd_div(double t, double k) {
 //   MODE CHECK: acc += |y_old kz - tgt|                  (line 2's marginal error).
 // MODE PRO (prologue): Tout = K_this Tin, transposed, nothing else.  y_new is stored
 // only when `store` (the state is needed: before a check, see the kernel).
-// Lines go in rounds of NW (one per warp); a round's Tout lines are staged in shared
-// memory and written out column-wise by the whole CTA (NW consecutive doubles per
-// point: coalesced), one barrier per round with the stage double-buffered.  The next
-// line's Tin loads are in flight while this one is scanned.
+// Lines go in rounds of RL = NW 32 / G (one per segment); a round's Tout lines are
+// staged in shared memory and written out column-wise by the whole CTA (RL consecutive
+// doubles per point: coalesced), one barrier per round with the stage double-buffered.
+// The next line's Tin loads are in flight while this one is scanned.
 constexpr int W_PRO = 0, W_UPD = 1, W_CHECK = 2;
 
-template <int E, int NW, int MODE>
+template <int G, int E, int MODE>
 __device__ __forceinline__ void half_pass(const double* __restrict__ Tin, const double* __restrict__ tgt,
                                           const double* __restrict__ yold, double* __restrict__ ynew, bool store,
                                           double* __restrict__ Tout, int len, int ld, int count, int ldo,
                                           double lam, const double* lvA, const double* lvB, double* stage, int sp,
-                                          int warp, int lane, double& acc, int& bad) {
+                                          int seg, int q, int nw, double& acc, int& bad) {
+  const int RL = nw * (32 / G);
+  const int k0 = q * E;               // this lane's first point on its line
+  const bool chunk = k0 < ld;         // the chunk lies inside the padded line
   double v[E];
-  vload_line<E>(v, Tin + (size_t)warp * ld, ld, lane, warp < count);
+  if (MODE != W_CHECK) vload<E>(v, Tin + (size_t)seg * ld + k0, chunk && seg < count);
   int buf = 0;
-  for (int r0 = 0; r0 < count; r0 += NW, buf ^= 1) {
-    const int r = r0 + warp;
-    double* st = stage + (size_t)buf * NW * sp;
-    if (r < count) {
-      const size_t base = (size_t)r * ld;
-      double nv[E], kz[E];
-      double tg[E];
-      if (MODE != W_PRO) vload_line<E>(tg, tgt + base, ld, lane, true);
-      vload_line<E>(nv, Tin + base + (size_t)NW * ld, ld, lane, r + NW < count);
-      warp_line_apply<E>(v, kz, lam, lvA, lvB, lane);
-      if (MODE != W_PRO) {
-        if (MODE == W_CHECK) {
-          double yo[E];
-          vload_line<E>(yo, yold + base, ld, lane, true);
+  for (int r0 = 0; r0 < count; r0 += RL, buf ^= 1) {
+    const int r = r0 + seg;
+    const bool live = r < count;
+    double* st = stage + (size_t)buf * RL * sp;
+    const size_t base = (size_t)r * ld + k0;
+    double nv[E], kz[E];
+    double tg[E];
+    if (MODE != W_PRO) vload<E>(tg, tgt + base, chunk && live);
+    // (check passes, rare, load their lines one at a time: the old psi takes the
+    // registers of the prefetch)
+    if (MODE == W_CHECK) vload<E>(v, Tin + base, chunk && live);
+    else vload<E>(nv, Tin + base + (size_t)RL * ld, chunk && r + RL < count);
+    seg_line_apply<G, E>(v, kz, lam, lvA, lvB, q);
+    if (MODE != W_PRO) {
+      if (MODE == W_CHECK) {
+        double yo[E];
+        vload<E>(yo, yold + base, chunk && live);
 #pragma unroll
-          for (int e = 0; e < E; ++e) acc += fabs(yo[e] * kz[e] - tg[e]);  // pads: 0 kz - 0
-        }
-        // line 7 / 12 (upd_div) with the range test hoisted: one warp-uniform branch per
-        // line; pads divide 0 / 1.  Non-finite test on sum(out) / 8 (positive terms: any
-        // inf or NaN survives, finite ones cannot overflow)
-        bool inr = true;
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-          if (lane * E + e >= len) kz[e] = 1.0;
-          const double ak = fabs(kz[e]);
-          inr &= ak > 0x1p-1000 && ak < 0x1p1000;
-        }
-        double chk = 0.0;
-        if (__all_sync(FULL, inr)) {
-#pragma unroll
-          for (int e = 0; e < E; ++e) tg[e] = Tr<double>::div<true>(tg[e], kz[e]);
-        } else {
-#pragma unroll
-          for (int e = 0; e < E; ++e) tg[e] = upd_div(tg[e], kz[e]);
-        }
-#pragma unroll
-        for (int e = 0; e < E; ++e) chk = fma(tg[e], 0.125, chk);
-        bad |= !isfinite(chk);
-        if (store) vstore_line<E>(ynew + base, tg, ld, lane);
-        warp_line_apply<E>(tg, kz, lam, lvA, lvB, lane);
+        for (int e = 0; e < E; ++e) acc += fabs(yo[e] * kz[e] - tg[e]);  // pads, dead lines: 0 kz - 0
       }
-      // stage row `warp`: this line's Tout values, lane chunk as 16-byte vectors
-      if (lane * E < len) {
-        double2* srow = reinterpret_cast<double2*>(st + (size_t)warp * sp + lane * E);
+      // line 7 / 12 (upd_div) with the range test hoisted: one warp-uniform branch per
+      // line; pads and dead lines divide 0 / 1.  Non-finite test on sum(out) / 16
+      // (positive terms: any inf or NaN survives, finite ones cannot overflow)
+      bool inr = true;
 #pragma unroll
-        for (int q = 0; q < E / 2; ++q) srow[q] = make_double2(kz[2 * q], kz[2 * q + 1]);
+      for (int e = 0; e < E; ++e) {
+        if (!live || k0 + e >= len) kz[e] = 1.0;
+        const double ak = fabs(kz[e]);
+        inr &= ak > 0x1p-1000 && ak < 0x1p1000;
       }
+      if (__all_sync(FULL, inr)) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) tg[e] = Tr<double>::div<true>(tg[e], kz[e]);
+      } else {
+#pragma unroll
+        for (int e = 0; e < E; ++e) tg[e] = upd_div(tg[e], kz[e]);
+      }
+      double chk = 0.0;
+#pragma unroll
+      for (int e = 0; e < E; ++e) chk = fma(tg[e], 0.0625, chk);
+      bad |= !isfinite(chk);
+      if (store && chunk && live) vstore<E>(ynew + base, tg);
+      seg_line_apply<G, E>(tg, kz, lam, lvA, lvB, q);
+    }
+    // stage row `seg`: this line's Tout values, lane chunk as 16-byte vectors
+    if (live && k0 < len) {
+      double2* srow = reinterpret_cast<double2*>(st + (size_t)seg * sp + k0);
+#pragma unroll
+      for (int h = 0; h < E / 2; ++h) srow[h] = make_double2(kz[2 * h], kz[2 * h + 1]);
+    }
+    if (MODE != W_CHECK) {
 #pragma unroll
       for (int e = 0; e < E; ++e) v[e] = nv[e];
     }
     __syncthreads();
-    // write-out: Tout[k ldo + r0 + w] = stage[w][k], NW consecutive doubles per point k,
-    // four per thread as one 32-byte store (ldo and r0 are multiples of 4)
-    const int nr = count - r0 < NW ? count - r0 : NW;
-    for (int t = threadIdx.x; t < len * (NW / 4); t += NW * 32) {
-      const int k = t / (NW / 4), w = 4 * (t % (NW / 4));
-      if (w >= nr) continue;
+    // write-out: Tout[k ldo + r0 + w] = stage[w][k], nr <= RL consecutive doubles per
+    // point k, four per thread as one 32-byte store (ldo and r0 are multiples of 4);
+    // thread t takes (k, group) = divmod(t, NQ), then steps by the block size
+    const int nr = count - r0 < RL ? count - r0 : RL;
+    const int NQ = (nr + 3) >> 2, T = nw * 32;
+    const int dk = T / NQ, dg = T - dk * NQ;
+    int k = threadIdx.x / NQ, g = threadIdx.x - k * NQ;
+    for (; k < len;) {
+      const int w = 4 * g;
       const double* sc = st + (size_t)w * sp + k;
       double* o = Tout + (size_t)k * ldo + r0 + w;
       if (w + 4 <= nr) {
@@ -590,21 +603,27 @@ __device__ __forceinline__ void half_pass(const double* __restrict__ Tin, const 
                      "d"(sc[3 * sp])
                      : "memory");
       } else {
-        for (int q = 0; w + q < nr; ++q) o[q] = sc[(size_t)q * sp];
+        for (int h = 0; w + h < nr; ++h) o[h] = sc[(size_t)h * sp];
+      }
+      k += dk;
+      g += dg;
+      if (g >= NQ) {
+        g -= NQ;
+        ++k;
       }
     }
   }
 }
 
-// 2D fp64 solve, one CTA per problem, one warp per line (K5w).  The loop keeps only the
-// two intermediates (TR, TC) and the targets live; phi and psi are stored only on the
-// iterations whose state a check can return (the iteration before every check, i.e.
-// before l = itr_max and, with tol > 0, before every check_interval-th one).  A problem
-// that turns non-finite replays from the last stored state with every iteration
-// stored, so it too returns the state at which it stopped (fs1.h).
-template <int E, int NT>
+// 2D fp64 solve, one CTA per problem (K5w).  The loop keeps only the two intermediates
+// (TR, TC) and the targets live; phi and psi are stored only on the iterations whose
+// state a check can return (the iteration before every check, i.e. before
+// l = itr_max and, with tol > 0, before every check_interval-th one).  A problem that
+// turns non-finite replays from the last stored state with every iteration stored, so
+// it too returns the state at which it stopped (fs1.h).
+template <int G, int E, int NT>
 __global__ void __launch_bounds__(NT) fs1_sep2d64w_kernel(const __grid_constant__ Sep2d64Params P) {
-  constexpr int NW = NT / 32;
+  const int NW = blockDim.x >> 5, BT = blockDim.x;  // launched with <= NT threads
   __shared__ double red[32];
   extern __shared__ __align__(16) double stage[];
   const int n = P.n, m = P.m;
@@ -628,16 +647,17 @@ __global__ void __launch_bounds__(NT) fs1_sep2d64w_kernel(const __grid_constant_
   double* U = P.u + pb * nm;
   double* V = P.v + pb * nm;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int seg = warp * (32 / G) + lane / G, q = lane % G;  // line slot in a round, lane in the line
   const int sp = w_sp(n > m ? n : m, E);
   {
     // zero the pads (and everything else) of all seven buffers, then fill
     double2* z = reinterpret_cast<double2*>(TR);
     const size_t nz = (4 * szR + 3 * szC) / 2;
-    for (size_t k = threadIdx.x; k < nz; k += NT) z[k] = make_double2(0.0, 0.0);
+    for (size_t k = threadIdx.x; k < nz; k += BT) z[k] = make_double2(0.0, 0.0);
   }
   __syncthreads();
   const double init = 1.0 / (double)nm;
-  for (size_t k = threadIdx.x; k < nm; k += NT) {
+  for (size_t k = threadIdx.x; k < nm; k += BT) {
     const size_t j = k / n, i = k - j * n;  // interface index k = j n + i
     UC[j * ldn + i] = P.warm ? U[k] : init;
     aC[j * ldn + i] = a[k];
@@ -655,8 +675,8 @@ __global__ void __launch_bounds__(NT) fs1_sep2d64w_kernel(const __grid_constant_
     if (prologue) {
       // TR = K1 phi (axis 1 on the columns of phi, stored transposed)
       double e0 = 0.0;
-      half_pass<E, NW, W_PRO>(UC, nullptr, nullptr, nullptr, false, TR, n, ldn, m, ldm, P.lam1, P.wA1, P.wB1,
-                              stage, sp, warp, lane, e0, bad);
+      half_pass<G, E, W_PRO>(UC, nullptr, nullptr, nullptr, false, TR, n, ldn, m, ldm, P.lam1, P.wA1, P.wB1,
+                                 stage, sp, seg, q, NW, e0, bad);
       __syncthreads();
       prologue = false;
     }
@@ -666,8 +686,8 @@ __global__ void __launch_bounds__(NT) fs1_sep2d64w_kernel(const __grid_constant_
     // lines 2-7 on the rows: psi = b / K2 TR, TC = K2 psi
     if (check) {
       double e = 0.0;
-      half_pass<E, NW, W_CHECK>(TR, bR, Vc, Vn, store, TC, m, ldm, n, ldn, P.lam2, P.wA2, P.wB2, stage, sp, warp,
-                                lane, e, bad);
+      half_pass<G, E, W_CHECK>(TR, bR, Vc, Vn, store, TC, m, ldm, n, ldn, P.lam2, P.wA2, P.wB2, stage, sp,
+                                   seg, q, NW, e, bad);
       errv = block_sum(e, red);
       if (it >= P.itr_max || errv <= P.tol) {
         flag = (use_tol && errv <= P.tol) ? FLAG_CONVERGED : FLAG_ITR_MAX;
@@ -675,8 +695,8 @@ __global__ void __launch_bounds__(NT) fs1_sep2d64w_kernel(const __grid_constant_
       }
     } else {
       double e = 0.0;
-      half_pass<E, NW, W_UPD>(TR, bR, nullptr, Vn, store, TC, m, ldm, n, ldn, P.lam2, P.wA2, P.wB2, stage, sp,
-                              warp, lane, e, bad);
+      half_pass<G, E, W_UPD>(TR, bR, nullptr, Vn, store, TC, m, ldm, n, ldn, P.lam2, P.wA2, P.wB2, stage, sp,
+                                 seg, q, NW, e, bad);
     }
     if (store) {
       double* t = Vc;
@@ -687,8 +707,8 @@ __global__ void __launch_bounds__(NT) fs1_sep2d64w_kernel(const __grid_constant_
     // lines 8-12 on the columns: phi = a / K1 TC, TR = K1 phi
     {
       double e = 0.0;
-      half_pass<E, NW, W_UPD>(TC, aC, nullptr, UC, store, TR, n, ldn, m, ldm, P.lam1, P.wA1, P.wB1, stage, sp,
-                              warp, lane, e, bad);
+      half_pass<G, E, W_UPD>(TC, aC, nullptr, UC, store, TR, n, ldn, m, ldm, P.lam1, P.wA1, P.wB1, stage, sp,
+                                 seg, q, NW, e, bad);
     }
     ++it;  // line 13
     if (__syncthreads_or(bad)) {
@@ -707,7 +727,7 @@ __global__ void __launch_bounds__(NT) fs1_sep2d64w_kernel(const __grid_constant_
   }
   __syncthreads();
   // phi and psi back to the interface layout
-  for (size_t k = threadIdx.x; k < nm; k += NT) {
+  for (size_t k = threadIdx.x; k < nm; k += BT) {
     const size_t j = k / n, i = k - j * n;
     U[k] = UC[j * ldn + i];
     V[k] = Vc[i * ldm + j];
@@ -728,45 +748,94 @@ __global__ void __launch_bounds__(NT) fs1_sep2d64w_kernel(const __grid_constant_
   if (threadIdx.x == 0) P.cost[pb] = cost;
 }
 
+// the instantiated (G, E) pairs; a plan picks the cheapest that covers max(n, m)
+// (NT: the launch bound, the most threads a plan may launch: 384 keeps E = 10 free of
+// spills)
+struct WVar {
+  int G, E, NT;
+};
+constexpr WVar W_VARS[] = {{1, 10, 384}, {2, 10, 384}, {4, 10, 384}, {8, 10, 384}, {16, 10, 384}, {32, 8, 512}};
+
 }  // namespace s64
 
-#ifndef W8NT
-#define W8NT 512
-#endif
-
+// K5w variant for a 2D problem: 1 + the index into W_VARS of the pair (G lanes per line,
+// E points per lane) with G E >= max(n, m) and the fewest instructions per line under
+// the count model (6 E + 12 log2 G + 20) G / 32 (a Horner / recursion step per point,
+// a scan level per doubling of G, spread over the 32 / G lines a warp carries); 0: no
+// variant covers the problem.
 int sep2d64w_chunk(long long n, long long m) {
   const long long L = n > m ? n : m;
-  for (int E : {2, 4, 8})
-    if (32LL * E >= L) return E;
-  return 0;
+  int best = 0;
+  double bc = 0.0;
+  for (int i = 0; i < (int)(sizeof(s64::W_VARS) / sizeof(s64::W_VARS[0])); ++i) {
+    const int G = s64::W_VARS[i].G, E = s64::W_VARS[i].E;
+    if ((long long)G * E < L) continue;
+    int lg = 0;
+    while ((1 << lg) < G) ++lg;
+    const double c = (6.0 * E + 12.0 * lg + 20.0) * G / 32.0;
+    if (!best || c < bc) {
+      best = i + 1;
+      bc = c;
+    }
+  }
+  return best;
 }
 
-static int w_threads(int E) { return E == 8 ? W8NT : 512; }
+void sep2d64w_geom(int var, int* G, int* E) {
+  *G = s64::W_VARS[var - 1].G;
+  *E = s64::W_VARS[var - 1].E;
+}
 
-size_t sep2d64w_workspace(long long n, long long m, int E) {
+size_t sep2d64w_workspace(long long n, long long m, int var) {
+  const int E = s64::W_VARS[var - 1].E;
   const size_t ldn = (size_t)s64::w_ld((int)n, E), ldm = (size_t)s64::w_ld((int)m, E);
   return (4 * (size_t)n * ldm + 3 * (size_t)m * ldn) * sizeof(double);
 }
 
-size_t sep2d64w_smem(long long n, long long m, int E) {
-  return (size_t)2 * (w_threads(E) / 32) * s64::w_sp((int)(n > m ? n : m), E) * sizeof(double);
+// threads for a K5w launch: the fewest warps (>= 4) that reach the smallest number of
+// rounds (RL = warps x 32 / G lines per round) over the two half-passes
+int sep2d64w_threads(long long n, long long m, int var) {
+  const int G = s64::W_VARS[var - 1].G, maxw = s64::W_VARS[var - 1].NT / 32;
+  auto rounds = [&](int nw) {
+    const long long RL = (long long)nw * (32 / G);
+    return (n + RL - 1) / RL + (m + RL - 1) / RL;
+  };
+  const long long best = rounds(maxw);
+  int nw = 4 < maxw ? 4 : maxw;
+  while (nw < maxw && rounds(nw) > best) ++nw;
+  return nw * 32;
 }
 
-const void* sep2d64w_fn(int E) {
-  switch (E) {
-    case 2: return (const void*)&s64::fs1_sep2d64w_kernel<2, 512>;
-    case 4: return (const void*)&s64::fs1_sep2d64w_kernel<4, 512>;
-    case 8: return (const void*)&s64::fs1_sep2d64w_kernel<8, W8NT>;
+size_t sep2d64w_smem(long long n, long long m, int var, int threads) {
+  const int G = s64::W_VARS[var - 1].G, E = s64::W_VARS[var - 1].E;
+  const int RL = threads / 32 * (32 / G);
+  return (size_t)2 * RL * s64::w_sp((int)(n > m ? n : m), E) * sizeof(double);
+}
+
+#define FS1_W_KERNEL(i) s64::fs1_sep2d64w_kernel<s64::W_VARS[i].G, s64::W_VARS[i].E, s64::W_VARS[i].NT>
+
+const void* sep2d64w_fn(int var) {
+  switch (var) {
+    case 1: return (const void*)&FS1_W_KERNEL(0);
+    case 2: return (const void*)&FS1_W_KERNEL(1);
+    case 3: return (const void*)&FS1_W_KERNEL(2);
+    case 4: return (const void*)&FS1_W_KERNEL(3);
+    case 5: return (const void*)&FS1_W_KERNEL(4);
+    case 6: return (const void*)&FS1_W_KERNEL(5);
     default: return nullptr;
   }
 }
 
-cudaError_t launch_sep2d64w(const Sep2d64Params& P, long long batch, int E, cudaStream_t st) {
-  const size_t smem = sep2d64w_smem(P.n, P.m, E);
-  switch (E) {
-    case 2: s64::fs1_sep2d64w_kernel<2, 512><<<(unsigned)batch, 512, smem, st>>>(P); break;
-    case 4: s64::fs1_sep2d64w_kernel<4, 512><<<(unsigned)batch, 512, smem, st>>>(P); break;
-    case 8: s64::fs1_sep2d64w_kernel<8, W8NT><<<(unsigned)batch, W8NT, smem, st>>>(P); break;
+cudaError_t launch_sep2d64w(const Sep2d64Params& P, long long batch, int var, int threads, cudaStream_t st) {
+  const size_t smem = sep2d64w_smem(P.n, P.m, var, threads);
+  const dim3 grid((unsigned)batch), block(threads);
+  switch (var) {
+    case 1: FS1_W_KERNEL(0)<<<grid, block, smem, st>>>(P); break;
+    case 2: FS1_W_KERNEL(1)<<<grid, block, smem, st>>>(P); break;
+    case 3: FS1_W_KERNEL(2)<<<grid, block, smem, st>>>(P); break;
+    case 4: FS1_W_KERNEL(3)<<<grid, block, smem, st>>>(P); break;
+    case 5: FS1_W_KERNEL(4)<<<grid, block, smem, st>>>(P); break;
+    case 6: FS1_W_KERNEL(5)<<<grid, block, smem, st>>>(P); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
