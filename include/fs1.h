@@ -144,7 +144,9 @@ fs1_status fs1_plan(const fs1_desc* desc, int device, fs1_plan_t** out, size_t* 
  *            desc.input_is_log (LOG domain).  Read only.
  *   u, v   : [batch][n*m] out (in, if warm_start): SCALING -> phi, psi;
  *            LOG -> F = log phi, G = log psi.  On return they hold the state
- *            (phi^(l), psi^(l)) at which the loop stopped.
+ *            (phi^(l), psi^(l)) at which the loop stopped;
+ *            the kernels may use them as scratch during the solve, and a NONFINITE
+ *            problem's u, v hold no defined state.
  *   iters  : [batch] int32, l at exit (number of completed iterations).
  *   err    : [batch] fp64, sum_i |psi_i (K^T phi)_i - b_i| evaluated on the exit
  *            state (PAPER.md:148 and §5's termination rule).

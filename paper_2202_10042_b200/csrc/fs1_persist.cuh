@@ -2,8 +2,9 @@
 //
 // One CTA owns one problem (one histogram pair) for the whole solve
 // (Algorithm 1).  Thread t owns the E consecutive grid
-// points [tE, tE+E); phi and psi live in registers, a and b in swizzled shared
-// memory, for all iterations.  Every K x (Eq. 3.1) is evaluated as the paper's
+// points [tE, tE+E); phi and psi live in registers (the 64-point fp32 chunks: one
+// array shared by both, ONE below), a and b in swizzled shared memory, for all
+// iterations.  Every K x (Eq. 3.1) is evaluated as the paper's
 // forward and backward first-order recursions (Eq. "recursion")
 // run as a chunked associative scan of the affine maps y -> lambda^L y + c:
 //   1. per thread: the chunk aggregates f = p at the chunk end and g = t at the
@@ -40,9 +41,29 @@ constexpr int NF_EVERY = 16;
 #ifndef FS1_NEWTON_WARPS
 #define FS1_NEWTON_WARPS 4
 #endif
+#ifndef FS1_ONE
+#define FS1_ONE 1
+#endif
+// resident warps per SM the one-array fp32 variants size their registers for
+#ifndef FS1_ONE_W64
+#define FS1_ONE_W64 12
+#endif
 constexpr int NOSC = FS1_NOSC;  // renormalisation skipped while |kexp| <= NOSC (LOGD)  // non-finite detection interval of multi-warp CTAs
 constexpr int FS1_NONFINITE_FLAG = 2;
 constexpr double LN2 = 0.69314718055994530942;
+
+// ONE: the 64-point fp32 variants hold a single state vector in registers.  A half-step reads
+// x into the array, overwrites it with the forward recursion p and recovers
+// x_k = p_k - lam p_{k-1} in the backward recursion, so phi and psi share one register
+// array (the other one lives only as the next half-step's input).  The vector a
+// check compares against (psi^(l)) and the state a stopping check
+// returns (phi^(l)) are stashed as raw mantissas in the output buffers u, v when a
+// loop top may need them; no third shared array (sK).  Halving the register state
+// raises the resident problems per SM (C5: 4 -> 6 CTAs, smem-bound by a and b).
+// Only the 64-point fp32 chunks use it: the 32-point ones already hold 16 warps per SM
+// with both vectors, and the recovery's extra FMA per point made C2 slower (2.33 ->
+// 2.57 ms; C5 47.3 -> 40.4 ms).
+template <class T, int E> constexpr bool persist_one() { return FS1_ONE && sizeof(T) == 4 && E >= 64; }
 
 template <class T, int E, int WARPS, bool LOGD> struct Persist {
   using Tt = Tr<T>;
@@ -50,14 +71,15 @@ template <class T, int E, int WARPS, bool LOGD> struct Persist {
   static constexpr int VEC = Tt::VEC;
   static constexpr int V = E / VEC;
   static constexpr int NT = 32 * WARPS;
+  static constexpr bool ONE = persist_one<T, E>();
   // fp64 quotient by Newton refinement in the small-CTA variants (latency-bound: one
   // or a few problems), by the correctly rounded reciprocal in the 8-32-warp ones
   static constexpr bool NEWTON = (WARPS <= FS1_NEWTON_WARPS);
   static_assert(E % VEC == 0, "E must be a multiple of the vector width");
 
-  // shared memory layout (bytes)
+  // shared memory layout (bytes): a, b mantissas [, y_old of a check (two-array mode)]
   static constexpr size_t ARR = (size_t)NT * V * sizeof(Vt);
-  static constexpr size_t OFF_XM = 3 * ARR;                          // [2 par][2 dir][WARPS] double
+  static constexpr size_t OFF_XM = (ONE ? 2 : 3) * ARR;              // [2 par][2 dir][WARPS] double
   static constexpr size_t OFF_XE = OFF_XM + 4 * WARPS * sizeof(double);  // [2][2][WARPS] int
   static constexpr size_t OFF_RED = OFF_XE + 4 * WARPS * sizeof(int);    // [2][WARPS] double
   static constexpr size_t OFF_INT = OFF_RED + 2 * WARPS * sizeof(double);  // [2][WARPS] int
@@ -234,7 +256,9 @@ template <class T, int E, int WARPS, bool LOGD> struct Half {
     const int* lpe;
     double* xm;
     int* xi;
+    const T* yold;           // ONE: this chunk's stashed y_old (global) for a check
   };
+  static constexpr bool ONE = PS::ONE;
 
   // Sub-chains of a thread chunk (ILP): the chunk is split into NCH runs of S = E/NCH
   // points whose recursions run interleaved; run c enters with the carry
@@ -259,6 +283,9 @@ template <class T, int E, int WARPS, bool LOGD> struct Half {
     p[0] = cf;
 #pragma unroll
     for (int r = 1; r < NCH; ++r) p[r] = fma(lS, p[r - 1], SLOW ? fq[r - 1] * s : fq[r - 1]);
+    T p0[NCH];  // ONE: p just before each run (recovers the run's first x)
+#pragma unroll
+    for (int r = 0; r < NCH; ++r) p0[r] = p[r];
 #pragma unroll
     for (int e = 0; e < S; ++e) {
 #pragma unroll
@@ -293,7 +320,14 @@ template <class T, int E, int WARPS, bool LOGD> struct Half {
           for (int r = 0; r < NCH; ++r) {
             const int e = r * S + S - 1 - i;
             Tt::unpack(tgt[PS::vidx(c.tid, e / VEC)], tv[r]);
-            if constexpr (CHECK) Tt::unpack(sK[PS::vidx(c.tid, e / VEC)], yo[r]);
+            if constexpr (CHECK && !ONE) Tt::unpack(sK[PS::vidx(c.tid, e / VEC)], yo[r]);
+            if constexpr (CHECK && ONE) {
+#pragma unroll
+              for (int q = 0; q < VEC; ++q) {
+                const int eq = (e / VEC) * VEC + q;
+                yo[r][q] = (!MASK || eq < c.nv) ? c.yold[eq] : T(0);
+              }
+            }
           }
         }
         T kx[NCH];
@@ -302,7 +336,13 @@ template <class T, int E, int WARPS, bool LOGD> struct Half {
           const int r = NCH - 1 - rr;
           const int e = r * S + S - 1 - i;
           kx[r] = fma(lam, t[r], y[e]);
-          t[r] = fma(lam, t[r], xs(e));
+          if constexpr (ONE) {
+            // x_e = p_e - lam p_{e-1}: y[e - 1] still holds p (written after this read)
+            const T pm = (i == S - 1) ? p0[r] : y[e - 1];
+            t[r] = fma(lam, t[r], fma(-lam, pm, y[e]));
+          } else {
+            t[r] = fma(lam, t[r], xs(e));
+          }
         }
 #pragma unroll
         for (int r = 0; r < NCH; ++r) {
@@ -417,7 +457,7 @@ template <class T, int E, int WARPS, bool LOGD> struct Half {
       cb = (T)er_rel(CB, R);
     }
 
-    if constexpr (CHECK) PS::sts(sK, c.tid, y);  // keep y_old
+    if constexpr (CHECK && !ONE) PS::sts(sK, c.tid, y);  // keep y_old (ONE: stashed already)
     double errp;
     int kexp;
     if (!LOGD || !slow) errp = passes<CHECK, MASK, false>(c, x, y, ye, tgt, te, sK, cf, cb, s, fq, gq, R, kexp);
@@ -456,6 +496,20 @@ template <class T, int E, int WARPS, bool LOGD> struct Half {
     PS::lds(sK, c.tid, y);
   }
 };
+
+// ONE: raw mantissas of one thread chunk to / from a global stash (rare: loop tops
+// that may check; same thread writes and reads)
+template <class T, int E>
+__device__ __forceinline__ void stash_store(T* g, int nv, const T (&x)[E]) {
+#pragma unroll
+  for (int e = 0; e < E; ++e)
+    if (e < nv) g[e] = x[e];
+}
+template <class T, int E>
+__device__ __forceinline__ void stash_load(const T* g, int nv, T (&x)[E]) {
+#pragma unroll
+  for (int e = 0; e < E; ++e) x[e] = (e < nv) ? g[e] : T(0);
+}
 
 
 // ---------------------------------------------------------------------------------------
@@ -628,9 +682,165 @@ __device__ double cost_pass(const PersistParams& P, const typename Tr<T>::V* sx,
 // ---------------------------------------------------------------------------------------
 // resident CTAs the register budget is sized for: 16 warps per SM, 8 when the chunk
 // state (2 E values of T per thread) needs more than 128 registers
+// (ONE: one E-vector per thread; 12 warps, the bound the shared a, b of N = 4096 set)
 template <class T, int E, int WARPS> constexpr int persist_minb() {
-  const int warps = (sizeof(T) * E >= 256) ? 8 : 16;
+  const int warps = persist_one<T, E>() ? FS1_ONE_W64 : ((sizeof(T) * E >= 256) ? 8 : 16);
   return warps / WARPS > 0 ? warps / WARPS : 1;
+}
+
+// The solve of the one-array variants (ONE): Algorithm 1 with a
+// single register array A that holds phi between half-steps and psi inside an
+// iteration.  u, v double as the stashes of phi^(l) and psi^(l) (raw mantissas, same
+// thread) for the loop tops that may check; the results overwrite them at the end.
+template <class T, int E, int WARPS, bool LOGD>
+__device__ __forceinline__ void persist_solve_one(const PersistParams& P, typename Half<T, E, WARPS, LOGD>::Ctx& c,
+                                                  typename Tr<T>::V* sA, typename Tr<T>::V* sB, double* xm,
+                                                  int* xi, double* red, int* ired, long long base, long long g0,
+                                                  bool full) {
+  using PS = Persist<T, E, WARPS, LOGD>;
+  using H = Half<T, E, WARPS, LOGD>;
+  const long long n = P.n;
+  const long long pid = blockIdx.x;
+  T* const ug = reinterpret_cast<T*>(P.u) + base;
+  T* const vg = reinterpret_cast<T*>(P.v) + base;
+  T* const su = ug + g0;  // stash of phi^(l)
+  T* const sv = vg + g0;  // stash of psi^(l)
+  T A[E];
+  int ae, be, pe = 0, qe = 0;
+  double err = NAN, cost = NAN;
+  int l = 0, flag = 0, par = 0;
+  int ue = 0, ve = 0;  // exponents of the stashed phi, psi
+  // fs1_cost (write_uv = 0): the loop top l = itr_max = 0 on the given state, u and v
+  // untouched: the return line only (err is not reported)
+  const bool cost_only = !P.write_uv;
+  if (cost_only) {
+    load_chunk<T, E, LOGD>(ug, n, g0, c.nv, LOGD, A, ue);
+    PS::sts(sA, c.tid, A);
+    load_chunk<T, E, LOGD>(vg, n, g0, c.nv, LOGD, A, ve);
+    PS::sts(sB, c.tid, A);
+    flag = 4;
+  } else {
+    load_chunk<T, E, LOGD>(reinterpret_cast<const T*>(P.a) + base, n, g0, c.nv, P.input_is_log, A, ae);
+    PS::sts(sA, c.tid, A);
+    load_chunk<T, E, LOGD>(reinterpret_cast<const T*>(P.b) + base, n, g0, c.nv, P.input_is_log, A, be);
+    PS::sts(sB, c.tid, A);
+    // ---- initial scalings or the caller's: psi^(0) to its stash (the first
+    // loop top may check on it), phi^(0) into A
+    if (P.warm) {
+      load_chunk<T, E, LOGD>(vg, n, g0, c.nv, LOGD, A, qe);
+      stash_store<T, E>(sv, c.nv, A);
+      load_chunk<T, E, LOGD>(ug, n, g0, c.nv, LOGD, A, pe);
+    } else {
+      const double inv = 1.0 / (double)n;
+      T m0;
+      int e0;
+      if constexpr (LOGD) { m0 = (T)Tr<double>::mant(inv); e0 = Tr<double>::expo(inv); }
+      else { m0 = (T)inv; e0 = 0; }
+#pragma unroll
+      for (int e = 0; e < E; ++e) A[e] = (e < c.nv) ? m0 : T(0);
+      pe = qe = e0;
+      stash_store<T, E>(sv, c.nv, A);
+    }
+    ue = pe;
+    ve = qe;
+    c.yold = sv;
+    __syncthreads();
+
+    int firstbad = 0x7fffffff;
+    const int itr_max = P.itr_max;
+    const bool use_tol = P.tol > 0.0;
+    const int ci = P.check_interval;
+    // (captures by value: a reference capture would take the kernel parameter's address
+    // and move it to local memory)
+    auto is_check = [=](int k) { return (k >= itr_max) || (use_tol && (k % ci) == 0); };
+    while (true) {
+      const bool check = is_check(l);
+      T accx = T(0), accy = T(0);
+      int R, kx;
+      if (check) {
+        // line 2: err = sum |psi^(l) (K^T phi^(l)) - b|; phi^(l) stashed first (a stop returns it)
+        stash_store<T, E>(su, c.nv, A);
+        ue = pe;
+        double ep = full ? H::template run<true, false>(c, P, A, pe, A, ve, sB, be, nullptr, par, accx, R, kx)
+                         : H::template run<true, true>(c, P, A, pe, A, ve, sB, be, nullptr, par, accx, R, kx);
+        par ^= 1;
+        if (!isfinite((double)accx)) firstbad = min(firstbad, l);
+        err = PS::block_sum(ep, red, par, c.lane, c.warp);
+        int fb;
+        if constexpr (WARPS > 1) fb = PS::block_min(firstbad, ired, par, c.lane, c.warp);
+        else fb = warp_min(firstbad);
+        if (fb != 0x7fffffff) { l = fb; flag = FS1_NONFINITE_FLAG; break; }
+        if (l >= itr_max || err <= P.tol) {
+          flag = (use_tol && err <= P.tol) ? 1 : 4;
+          break;
+        }
+        if (full) H::template finish<false>(c, A, qe, sB, be, R, kx);
+        else H::template finish<true>(c, A, qe, sB, be, R, kx);
+      } else {
+        // lines 3-7: psi = b ./ (K^T phi)
+        if (full) H::template run<false, false>(c, P, A, pe, A, qe, sB, be, nullptr, par, accx, R, kx);
+        else H::template run<false, true>(c, P, A, pe, A, qe, sB, be, nullptr, par, accx, R, kx);
+        par ^= 1;
+      }
+      if (is_check(l + 1)) {  // the next loop top compares against psi^(l+1)
+        stash_store<T, E>(sv, c.nv, A);
+        ve = qe;
+      }
+      // lines 8-12: phi = a ./ (K psi)
+      if (full) H::template run<false, false>(c, P, A, qe, A, pe, sA, ae, nullptr, par, accy, R, kx);
+      else H::template run<false, true>(c, P, A, qe, A, pe, sA, ae, nullptr, par, accy, R, kx);
+      par ^= 1;
+      if (!isfinite((double)accx)) firstbad = min(firstbad, l);
+      else if (!isfinite((double)accy)) firstbad = min(firstbad, l + 1);
+      ++l;  // line 13
+      if constexpr (WARPS == 1) {
+        if (__any_sync(FULL, firstbad != 0x7fffffff)) {
+          l = warp_min(firstbad);
+          flag = FS1_NONFINITE_FLAG;
+          break;
+        }
+      } else {
+        if ((l % NF_EVERY) == 0) {
+          par ^= 1;
+          const int fb = PS::block_min(firstbad, ired, par, c.lane, c.warp);
+          if (fb != 0x7fffffff) { l = fb; flag = FS1_NONFINITE_FLAG; break; }
+        }
+      }
+    }
+
+  }  // !cost_only
+
+  // ---- outputs: the state of the stopping loop top from the stashes
+  if (flag != FS1_NONFINITE_FLAG) {
+    par ^= 1;
+    __syncthreads();  // a, b are no longer needed: their shared arrays take phi, psi
+    if (!cost_only) {
+      stash_load<T, E>(su, c.nv, A);
+      PS::sts(sA, c.tid, A);
+      stash_load<T, E>(sv, c.nv, A);
+      PS::sts(sB, c.tid, A);
+    }
+    const double cp = cost_pass<T, E, WARPS, LOGD>(P, sA, ue, sB, ve, c.tid, c.lane, c.warp, xm, xi);
+    cost = PS::block_sum(cp, red, par, c.lane, c.warp);
+    if (!cost_only) {
+      PS::lds(sA, c.tid, A);
+      store_chunk<T, E, LOGD>(ug, g0, c.nv, A, ue);
+      PS::lds(sB, c.tid, A);
+      store_chunk<T, E, LOGD>(vg, g0, c.nv, A, ve);
+    }
+  } else {
+    err = NAN;
+    store_chunk<T, E, LOGD>(ug, g0, c.nv, A, pe);  // the non-finite state; v holds no result
+#pragma unroll
+    for (int e = 0; e < E; ++e)
+      if (e < c.nv) sv[e] = (T)NAN;
+  }
+  if (c.tid == 0) {
+    if (P.iters) P.iters[pid] = l;
+    if (P.err) P.err[pid] = err;
+    if (P.flags) P.flags[pid] = flag;
+    if (P.cost) P.cost[pid] = cost;
+  }
 }
 
 template <class T, int E, int WARPS, bool LOGD>
@@ -683,6 +893,10 @@ __global__ void __launch_bounds__(32 * WARPS, (persist_minb<T, E, WARPS>())) fs1
   }
   // warp-uniform: the masked and unmasked paths contain different barriers
   const bool full = __all_sync(FULL, c.nv == E);
+  if constexpr (PS::ONE) {
+    persist_solve_one<T, E, WARPS, LOGD>(P, c, sA, sB, xm, xi, red, ired, base, g0, full);
+    return;
+  }
 
   // ---- inputs into shared memory (mantissas) and registers (chunk exponents)
   T phi[E], psi[E];
