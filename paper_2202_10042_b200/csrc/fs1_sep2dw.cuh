@@ -48,6 +48,9 @@
 namespace fs1 {
 namespace sepw {
 
+#ifndef FS1_K3W_LATE_TMA
+#define FS1_K3W_LATE_TMA 1
+#endif
 constexpr int W = 8;        // warps = lines per CTA group
 constexpr int NT = 32 * W;
 constexpr int LIMF = 60;    // carries up to 2^60 above a chunk keep its exponent
@@ -280,16 +283,24 @@ __device__ __forceinline__ void fused_pass(sep::Ctx& c, WarpIO& io, const AxT& T
     float A[E];
     if (line < nlines) {
       const size_t off = (size_t)line * C::LP;
-      if ((MODE & UPD) && lane == 0) {
-        stm::fence_async_smem();
-        stm::mbar_expect_tx(&io.mb[1], (unsigned)C::LINEB);
-        stm::bulk_g2s(io.ts, TM + off, (unsigned)C::LINEB, &io.mb[1]);
-      }
+      // the target line arrives by TMA; issued once this warp's X line has landed, so the
+      // two 16 MB bursts of a pass (every warp's X, then every warp's target) share L2
+      // bandwidth with the first apply instead of with each other
+      auto issue_target = [&]() {
+        if ((MODE & UPD) && lane == 0) {
+          stm::fence_async_smem();
+          stm::mbar_expect_tx(&io.mb[1], (unsigned)C::LINEB);
+          stm::bulk_g2s(io.ts, TM + off, (unsigned)C::LINEB, &io.mb[1]);
+        }
+      };
+      if (!FS1_K3W_LATE_TMA) issue_target();
       load_line<E>(X + off, lane, A);  // E/8 coalesced 256-bit loads, all in flight at once
       if (t) t[1] = stm::gtimer() + (A[0] == 12345.f);
       int oe2 = 0;
       if (MODE & UPD) {
-        const int R = line_apply<E>(A, T, lane);
+        const int oe1 = prep_log<E>(A);
+        if (FS1_K3W_LATE_TMA) issue_target();
+        const int R = line_apply_lin<E>(A, oe1, T, lane);
         if (t) t[2] = stm::gtimer() + (R == 12345);
         const int tx = TX[(size_t)line * 32 + lane];
         oe2 = (tx == ZE) ? ZE : tx - R;
