@@ -48,6 +48,11 @@
 namespace fs1 {
 namespace sepw {
 
+// per-phase timestamps of pass R at iteration 5 (tools/phase_sep.py) only in probe builds
+// (tools/variant.sh probe -DFS1_K3W_PROBE=1)
+#ifndef FS1_K3W_PROBE
+#define FS1_K3W_PROBE 0
+#endif
 #ifndef FS1_K3W_LATE_TMA
 #define FS1_K3W_LATE_TMA 1
 #endif
@@ -277,7 +282,7 @@ __device__ __forceinline__ void fused_pass(sep::Ctx& c, WarpIO& io, const AxT& T
   float* stage = c.s.stage;
   int gi = 0;
   for (int grp = c.r; grp < ngroups; grp += G, ++gi) {
-    unsigned long long* t = (td && lane == 0 && gi < 2) ? td + (((size_t)c.r * W + w) * 2 + gi) * 8 : nullptr;
+    unsigned long long* t = (FS1_K3W_PROBE && td && lane == 0 && gi < 2) ? td + (((size_t)c.r * W + w) * 2 + gi) * 8 : nullptr;
     if (t) t[0] = stm::gtimer();
     const int line = grp * W + w;
     float A[E];

@@ -311,3 +311,80 @@ def test_log_fp32_renormalisation_skip_and_apply(spread):
     ref = sinkhorn.solve(A.astype(np.float64), B.astype(np.float64), n=n, h1=1 / n, eps=eps, itr_max=60,
                          domain="log", input_is_log=True, apply="recur")
     assert_solve_parity(out, ref, "log", "f32")
+
+
+# ------------------------------------------------------------------ one-array variant (ONE)
+# The 64-point fp32 chunks keep one state vector in registers and stash phi^(l), psi^(l)
+# in u, v for the loop tops that may check (fs1_persist.cuh).
+ONE_N = [(2000, "persist_f32_log_E64_W1"), (3000, "persist_f32_log_E64_W2"), (7000, "persist_f32_log_E64_W4")]
+
+
+def _one_kernel(n, eps, itr, **kw):
+    spec = fs1.Spec(ndim=1, n=n, m=1, h1=1 / n, h2=0.0, eps=eps, batch=2, dtype=torch.float32, domain="log",
+                    itr_max=itr, **kw)
+    return fs1.plan(spec, 0).info()["kernel"]
+
+
+@pytest.mark.parametrize("n,kern", ONE_N)
+def test_one_array_tolerance_stop(n, kern):
+    """tol > 0 with check_interval 7: every loop top l % 7 == 0 compares psi^(l) (stashed at
+    the previous phi half-step) and may return phi^(l) (stashed before the check).  The
+    GPU's stop lands within one interval of the oracle's (fp32 vs fp64 err near tol), and
+    its returned state equals the oracle's fixed-iteration replay at that l."""
+    eps, ci = 0.002, 7
+    A, B = gi.batch("c5", range(2), n=n)
+    ag, bg = _cuda(A, "f32"), _cuda(B, "f32")
+    A64, B64 = ag.double().cpu().numpy(), bg.double().cpu().numpy()
+    # tol: the larger err of the pair at l = 56 (both stop by about 8 check intervals)
+    r56 = sinkhorn.solve(A64, B64, n=n, h1=1 / n, eps=eps, itr_max=56, domain="log", apply="recur")
+    tol = float(np.max(r56["err"])) * (1 + 1e-3)
+    assert _one_kernel(n, eps, 3000, tol=tol, check_interval=ci) == kern
+    out = fs1.solve(ag, bg, h=1 / n, eps=eps, itr_max=3000, tol=tol, check_interval=ci, domain="log")
+    ref = sinkhorn.solve(A64, B64, n=n, h1=1 / n, eps=eps, itr_max=3000, tol=tol, check_interval=ci,
+                         domain="log", apply="recur")
+    it = out["iters"].cpu().numpy()
+    assert np.all(out["flags"].cpu().numpy() == 1) and np.all(it % ci == 0)
+    assert np.all(np.abs(it - ref["iters"]) <= ci), (it, ref["iters"])
+    for p in range(2):
+        rp = sinkhorn.solve(A64[p:p + 1], B64[p:p + 1], n=n, h1=1 / n, eps=eps, itr_max=int(it[p]), domain="log",
+                            apply="recur")
+        sub = {k: v[p:p + 1] for k, v in out.items()}
+        sub["flags"] = torch.full_like(sub["flags"], 4)  # the replay stops at itr_max
+        assert_solve_parity(sub, rp, "log", "f32")
+        assert out["err"][p].item() <= tol
+
+
+@pytest.mark.parametrize("n,kern", ONE_N[:2])
+def test_one_array_warm_start_and_cost(n, kern):
+    """solve(12) then solve(18, warm) == solve(30) (fp32 rounding), and fs1_cost on the
+    result (the write_uv = 0 path) equals the fused cost and leaves u, v untouched."""
+    eps = 0.002
+    A, B = gi.batch("c5", range(2), n=n)
+    assert _one_kernel(n, eps, 30) == kern
+    ag, bg = _cuda(A, "f32"), _cuda(B, "f32")
+    full = fs1.solve(ag, bg, h=1 / n, eps=eps, itr_max=30, domain="log")
+    h1 = fs1.solve(ag, bg, h=1 / n, eps=eps, itr_max=12, domain="log")
+    h2 = fs1.solve(ag, bg, h=1 / n, eps=eps, itr_max=18, domain="log", u0=h1["u"], v0=h1["v"])
+    assert rel_norm(h2["u"].double().cpu().numpy(), full["u"].double().cpu().numpy()) <= 1e-5
+    assert rel_norm(h2["v"].double().cpu().numpy(), full["v"].double().cpu().numpy()) <= 1e-5
+    u0, v0 = full["u"].clone(), full["v"].clone()
+    c = fs1.cost(full["u"], full["v"], h=1 / n, eps=eps, domain="log")
+    assert torch.equal(full["u"], u0) and torch.equal(full["v"], v0)
+    np.testing.assert_allclose(c.cpu().numpy(), full["cost"].cpu().numpy(), rtol=1e-6)
+
+
+def test_one_array_nonfinite_weight():
+    """A +inf log-weight of a poisons its problem: phi^(1) = a / K psi^(1) is the first
+    non-finite state, so the problem stops NONFINITE with l = 1; the other
+    problem of the batch is unaffected and equals its single-problem solve bitwise."""
+    n, eps = 3000, 0.002
+    A, B = gi.batch("c5", range(2), n=n)
+    la, lb = np.log(A), np.log(B)
+    la[1, 1234] = np.inf
+    ag, bg = _cuda(la, "f32"), _cuda(lb, "f32")
+    out = fs1.solve(ag, bg, h=1 / n, eps=eps, itr_max=40, domain="log", input_is_log=True)
+    assert out["flags"][1].item() == 2 and out["iters"][1].item() == 1
+    one = fs1.solve(ag[:1].contiguous(), bg[:1].contiguous(), h=1 / n, eps=eps, itr_max=40, domain="log",
+                    input_is_log=True)
+    assert out["flags"][0].item() == 4 and torch.equal(out["u"][0], one["u"][0])
+    assert torch.equal(out["cost"][:1], one["cost"])

@@ -1,4 +1,6 @@
-"""Per-phase timing of the K3w pass R at iteration 5 on C4 (globaltimer stamps per warp)."""
+"""Per-phase timing of the K3w pass R at iteration 5 on C4 (globaltimer stamps per warp).
+The stamps are compiled in only in probe builds: bash tools/variant.sh probe -DFS1_K3W_PROBE=1,
+then run with FS1_LIB=gpurun_var/lib_probe.so."""
 import sys, os, ctypes
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
