@@ -63,7 +63,13 @@ constexpr double LN2 = 0.69314718055994530942;
 // Only the 64-point fp32 chunks use it: the 32-point ones already hold 16 warps per SM
 // with both vectors, and the recovery's extra FMA per point made C2 slower (2.33 ->
 // 2.57 ms; C5 47.3 -> 40.4 ms).
-template <class T, int E> constexpr bool persist_one() { return FS1_ONE && sizeof(T) == 4 && E >= 64; }
+#ifndef FS1_ONE_MINE
+#define FS1_ONE_MINE 64
+#endif
+#ifndef FS1_ONE_W32
+#define FS1_ONE_W32 28
+#endif
+template <class T, int E> constexpr bool persist_one() { return FS1_ONE && sizeof(T) == 4 && E >= FS1_ONE_MINE; }
 
 template <class T, int E, int WARPS, bool LOGD> struct Persist {
   using Tt = Tr<T>;
@@ -684,7 +690,8 @@ __device__ double cost_pass(const PersistParams& P, const typename Tr<T>::V* sx,
 // state (2 E values of T per thread) needs more than 128 registers
 // (ONE: one E-vector per thread; 12 warps, the bound the shared a, b of N = 4096 set)
 template <class T, int E, int WARPS> constexpr int persist_minb() {
-  const int warps = persist_one<T, E>() ? FS1_ONE_W64 : ((sizeof(T) * E >= 256) ? 8 : 16);
+  const int warps = persist_one<T, E>() ? (E >= 64 ? FS1_ONE_W64 : E >= 32 ? FS1_ONE_W32 : 16)
+                                       : ((sizeof(T) * E >= 256) ? 8 : 16);
   return warps / WARPS > 0 ? warps / WARPS : 1;
 }
 
