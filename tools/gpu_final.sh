@@ -9,8 +9,9 @@ if [ -z "$NOTEST" ]; then
   tail -3 $O/pytest_gpu.log
 fi
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/smoke.log
+timeout 600 python tools/golden_errors.py > $O/golden_errors.txt 2>&1
 timeout 600 python bench.py > $O/bench_default.json 2> $O/bench_default.err
-for c in ${CFGS:-c1 c2 c4 c5 e1_8000 e2_8000 e2s_8000 e3_160}; do
+for c in ${CFGS:-c1 c2 c4 c5 e1_8000 e2_8000 e2s_8000 e3_160 e3_80}; do
   timeout 600 python bench.py --config $c --steps 5 --warmup 3 > $O/bench_$c.json 2> $O/bench_$c.err
 done
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > $O/bench_ref.json 2> $O/bench_ref.err
@@ -20,7 +21,7 @@ for c in ${LCFGS:-c3 c2 c4 c5}; do
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_$c.csv \
     python bench.py --config $c --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > $O/ncu_launch_$c.log 2>&1
 done
-for spec in ${PCFGS:-"c3 fs1_stream_kernel" "c4 fs1_sep2dw" "c5 fs1_persist_solve" "c2 fs1_persist_solve"}; do
+for spec in ${PCFGS:-"c3 fs1_stream_kernel" "c4 fs1_sep2dw" "c5 fs1_persist_solve" "c2 fs1_persist_solve" "e3_160 fs1_sep2d64w"}; do
   set -- $spec
   timeout 1200 ncu --set full --clock-control none --import-source on -k regex:$2 -s 1 -c 1 -o $O/prof_$1 -f \
     python bench.py --config $1 --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > $O/ncu_full_$1.log 2>&1
