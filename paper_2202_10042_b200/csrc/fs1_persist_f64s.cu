@@ -11,9 +11,6 @@ static const PersistEntry kTable[] = {
     FS1_PERSIST_ENTRY(double, 1, 8, 4, false),
     FS1_PERSIST_ENTRY(double, 1, 8, 16, false),
     FS1_PERSIST_ENTRY(double, 1, 16, 16, false),
-    FS1_PERSIST_ENTRY(double, 1, 2, 32, false),
-    FS1_PERSIST_ENTRY(double, 1, 4, 32, false),
-    FS1_PERSIST_ENTRY(double, 1, 8, 32, false),
 };
 const PersistEntry* persist_table_f64s(int* count) {
   *count = (int)(sizeof(kTable) / sizeof(kTable[0]));
