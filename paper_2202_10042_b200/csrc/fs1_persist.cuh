@@ -63,6 +63,11 @@ constexpr double LN2 = 0.69314718055994530942;
 // Only the 64-point fp32 chunks use it: the 32-point ones already hold 16 warps per SM
 // with both vectors, and the recovery's extra FMA per point made C2 slower (2.33 ->
 // 2.57 ms; C5 47.3 -> 40.4 ms).
+// the guarded renormalisation skip also in the one-array 64-point chunks: measured
+// slower (C5 39.6 -> 42.3 ms: the second copy of the backward loop), off
+#ifndef FS1_SKIP64
+#define FS1_SKIP64 0
+#endif
 #ifndef FS1_ONE_MINE
 #define FS1_ONE_MINE 64
 #endif
@@ -226,8 +231,10 @@ template <class T, int E, int WARPS, bool LOGD> struct Persist {
 #pragma unroll
       for (int w = WARPS - 1; w >= 0; --w)
         if (w > warp) CG = er_add(er_mul(CG, LW), ER<double>{wgm[w], wge[w]});
-      cf = er_add(cf, er_mul(CF, lP));
-      cb = er_add(cb, er_mul(CG, rP));
+      // warp-uniform skips of the zero contributions (warp 0 has no warp to its left,
+      // the last none to its right): bit-identical, adding an ER zero returns cf / cb
+      if (warp > 0) cf = er_add(cf, er_mul(CF, lP));
+      if (warp < WARPS - 1) cb = er_add(cb, er_mul(CG, rP));
     }
   }
   // the same with the lane powers read from a lane-indexed shared table where they are
@@ -367,7 +374,7 @@ template <class T, int E, int WARPS, bool LOGD> struct Half {
         }
       }
     };
-    if constexpr (LOGD && !CHECK && sizeof(T) * E <= 128) {
+    if constexpr (LOGD && !CHECK && (sizeof(T) * E <= 128 || (FS1_SKIP64 && ONE))) {
       // (only for chunks whose two state vectors leave registers to spare: the second
       // copy of the loop costs the 64-element float variant more than it saves)
       // The renormalisation is an exact power of two: skip its multiply when every chunk
