@@ -183,6 +183,23 @@ fs1_status fs1_apply(const fs1_plan_t* plan, const void* x, void* y, void* works
 #define FS1_MAX_TPLAN 8192
 fs1_status fs1_transport_plan(const fs1_plan_t* plan, const void* u, const void* v, void* gamma, void* stream);
 
+/* fs1_plan_entries — individual entries of the transport plan gamma = diag(phi) K diag(psi)
+ * (gamma_ij = e^{-1/2-alpha_i/eps} K_ij e^{-1/2-beta_j/eps}; SPEC's
+ * plan_entry) at caller-given index triples, for problems of any size and dimension
+ * (no FS1_MAX_TPLAN limit: nothing N^2 is formed):
+ *   gamma = exp(F_k + G_l - dist(k, l) / eps) in fp64, dist the l1 grid distance
+ *   (1D h1 |k - l|; 2D / 3D per axis of the column-major flat indices (z m + j) n + i,
+ *   weighted by h1, h2, h3); SCALING: F = log phi, G = log psi (phi_k = 0 or psi_l = 0
+ *   gives 0); LOG / STABILIZED: u, v hold F, G.
+ *   u, v  : [batch][size] state as fs1_solve returns it (device, plan dtype).
+ *   idx   : [count][3] int64 (problem p, source flat index k, target flat index l), device.
+ *   out   : [count] fp64, device, caller-owned.  count may be 0.
+ * Errors: FS1_ERR_ARG (NULL plan, or NULL pointers with count > 0, or count < 0).  A
+ * triple outside [0, batch) x [0, size)^2 writes NaN to its slot (not an error code:
+ * the entries are computed asynchronously on `stream`).                            */
+fs1_status fs1_plan_entries(const fs1_plan_t* plan, const void* u, const void* v, const int64_t* idx,
+                            long long count, double* out, void* stream);
+
 /* fs1_dual — the dual objective of the entropic problem Eq. (2.3) at the
  * state (u, v) as fs1_solve returns it:
  *   D = eps (sum_k a_k F_k + sum_l b_l G_l - sum_kl gamma_kl) + eps (sum a + sum b) / 2,

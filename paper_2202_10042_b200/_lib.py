@@ -16,7 +16,7 @@ FS1_F32, FS1_F64 = 0, 1
 FS1_SCALING, FS1_LOG, FS1_STABILIZED = 0, 1, 2
 FLAG_CONVERGED, FLAG_NONFINITE, FLAG_ITR_MAX = 1, 2, 4
 
-EXPORTS = ["fs1_plan", "fs1_solve", "fs1_cost", "fs1_apply", "fs1_transport_plan", "fs1_dual",
+EXPORTS = ["fs1_plan", "fs1_solve", "fs1_cost", "fs1_apply", "fs1_transport_plan", "fs1_plan_entries", "fs1_dual",
            "fs1_eps_scaling_plan", "fs1_solve_eps_scaling", "fs1_plan_info",
            "fs1_plan_destroy", "fs1_status_string", "fs1_abi_version",
            # include/fs1_shard.h
@@ -88,6 +88,8 @@ def lib():
         L.fs1_apply.restype = st
         L.fs1_transport_plan.argtypes = [vp] * 5
         L.fs1_transport_plan.restype = st
+        L.fs1_plan_entries.argtypes = [vp, vp, vp, vp, ctypes.c_longlong, vp, vp]
+        L.fs1_plan_entries.restype = st
         L.fs1_dual.argtypes = [vp] * 9
         L.fs1_dual.restype = st
         dd = ctypes.c_double

@@ -817,6 +817,19 @@ fs1_status fs1_transport_plan(const fs1_plan_t* plan, const void* u, const void*
   return e == cudaSuccess ? FS1_OK : FS1_ERR_CUDA;
 }
 
+fs1_status fs1_plan_entries(const fs1_plan_t* plan, const void* u, const void* v, const int64_t* idx,
+                            long long count, double* out, void* stream) {
+  if (!plan || count < 0) return FS1_ERR_ARG;
+  if (count == 0) return FS1_OK;
+  if (!u || !v || !idx || !out) return FS1_ERR_ARG;
+  const fs1_desc& d = plan->d;
+  const double c1 = d.h1 / d.eps, c2 = d.ndim >= 2 ? d.h2 / d.eps : 0.0, c3 = d.ndim == 3 ? d.h3 / d.eps : 0.0;
+  const long long l = d.ndim == 3 ? d.l : 1;
+  const cudaError_t e = launch_entries(d.dtype == FS1_F64 ? 1 : 0, u, v, (const long long*)idx, count, out, d.batch,
+                                       d.n, d.m, l, c1, c2, c3, d.domain != FS1_SCALING ? 1 : 0, (cudaStream_t)stream);
+  return e == cudaSuccess ? FS1_OK : FS1_ERR_CUDA;
+}
+
 fs1_status fs1_apply(const fs1_plan_t* plan, const void* x, void* y, void* workspace, void* stream) {
   if (!plan || !x || !y || x == y) return FS1_ERR_ARG;
   if (plan->ws && (!workspace || ((uintptr_t)workspace & 255))) return FS1_ERR_WORKSPACE;

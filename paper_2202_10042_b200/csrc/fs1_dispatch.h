@@ -79,5 +79,8 @@ cudaError_t launch_rescale(int dtype, void* u, void* v, long long count, double 
 // transport-plan materialisation (fs1_tplan.cu)
 cudaError_t launch_tplan(int dtype, const void* u, const void* v, void* g, long long batch, long long n, long long m,
                          double c1, double c2, int logd, cudaStream_t st);
+cudaError_t launch_entries(int dtype, const void* u, const void* v, const long long* idx, long long count,
+                           double* out, long long batch, long long n, long long m, long long l, double c1, double c2,
+                           double c3, int logd, cudaStream_t st);
 
 }  // namespace fs1

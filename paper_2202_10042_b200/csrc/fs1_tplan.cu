@@ -7,6 +7,7 @@
 //              underflows alone, Remark 3.3)
 // in fp64 and rounded once to the plan dtype.  1D index (i, j); 2D problems use the
 // column-major flat index k = j2 n + i2 on both sides and the l1 distance.
+// k_entries: single entries at index triples for problems of any size (fs1_plan_entries).
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -45,6 +46,47 @@ cudaError_t launch_tplan(int dtype, const void* u, const void* v, void* g, long 
   else
     k_tplan<double><<<(unsigned)blocks, threads, 0, st>>>((const double*)u, (const double*)v, (double*)g, batch, n, m,
                                                           c1, c2, logd);
+  return cudaGetLastError();
+}
+
+// Entries at index triples (fs1_plan_entries): one thread per triple, the same formula
+// for any size and dimension (3D: flat index (z m + j) n + i), fp64 output; a triple
+// outside the ranges gives NaN.
+template <class T>
+__global__ void k_entries(const T* u, const T* v, const long long* idx, long long count, double* out,
+                          long long batch, long long n, long long m, long long l, double c1, double c2, double c3,
+                          int logd) {
+  const long long size = n * m * l;
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < count;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long p = idx[3 * t], k = idx[3 * t + 1], q = idx[3 * t + 2];
+    if (p < 0 || p >= batch || k < 0 || k >= size || q < 0 || q >= size) {
+      out[t] = NAN;
+      continue;
+    }
+    const long long ki = k % n, kj = (k / n) % m, kz = k / (n * m);
+    const long long qi = q % n, qj = (q / n) % m, qz = q / (n * m);
+    const double d = c1 * (double)llabs(ki - qi) + c2 * (double)llabs(kj - qj) + c3 * (double)llabs(kz - qz);
+    const double a = (double)u[p * size + k], b = (double)v[p * size + q];
+    double val;
+    if (logd) val = exp(a + b - d);
+    else val = (a > 0.0 && b > 0.0) ? exp(log(a) + log(b) - d) : 0.0;
+    out[t] = val;
+  }
+}
+
+cudaError_t launch_entries(int dtype, const void* u, const void* v, const long long* idx, long long count,
+                           double* out, long long batch, long long n, long long m, long long l, double c1, double c2,
+                           double c3, int logd, cudaStream_t st) {
+  if (count == 0) return cudaSuccess;
+  const int threads = 256;
+  const long long blocks = std::min<long long>((count + threads - 1) / threads, 148LL * 16);
+  if (dtype == 0)
+    k_entries<float><<<(unsigned)blocks, threads, 0, st>>>((const float*)u, (const float*)v, idx, count, out, batch,
+                                                           n, m, l, c1, c2, c3, logd);
+  else
+    k_entries<double><<<(unsigned)blocks, threads, 0, st>>>((const double*)u, (const double*)v, idx, count, out,
+                                                            batch, n, m, l, c1, c2, c3, logd);
   return cudaGetLastError();
 }
 

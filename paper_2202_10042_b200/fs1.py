@@ -250,6 +250,27 @@ def transport_plan(u, v, *, h, eps, domain="scaling", shape=None, h2=None):
     return g
 
 
+def plan_entries(u, v, idx, *, h, eps, domain="scaling", shape=None, h2=None, h3=None):
+    """gamma_kl of the transport plan at index triples idx = [count, 3] int64 (problem,
+    source flat index, target flat index) for problems of any size: [count] fp64
+    (fs1_plan_entries; NaN for a triple out of range)."""
+    dev = u.device.index
+    size = _geom(u, shape, h, h2, h3)[4]
+    _check(u, "u", u.dtype, dev, size)
+    _check(v, "v", u.dtype, dev, size, u.numel())
+    if idx.dtype != torch.int64 or idx.dim() != 2 or idx.shape[1] != 3 or idx.device != u.device:
+        raise ValueError("idx must be an int64 [count, 3] tensor on u's device")
+    idx = idx.contiguous()
+    batch = u.numel() // size
+    spec = _spec(u, shape, h, h2, h3, eps, batch, domain=domain, itr_max=0)
+    p = plan(spec, dev)
+    out = torch.empty(idx.shape[0], dtype=torch.float64, device=u.device)
+    s = L.lib().fs1_plan_entries(p._h, _ptr(u), _ptr(v), _ptr(idx), idx.shape[0], _ptr(out), _stream(dev))
+    if s != L.FS1_OK:
+        raise L.FS1Error(s, "fs1_plan_entries")
+    return out
+
+
 def dual(a, b, u, v, *, h, eps, domain="scaling", input_is_log=False, shape=None, h2=None, h3=None, kernel=0):
     """fs1_dual: the dual objective of Eq. (2.3) at the state (u, v) for every pair ([batch] fp64)."""
     dev = u.device.index

@@ -80,6 +80,7 @@ def test_null_arguments():
     assert lib.fs1_solve(None, None, None, None, None, None, None, None, None, None, None) == L.FS1_ERR_ARG
     assert lib.fs1_cost(None, None, None, None, None, None) == L.FS1_ERR_ARG
     assert lib.fs1_apply(None, None, None, None, None) == L.FS1_ERR_ARG
+    assert lib.fs1_plan_entries(None, None, None, None, 0, None, None) == L.FS1_ERR_ARG
     lib.fs1_plan_destroy(None)
 
 
