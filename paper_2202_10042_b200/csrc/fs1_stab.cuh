@@ -40,12 +40,33 @@
 namespace fs1 {
 namespace stab {
 
+// unroll depth of the three half-step passes (the loads of the coefficient arrays go to
+// L2: deeper unrolling keeps more of them in flight)
+#ifndef FS1_STAB_UNROLL
+#define FS1_STAB_UNROLL 16
+#endif
+#define FS1_STAB_STR2(x) #x
+#define FS1_STAB_STR(x) FS1_STAB_STR2(unroll x)
+#define FS1_STAB_UNROLL_STR FS1_STAB_STR(FS1_STAB_UNROLL)
+
 enum { WA = 0, WB, WW, WFA, WGA, WFB, WGB, WTA, WTB, WN };  // workspace arrays per problem
 constexpr int FS1F_CONVERGED = 1, FS1F_NONFINITE = 2, FS1F_ITR_MAX = 4;
 
 // The workspace arrays are written and read by the same CTA only: plain (L1-coherent
 // for the CTA) loads, never the non-coherent or L1-bypassing paths.
 __device__ __forceinline__ double ld_(const double* p) { return *p; }
+
+// line 7 / 12's quotient: a reciprocal estimate with one Newton step and a residual
+// correction (< 1 ulp) where the denominator lies in 2^-1000 .. 2^1000, the IEEE '/'
+// otherwise (zero, non-finite or extreme denominators keep its exact semantics)
+#ifndef FS1_STAB_NDIV
+#define FS1_STAB_NDIV 1
+#endif
+__device__ __forceinline__ double sdiv(double t, double k) {
+  if (!FS1_STAB_NDIV) return t / k;
+  const double ak = fabs(k);
+  return (ak > 0x1p-1000 && ak < 0x1p1000) ? Tr<double>::div<true>(t, k) : t / k;
+}
 
 // an extended-range value as a double (overflow -> inf, underflow -> 0)
 __device__ __forceinline__ double er_val(ER<double> x) {
@@ -187,7 +208,7 @@ __device__ __forceinline__ void half(long long n, const double* xs, double* ys, 
   // product of many coefficients ever under/overflows on its own (Remark 3.3).
   double mf = 1.0, mb = 1.0;
   double Cf = 0.0, Cb = 0.0;
-#pragma unroll 4
+_Pragma(FS1_STAB_UNROLL_STR)
   for (int e = 0; e < E; ++e) {
     const int i = e * T + t;
     const double f = ld_(fv + i), g = ld_(gv + E * T - T - e * T + t);
@@ -217,14 +238,14 @@ __device__ __forceinline__ void half(long long n, const double* xs, double* ys, 
   double r = er_val(cf.C);
   double u = er_val(cb.C);
   // pass 2: the forward recursion r_k
-#pragma unroll 4
+_Pragma(FS1_STAB_UNROLL_STR)
   for (int e = 0; e < E; ++e) {
     const int i = e * T + t;
     r = fma(ld_(fv + i), r, ld_(wv + i) * xs[i]);
     R[i] = r;
   }
   // pass 3: backward recursion fused with the update
-#pragma unroll 4
+_Pragma(FS1_STAB_UNROLL_STR)
   for (int e = E - 1; e >= 0; --e) {
     const int i = e * T + t;
     const long long k = (long long)t * E + e;
@@ -233,7 +254,7 @@ __device__ __forceinline__ void half(long long n, const double* xs, double* ys, 
     const double kx = R[i] + su;        // (K~ x)_k = r_k + s_k
     u = su + ld_(wv + i) * xs[i];    // u_k = s_k + w_k x_k
     const double tg = ld_(tv + i);
-    const double y = k < n ? tg / kx : 0.0;
+    const double y = k < n ? sdiv(tg, kx) : 0.0;
     if (CHECK) {
       if (k < n) errp += fabs(ys[i] * kx - tg);
       R[i] = y;
