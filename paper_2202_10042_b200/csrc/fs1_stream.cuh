@@ -715,7 +715,13 @@ __device__ __forceinline__ void stream_half(Ctx& c, const StreamParams& P, const
       tn = fma(lam, tn, xv[e]);
       if (CHECK) errp += fabs(fma(ov[e] * sce, kx, -tv[e]));
       if (WRITE) {
-        if (DIV) tv[e] = guard ? (tv[e] > 0.0 ? fdiv(tv[e], kx) : 0.0) : fdiv(tv[e], kx);
+        if (DIV) {
+          // branch-free: the quotient always, a select for the zero targets of a guarded
+          // tile (the nested conditional compiled to two branches and two copies of the
+          // division per point)
+          const double q = fdiv(tv[e], kx);
+          tv[e] = (guard && !(tv[e] > 0.0)) ? 0.0 : q;
+        }
         else tv[e] = kx;
       }
     }
