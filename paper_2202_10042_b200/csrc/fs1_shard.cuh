@@ -492,7 +492,10 @@ __global__ void __launch_bounds__(32 * NW) k_half(const ShardParams P, const Hal
       const double kx = fma(lam, tn, pf[e]);
       tn = fma(lam, tn, xv[e]);
       if (CHECK) errp += fabs(fma(ov[e] * sce, kx, -tv[e]));
-      if (WRITE) tv[e] = guard ? (tv[e] > 0.0 ? stm::fdiv(tv[e], kx) : 0.0) : stm::fdiv(tv[e], kx);
+      if (WRITE) {  // branch-free (as K2's update): the quotient, a select for guarded zeros
+        const double q = stm::fdiv(tv[e], kx);
+        tv[e] = (guard && !(tv[e] > 0.0)) ? 0.0 : q;
+      }
     }
     if (CHECK) {
       const double es = warp_sum(errp);
