@@ -112,15 +112,12 @@ __device__ __forceinline__ float p2f(int d) {  // exact 2^d, 0 below 2^-126
   return d >= -126 ? __uint_as_float((unsigned)(d + 127) << 23) : 0.f;
 }
 __device__ __forceinline__ ERf ern(float x, int e) {  // normalise x 2^e (x >= 0, normal or 0)
+  // selects, no branch (a branch here made every scan level of line_apply_lin divergent)
+  const unsigned u = __float_as_uint(x);
+  const bool pos = x > 0.f;
   ERf r;
-  if (x > 0.f) {
-    const unsigned u = __float_as_uint(x);
-    r.e = e + (int)((u >> 23) & 0xffu) - 127;
-    r.m = __uint_as_float((u & 0x807fffffu) | 0x3f800000u);
-  } else {
-    r.m = 0.f;
-    r.e = ZE;
-  }
+  r.e = pos ? e + (int)((u >> 23) & 0xffu) - 127 : ZE;
+  r.m = pos ? __uint_as_float((u & 0x807fffffu) | 0x3f800000u) : 0.f;
   return r;
 }
 __device__ __forceinline__ ERf era(ERf a, ERf b) {
@@ -182,8 +179,15 @@ __device__ __forceinline__ int line_apply_lin(float (&A)[E], int oe, const AxT& 
     const int d = 1 << k;
     const ERf up{__shfl_up_sync(FULL, F.m, d), __shfl_up_sync(FULL, F.e, d)};
     const ERf dn{__shfl_down_sync(FULL, B.m, d), __shfl_down_sync(FULL, B.e, d)};
-    if (lane >= d) F = era(erm(up, T.Lm[k], T.Le[k]), F);
-    if (lane + d < 32) B = era(erm(dn, T.Lm[k], T.Le[k]), B);
+    // combined on every lane, kept by a select (branch-free: the lanes below d / above
+    // 31 - d would otherwise diverge at every level)
+    const ERf Fn = era(erm(up, T.Lm[k], T.Le[k]), F);
+    const ERf Bn = era(erm(dn, T.Lm[k], T.Le[k]), B);
+    const bool tf = lane >= d, tb = lane + d < 32;
+    F.m = tf ? Fn.m : F.m;
+    F.e = tf ? Fn.e : F.e;
+    B.m = tb ? Bn.m : B.m;
+    B.e = tb ? Bn.e : B.e;
   }
   ERf cf{__shfl_up_sync(FULL, F.m, 1), __shfl_up_sync(FULL, F.e, 1)};
   ERf cb{__shfl_down_sync(FULL, B.m, 1), __shfl_down_sync(FULL, B.e, 1)};
