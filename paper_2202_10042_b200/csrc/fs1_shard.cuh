@@ -197,8 +197,13 @@ __device__ __forceinline__ void warp_pair_scan(PowTab t, int lane, ER<double>& F
     const int us = __shfl_up_sync(FULL, sF, d);
     const ER<double> dg = shfl_down_er(G, d);
     const int ds = __shfl_down_sync(FULL, sG, d);
-    if (lane >= d) { F = er_fma(uf, tpow(t, sF), F); sF += us; }
-    if (lane + d < 32) { G = er_fma(dg, tpow(t, sG), G); sG += ds; }
+    // combined on every lane, kept by selects (branch-free scan levels)
+    const ER<double> Fn = er_fma(uf, tpow(t, sF), F), Gn = er_fma(dg, tpow(t, sG), G);
+    const bool tf = lane >= d, tb = lane + d < 32;
+    F = ER<double>{tf ? Fn.m : F.m, tf ? Fn.e : F.e};
+    sF += tf ? us : 0;
+    G = ER<double>{tb ? Gn.m : G.m, tb ? Gn.e : G.e};
+    sG += tb ? ds : 0;
   }
 }
 

@@ -87,6 +87,12 @@ __device__ __forceinline__ Aff ident(Aff*) { return Aff{er1(), er_zero<double>()
 __device__ __forceinline__ Aff compose(Aff L, Aff E) {  // L after E
   return Aff{er_mul(L.M, E.M), erfma(L.M, E.C, L.C)};
 }
+// branch-free keep-or-replace of a map at a scan level (an `if (lane >= d) x = ...`
+// around the extended-range compose compiled to a divergent branch at every level)
+__device__ __forceinline__ ER<double> er_sel(bool p, ER<double> a, ER<double> b) {
+  return ER<double>{p ? a.m : b.m, p ? a.e : b.e};
+}
+__device__ __forceinline__ Aff msel(bool p, Aff a, Aff b) { return Aff{er_sel(p, a.M, b.M), er_sel(p, a.C, b.C)}; }
 __device__ __forceinline__ Aff shfl_up_m(Aff x, int d) { return Aff{shfl_up_er(x.M, d), shfl_up_er(x.C, d)}; }
 __device__ __forceinline__ Aff shfl_down_m(Aff x, int d) { return Aff{shfl_down_er(x.M, d), shfl_down_er(x.C, d)}; }
 __device__ __forceinline__ Aff shfl_idx_m(Aff x, int s) { return Aff{shfl_idx_er(x.M, s), shfl_idx_er(x.C, s)}; }
@@ -99,6 +105,9 @@ __device__ __forceinline__ Jor ident(Jor*) { return Jor{er1(), er_zero<double>()
 __device__ __forceinline__ Jor compose(Jor L, Jor E) {
   return Jor{er_mul(L.a, E.a), er_add(er_mul(L.a, E.b), er_mul(L.b, E.a)), erfma(L.a, E.c1, L.c1),
              er_add(er_add(er_mul(L.b, E.c1), er_mul(L.a, E.c2)), L.c2)};
+}
+__device__ __forceinline__ Jor msel(bool p, Jor a, Jor b) {
+  return Jor{er_sel(p, a.a, b.a), er_sel(p, a.b, b.b), er_sel(p, a.c1, b.c1), er_sel(p, a.c2, b.c2)};
 }
 __device__ __forceinline__ Jor shfl_up_m(Jor x, int d) {
   return Jor{shfl_up_er(x.a, d), shfl_up_er(x.b, d), shfl_up_er(x.c1, d), shfl_up_er(x.c2, d)};
@@ -117,7 +126,7 @@ __device__ __forceinline__ Map block_scan_excl(Map x, Map* sm) {
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
     const Map y = FWD ? shfl_up_m(x, d) : shfl_down_m(x, d);
-    if (FWD ? lane >= d : lane + d < 32) x = compose(x, y);
+    x = msel(FWD ? lane >= d : lane + d < 32, compose(x, y), x);
   }
   if (lane == (FWD ? 31 : 0)) sm[warp] = x;
   __syncthreads();
@@ -144,8 +153,8 @@ __device__ __forceinline__ void block_scan2(Aff xf, Aff xb, Aff* sm, Aff& ef, Af
   for (int d = 1; d < 32; d <<= 1) {
     const Aff yf = shfl_up_m(xf, d);
     const Aff yb = shfl_down_m(xb, d);
-    if (lane >= d) xf = compose(xf, yf);
-    if (lane + d < 32) xb = compose(xb, yb);
+    xf = msel(lane >= d, compose(xf, yf), xf);
+    xb = msel(lane + d < 32, compose(xb, yb), xb);
   }
   if (lane == 31) sm[warp] = xf;
   if (lane == 0) sm[W + warp] = xb;
@@ -157,8 +166,8 @@ __device__ __forceinline__ void block_scan2(Aff xf, Aff xb, Aff* sm, Aff& ef, Af
   for (int d = 1; d < W; d <<= 1) {
     const Aff yf = shfl_up_m(wf, d);
     const Aff yb = shfl_down_m(wb, d);
-    if (lane >= d) wf = compose(wf, yf);
-    if (lane + d < W) wb = compose(wb, yb);
+    wf = msel(lane >= d, compose(wf, yf), wf);
+    wb = msel(lane + d < W, compose(wb, yb), wb);
   }
   // composite of the warps before (after) this one: lane warp-1 (warp+1) of the scans
   Aff cwf = shfl_idx_m(wf, warp > 0 ? warp - 1 : 0);
