@@ -21,7 +21,9 @@ for c in ${LCFGS:-c3 c2 c4 c5}; do
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_$c.csv \
     python bench.py --config $c --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > $O/ncu_launch_$c.log 2>&1
 done
-for spec in ${PCFGS:-"c3 fs1_stream_kernel" "c4 fs1_sep2dw" "c5 fs1_persist_solve" "c2 fs1_persist_solve" "e3_160 fs1_sep2d64w"}; do
+# PCFGS: comma-separated "config kernel-regex" pairs
+IFS=, read -ra SPECS <<< "${PCFGS:-c3 fs1_stream_kernel,c4 fs1_sep2dw,c5 fs1_persist_solve,c2 fs1_persist_solve,e3_160 fs1_sep2d64w,e2s_8000 fs1_stab}"
+for spec in "${SPECS[@]}"; do
   set -- $spec
   timeout 1200 ncu --set full --clock-control none --import-source on -k regex:$2 -s 1 -c 1 -o $O/prof_$1 -f \
     python bench.py --config $1 --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > $O/ncu_full_$1.log 2>&1
