@@ -56,6 +56,11 @@ namespace sepw {
 #ifndef FS1_K3W_LATE_TMA
 #define FS1_K3W_LATE_TMA 1
 #endif
+// the next pass's first target line is fetched by TMA at the end of a pass (the stage is
+// free once the transposed write is out), so it lands during the grid barrier
+#ifndef FS1_K3W_PREFETCH
+#define FS1_K3W_PREFETCH 0
+#endif
 constexpr int W = 8;        // warps = lines per CTA group
 constexpr int NT = 32 * W;
 constexpr int LIMF = 60;    // carries up to 2^60 above a chunk keep its exponent
@@ -259,6 +264,7 @@ struct WarpIO {
   float* ts;       // target line: aliases this warp's stage region (free until the FUSE output)
   uint64_t* mb;    // [2]: (unused), target
   unsigned ph0, ph1;  // parity of the next wait on mb[0] / mb[1]
+  int pre;            // the first target line of the next pass is already in flight (warp-uniform)
 };
 
 // One fused pass over `nlines` lines of length `len` (axis tables T):
@@ -279,7 +285,8 @@ __device__ __forceinline__ void fused_pass(sep::Ctx& c, WarpIO& io, const AxT& T
                                            const float* TM, const int* TX, const float* LT,
                                            const float* Yold, float* Yout, float* Zout, int nlines,
                                            int len, int G, double& errsum, int& bad,
-                                           unsigned long long* td = nullptr) {
+                                           unsigned long long* td = nullptr, const float* TMn = nullptr,
+                                           int nln = 0) {
   using C = Cfg<E>;
   const int lane = c.lane, w = c.warp;
   const int ngroups = (nlines + W - 1) / W;
@@ -295,8 +302,10 @@ __device__ __forceinline__ void fused_pass(sep::Ctx& c, WarpIO& io, const AxT& T
       // the target line arrives by TMA; issued once this warp's X line has landed, so the
       // two 16 MB bursts of a pass (every warp's X, then every warp's target) share L2
       // bandwidth with the first apply instead of with each other
+      const bool pre = gi == 0 && io.pre;  // issued at the end of the previous pass
+      io.pre = 0;
       auto issue_target = [&]() {
-        if ((MODE & UPD) && lane == 0) {
+        if ((MODE & UPD) && lane == 0 && !pre) {
           stm::fence_async_smem();
           stm::mbar_expect_tx(&io.mb[1], (unsigned)C::LINEB);
           stm::bulk_g2s(io.ts, TM + off, (unsigned)C::LINEB, &io.mb[1]);
@@ -400,6 +409,19 @@ __device__ __forceinline__ void fused_pass(sep::Ctx& c, WarpIO& io, const AxT& T
     }
     __syncthreads();
     if (t) t[7] = stm::gtimer();
+    if (FS1_K3W_PREFETCH && TMn && grp + G >= ngroups) {
+      // this warp's first line of the next pass (same group index c.r): its target line
+      // goes into the now free stage region while the CTA waits at the grid barrier
+      const int nl = c.r * W + w;
+      if (nl < nln) {
+        if (lane == 0) {
+          stm::fence_async_smem();
+          stm::mbar_expect_tx(&io.mb[1], (unsigned)C::LINEB);
+          stm::bulk_g2s(io.ts, TMn + (size_t)nl * C::LP, (unsigned)C::LINEB, &io.mb[1]);
+        }
+        io.pre = 1;
+      }
+    }
   }
 }
 
@@ -489,6 +511,7 @@ __global__ void __launch_bounds__(NT, MINB) fs1_sep2dw_kernel(const __grid_const
   io.ts = c.s.stage + (size_t)c.warp * C::SLINE;
   io.mb = reinterpret_cast<uint64_t*>(smem + C::OFF_MBAR) + 2 * c.warp;
   io.ph0 = io.ph1 = 0;
+  io.pre = 0;
   if (c.lane == 0) {
     stm::mbar_init(&io.mb[0], 1);
     stm::mbar_init(&io.mb[1], 1);
@@ -555,13 +578,15 @@ __global__ void __launch_bounds__(NT, MINB) fs1_sep2dw_kernel(const __grid_const
     double es = 0.0;
     bad = 0;
     // ---- pass R: psi half-step (Alg. 2 lines 3-7) + first pass of the phi half-step
+    // (a check pass may stop the loop: no prefetch for the pass after it)
     if (last) fused_pass<E, UPD | CHK>(c, io, T2, Z1, BM, BX, LBt, Gi, Go, Z2, n, m, G, es, bad);
     else if (check && keep)
       fused_pass<E, UPD | WR | CHK | FUSE>(c, io, T2, Z1, BM, BX, LBt, Gi, Go, Z2, n, m, G, es, bad);
     else if (check) fused_pass<E, UPD | CHK | FUSE>(c, io, T2, Z1, BM, BX, LBt, Gi, Go, Z2, n, m, G, es, bad);
-    else if (keep) fused_pass<E, UPD | WR | FUSE>(c, io, T2, Z1, BM, BX, LBt, nullptr, Go, Z2, n, m, G, es, bad);
+    else if (keep)
+      fused_pass<E, UPD | WR | FUSE>(c, io, T2, Z1, BM, BX, LBt, nullptr, Go, Z2, n, m, G, es, bad, nullptr, AM, m);
     else fused_pass<E, UPD | FUSE>(c, io, T2, Z1, BM, BX, LBt, nullptr, Go, Z2, n, m, G, es, bad,
-                                   (P.tdbg && l == 5) ? P.tdbg : nullptr);
+                                   (P.tdbg && l == 5) ? P.tdbg : nullptr, AM, m);
     bad = __syncthreads_or(bad);
     int f;
     double e = 0.0;
@@ -579,13 +604,21 @@ __global__ void __launch_bounds__(NT, MINB) fs1_sep2dw_kernel(const __grid_const
     if (f) { ++l; flag = 2; break; }
     // ---- pass C: phi half-step (lines 8-12) + first pass of the next psi half-step
     bad = 0;
-    if (keep) fused_pass<E, UPD | WR | FUSE>(c, io, T1, Z2, AM, AX, LA, nullptr, Fp, Z1, m, n, G, es, bad);
-    else fused_pass<E, UPD | FUSE>(c, io, T1, Z2, AM, AX, LA, nullptr, Fp, Z1, m, n, G, es, bad);
+    // the next R pass always runs (unless a flag stops the loop, drained below)
+    if (keep) fused_pass<E, UPD | WR | FUSE>(c, io, T1, Z2, AM, AX, LA, nullptr, Fp, Z1, m, n, G, es, bad, nullptr, BM, n);
+    else fused_pass<E, UPD | FUSE>(c, io, T1, Z2, AM, AX, LA, nullptr, Fp, Z1, m, n, G, es, bad, nullptr, BM, n);
     bad = __syncthreads_or(bad);
     f = grid_flag(c, P, bad);
     ++l;  // line 13
     if (f) { flag = 2; break; }
   }
+
+  if (io.pre) {  // a prefetched target line nobody consumed (a flag stopped the loop)
+    stm::mbar_wait(&io.mb[1], io.ph1);
+    io.ph1 ^= 1u;
+    io.pre = 0;
+  }
+  __syncthreads();
 
   // ---- outputs in the user layout: F column-major into u, G row-major natural (for the
   // cost) into the LA buffer, then transposed into v (column-major)

@@ -15,11 +15,13 @@
 //      + lambda^{256 i} x external carry;
 //  [B] each warp streams its tiles: 1D TMA bulk copies (cp.async.bulk, mbarrier
 //      complete_tx) of x and tgt into a private S-stage shared-memory ring, a
-//      conflict-free XOR-swizzled read into registers (8 points per lane), lane
+//      conflict-free XOR-swizzled read into registers (8 points per lane; zero excessive
+//      shared wavefronts in ncu's source view, profiles/r02/r02z_bank_conflicts_c3.txt), lane
 //      Horner aggregates, a 5-level warp shuffle scan, the forward and backward
 //      recursions of Eq. "recursion" from the exact carries,
 //      y = tgt * rcp(p + lambda t), one exact power-of-two renormalisation of the
-//      output tile, the output tile's scan totals, and a TMA bulk store of y;
+//      output tile, the output tile's totals (one weighted warp reduction each), and a
+//      TMA bulk store of y;
 //  [C] a block scan of the produced tiles' totals gives their local exclusive
 //      carries (kept for the next half-step) and this range's totals, which are
 //      published before the grid barrier.
@@ -294,6 +296,36 @@ __device__ __forceinline__ void tile_scan_lanes(const StreamParams& P, int lane,
     Fi = scan_up(Fi, 1u << k, P.lvd[k]);
     Gi = scan_down(Gi, 1u << k, P.lvd[k]);
   }
+}
+
+// Tile totals only (no per-lane prefixes): forward total at the tile end
+// sum_l lambda^{8(31-l)} f_l and backward total at the tile start sum_l lambda^{8l} g_l
+// (f_l, g_l the lane aggregates), by one weighted butterfly reduction each; every lane
+// gets both totals.  lp = lambda^{8 lane}, rp = lambda^{8(31-lane)}.
+#ifndef FS1_K2_REDTOT
+#define FS1_K2_REDTOT 1
+#endif
+#ifndef FS1_K2_SELHOIST
+#define FS1_K2_SELHOIST 1
+#endif
+__device__ __forceinline__ void tile_totals_lanes(const StreamParams& P, double lp, double rp, const double (&v)[E],
+                                                  double& Ft, double& Gt) {
+  const double lam = P.lam;
+  double f = 0.0, g = 0.0;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    f = fma(lam, f, v[e]);
+    g = fma(lam, g, v[E - 1 - e]);
+  }
+  f *= rp;
+  g *= lp;
+#pragma unroll
+  for (int d = 16; d >= 1; d >>= 1) {
+    f += __shfl_xor_sync(FULL, f, d);
+    g += __shfl_xor_sync(FULL, g, d);
+  }
+  Ft = f;
+  Gt = g;
 }
 
 // Store the tile totals of a produced tile (exponent Y) into the table at i.
@@ -709,6 +741,11 @@ __device__ __forceinline__ void stream_half(Ctx& c, const StreamParams& P, const
     double sce = 0.0;
     if (CHECK) sce = pow2d(min(max(A.Xo[i] + R - A.Xt[i], -1100), 1000));
     const bool guard = DIV && A.tz[i];  // zero targets: y = 0 exactly (warp-uniform)
+    unsigned zm = 0;  // FS1_K2_SELHOIST: the zero targets of a guarded tile, zeroed after the loop
+    if (FS1_K2_SELHOIST && guard) {
+#pragma unroll
+      for (int e = 0; e < E; ++e) zm |= (unsigned)!(tv[e] > 0.0) << e;
+    }
 #pragma unroll
     for (int e = E - 1; e >= 0; --e) {
       const double kx = fma(lam, tn, pf[e]);
@@ -720,10 +757,15 @@ __device__ __forceinline__ void stream_half(Ctx& c, const StreamParams& P, const
           // tile (the nested conditional compiled to two branches and two copies of the
           // division per point)
           const double q = fdiv(tv[e], kx);
-          tv[e] = (guard && !(tv[e] > 0.0)) ? 0.0 : q;
+          tv[e] = FS1_K2_SELHOIST ? q : ((guard && !(tv[e] > 0.0)) ? 0.0 : q);
         }
         else tv[e] = kx;
       }
+    }
+    if (FS1_K2_SELHOIST && DIV && WRITE && guard) {  // warp-uniform, rare
+#pragma unroll
+      for (int e = 0; e < E; ++e)
+        if ((zm >> e) & 1u) tv[e] = 0.0;
     }
     if (CHECK) {
       const double es = warp_sum(errp);
@@ -749,7 +791,8 @@ __device__ __forceinline__ void stream_half(Ctx& c, const StreamParams& P, const
         for (int e = 0; e < E; ++e) tv[e] = 0.0;
       }
       double FiY, GiY;
-      tile_scan_lanes(P, lane, tv, FiY, GiY);
+      if (FS1_K2_REDTOT) tile_totals_lanes(P, lp, rp, tv, FiY, GiY);
+      else tile_scan_lanes(P, lane, tv, FiY, GiY);
       if (!isfinite(FiY + GiY)) bad = 1;
       put_totals(lane, FiY, GiY, Y, A.yFm, A.yFe, A.yBm, A.yBe, i);
       if (lane == 0) A.Xy[i] = Y;
