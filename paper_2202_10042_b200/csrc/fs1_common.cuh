@@ -153,6 +153,37 @@ __device__ __forceinline__ int warp_min(int v) { return __reduce_min_sync(FULL, 
 // Warp scan step without selects: the shuffle's in-range predicate guards the FMA.
 // up:   v + m * v[lane - d]  (lane >= d), else v
 // down: v + m * v[lane + d]  (lane + d < 32), else v
+#ifndef FS1_SCAN_SELM
+#define FS1_SCAN_SELM 1
+#endif
+#if FS1_SCAN_SELM
+// Variant: the shuffle's predicate selects the multiplier (m or 0) and one FMA updates v in
+// place (out-of-range lanes get their own value back, times 0).
+__device__ __forceinline__ double scan_up(double v, unsigned d, double m) {
+  asm("{\n\t.reg .pred p;\n\t.reg .b32 lo, hi, a, b;\n\t.reg .f64 s, mm;\n\t"
+      "mov.b64 {lo, hi}, %0;\n\t"
+      "shfl.sync.up.b32 a|p, lo, %1, 0, -1;\n\t"
+      "shfl.sync.up.b32 b, hi, %1, 0, -1;\n\t"
+      "mov.b64 s, {a, b};\n\t"
+      "selp.f64 mm, %2, 0d0000000000000000, p;\n\t"
+      "fma.rn.f64 %0, mm, s, %0;\n\t}"
+      : "+d"(v)
+      : "r"(d), "d"(m));
+  return v;
+}
+__device__ __forceinline__ double scan_down(double v, unsigned d, double m) {
+  asm("{\n\t.reg .pred p;\n\t.reg .b32 lo, hi, a, b;\n\t.reg .f64 s, mm;\n\t"
+      "mov.b64 {lo, hi}, %0;\n\t"
+      "shfl.sync.down.b32 a|p, lo, %1, 31, -1;\n\t"
+      "shfl.sync.down.b32 b, hi, %1, 31, -1;\n\t"
+      "mov.b64 s, {a, b};\n\t"
+      "selp.f64 mm, %2, 0d0000000000000000, p;\n\t"
+      "fma.rn.f64 %0, mm, s, %0;\n\t}"
+      : "+d"(v)
+      : "r"(d), "d"(m));
+  return v;
+}
+#else
 __device__ __forceinline__ double scan_up(double v, unsigned d, double m) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t.reg .b32 lo, hi, a, b;\n\t.reg .f64 s;\n\t"
@@ -177,6 +208,7 @@ __device__ __forceinline__ double scan_down(double v, unsigned d, double m) {
       : "r"(d), "d"(m));
   return v;
 }
+#endif
 // exclusive neighbours: v[lane-1] (0 at lane 0) and v[lane+1] (0 at lane 31)
 __device__ __forceinline__ double prev_or0(double v) {
   double r = 0.0;

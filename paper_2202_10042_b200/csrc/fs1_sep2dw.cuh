@@ -61,6 +61,11 @@ namespace sepw {
 #ifndef FS1_K3W_PREFETCH
 #define FS1_K3W_PREFETCH 0
 #endif
+// fused passes test the updated line for NaN / +inf through the second apply's chunk
+// aggregates instead of point by point
+#ifndef FS1_K3W_AGGNF
+#define FS1_K3W_AGGNF 1
+#endif
 constexpr int W = 8;        // warps = lines per CTA group
 constexpr int NT = 32 * W;
 constexpr int LIMF = 60;    // carries up to 2^60 above a chunk keep its exponent
@@ -163,8 +168,11 @@ __device__ __forceinline__ int prep_log(float (&A)[E]) {
 
 // A: this lane's chunk as linear mantissas relative to 2^oe (oe = ZE: zero chunk).
 // On return A[e] = (K x)_e relative to 2^R (linear fp32), R returned.
+// nf (optional): set when this lane's chunk holds a NaN or +inf (its aggregates are then
+// non-finite: the chains only add non-negative terms), the update's non-finite test
 template <int E>
-__device__ __forceinline__ int line_apply_lin(float (&A)[E], int oe, const AxT& T, int lane) {
+__device__ __forceinline__ int line_apply_lin(float (&A)[E], int oe, const AxT& T, int lane,
+                                              int* nf = nullptr) {
   constexpr int H = E / 2;
   // chunk aggregates (Horner, zero carries), 4 independent chains over the halves
   const float lam = T.lam, lH = T.lamH;
@@ -176,8 +184,10 @@ __device__ __forceinline__ int line_apply_lin(float (&A)[E], int oe, const AxT& 
     g0 = fmaf(lam, g0, A[H - 1 - e]);
     g1 = fmaf(lam, g1, A[E - 1 - e]);
   }
-  ERf F = ern(fmaf(lH, f0, f1), oe);  // forward total at the chunk end
-  ERf B = ern(fmaf(lH, g1, g0), oe);  // backward total at the chunk start
+  const float fa = fmaf(lH, f0, f1), ga = fmaf(lH, g1, g0);
+  if (nf) *nf |= !(fa + ga < INFINITY);
+  ERf F = ern(fa, oe);  // forward total at the chunk end
+  ERf B = ern(ga, oe);  // backward total at the chunk start
   // warp inclusive scans of the affine maps y -> lambda^{E d} y + c (Hillis-Steele)
 #pragma unroll
   for (int k = 0; k < 5; ++k) {
@@ -352,7 +362,7 @@ __device__ __forceinline__ void fused_pass(sep::Ctx& c, WarpIO& io, const AxT& T
               if (MODE & WR) b |= (ys[r] != ys[r]) | (ys[r] == INFINITY);
             }
             const float v = tmv[r] * Tr<float>::rcp(k);
-            b |= (v != v) | (v == INFINITY);
+            if (!(FS1_K3W_AGGNF && (MODE & FUSE))) b |= (v != v) | (v == INFINITY);
             A[e] = v;
           }
           if (MODE & WR) stg8(Yout + off + (j * 32 + lane) * 8, ys);
@@ -365,7 +375,10 @@ __device__ __forceinline__ void fused_pass(sep::Ctx& c, WarpIO& io, const AxT& T
       }
       if (t) t[4] = stm::gtimer() + (A[1] == 12345.f);
       if (MODE & FUSE) {
-        const int R2 = (MODE & UPD) ? line_apply_lin<E>(A, oe2, T, lane) : line_apply<E>(A, T, lane);
+        int nf = 0;
+        const int R2 = (MODE & UPD) ? line_apply_lin<E>(A, oe2, T, lane, FS1_K3W_AGGNF ? &nf : nullptr)
+                                    : line_apply<E>(A, T, lane);
+        if (FS1_K3W_AGGNF && (MODE & UPD) && nf) bad = 1;
         if (t) t[5] = stm::gtimer() + (R2 == 12345);
         const float Rl2 = (float)R2 * LN2;
         __syncwarp();  // every lane has read its target chunk (the stage aliases it)

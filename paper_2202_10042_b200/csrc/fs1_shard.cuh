@@ -87,6 +87,29 @@ __device__ __forceinline__ void lane_scan(const ShardParams& P, const double (&v
   }
 }
 
+// tile totals only (as K2's tile_totals_lanes): forward sum_l lambda^{8(31-l)} f_l at the
+// tile end, backward sum_l lambda^{8l} g_l at its start, on every lane (lp = lambda^{8 lane},
+// rp = lambda^{8(31-lane)})
+__device__ __forceinline__ void lane_tot(const ShardParams& P, double lp, double rp, const double (&v)[E],
+                                         double& Ft, double& Gt) {
+  const double lam = P.lam;
+  double f = 0.0, g = 0.0;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    f = fma(lam, f, v[e]);
+    g = fma(lam, g, v[E - 1 - e]);
+  }
+  f *= rp;
+  g *= lp;
+#pragma unroll
+  for (int d = 16; d >= 1; d >>= 1) {
+    f += __shfl_xor_sync(FULL, f, d);
+    g += __shfl_xor_sync(FULL, g, d);
+  }
+  Ft = f;
+  Gt = g;
+}
+
 __device__ __forceinline__ void put_tot(const ShardParams& P, int lane, double Fi, double Gi, int X, int i,
                                         double* Fm, int* Fe, double* Bm, int* Be) {
   if (lane == 31) {
@@ -491,16 +514,23 @@ __global__ void __launch_bounds__(32 * NW) k_half(const ShardParams P, const Hal
     }
     const int Xt = io.tX[i];
     const bool guard = io.tz[i];
+    unsigned zm = 0;  // zero targets of a guarded tile (warp-uniform test), zeroed after the loop
+    if (WRITE && guard) {
+#pragma unroll
+      for (int e = 0; e < E; ++e) zm |= (unsigned)!(tv[e] > 0.0) << e;
+    }
     double tn = cb, errp = 0.0;
 #pragma unroll
     for (int e = E - 1; e >= 0; --e) {
       const double kx = fma(lam, tn, pf[e]);
       tn = fma(lam, tn, xv[e]);
       if (CHECK) errp += fabs(fma(ov[e] * sce, kx, -tv[e]));
-      if (WRITE) {  // branch-free (as K2's update): the quotient, a select for guarded zeros
-        const double q = stm::fdiv(tv[e], kx);
-        tv[e] = (guard && !(tv[e] > 0.0)) ? 0.0 : q;
-      }
+      if (WRITE) tv[e] = stm::fdiv(tv[e], kx);  // branch-free (as K2's update)
+    }
+    if (WRITE && guard) {
+#pragma unroll
+      for (int e = 0; e < E; ++e)
+        if ((zm >> e) & 1u) tv[e] = 0.0;
     }
     if (CHECK) {
       const double es = warp_sum(errp);
@@ -525,7 +555,7 @@ __global__ void __launch_bounds__(32 * NW) k_half(const ShardParams P, const Hal
         for (int e = 0; e < E; ++e) tv[e] = 0.0;
       }
       double FiY, GiY;
-      lane_scan(P, tv, FiY, GiY);
+      lane_tot(P, lp, rp, tv, FiY, GiY);
       if (!isfinite(FiY + GiY)) bad = 1;
       put_tot(P, lane, FiY, GiY, Y, i, io.yb.Fm, io.yb.Fe, io.yb.Bm, io.yb.Be);
       st_tile(io.ym + (size_t)i * TILE, lane, tv);

@@ -240,3 +240,22 @@ def test_config4_full_run_properties():
     L2 = recur.wsweep_log(recur.sweep_log(G, c1, axis=1), c2, cfg.h2, axis=2)
     ref = recur.sum_exp2(F, L1) + recur.sum_exp2(F, L2)
     assert rel(out["cost"].item(), ref) <= TOL32
+
+
+@pytest.mark.parametrize("side", ["a", "b"])
+@pytest.mark.parametrize("n,m", [(256, 200), (1500, 1100)])
+def test_sep2d_warp_line_nonfinite_weight(side, n, m):
+    """K3w: a +inf log-weight poisons the problem in the first half-step that divides by
+    it (phi^(1) = a / K psi for a, psi^(1) = b / K^T phi for b): the solve stops NONFINITE
+    with l = 1 and NaN cost / err (S7, PAPER.md:148 has no finite error then); a NaN does
+    the same."""
+    for bad in (np.inf, np.nan):
+        la, lb = _pair2d(n, m, 7 * n + m)
+        (la if side == "a" else lb)[(m // 2) * n + n // 3] = bad  # column-major flat index
+        kw = dict(h=1 / n, h2=1 / m, eps=2e-3, itr_max=20, domain="log", input_is_log=True, shape=(n, m))
+        assert fs1.plan(fs1.Spec(ndim=2, n=n, m=m, h1=1 / n, h2=1 / m, eps=2e-3, batch=1,
+                                 dtype=torch.float32, domain="log", input_is_log=True,
+                                 itr_max=20)).info()["kernel"].startswith("sep2dw")
+        out = fs1.solve(_cuda(la[None]), _cuda(lb[None]), **kw)
+        assert out["flags"].item() == 2 and out["iters"].item() == 1, (bad, out["flags"], out["iters"])
+        assert np.isnan(out["cost"].item())
