@@ -493,7 +493,47 @@ __device__ __forceinline__ void fill(const sep::Ctx& c, float* dst, size_t cnt, 
 
 // Grid barrier that also ORs one flag over the CTAs (non-check passes: no error sum).
 // bar[1] is a sticky word (zeroed at launch with the barrier counter).
+// FS1_K3W_FLAG64: bar[0] (counter) and bar[1] (flag word) are one aligned 8-byte pair and
+// the spinning thread reads both with one 64-bit acquire load.  A CTA's OR precedes its
+// release-add, so the load that sees the last arrival also sees every OR: no second L2
+// round trip for the flag, and (called right after the caller's __syncthreads_or, with a
+// block-uniform myflag) one block barrier per pass instead of four.
+#ifndef FS1_K3W_FLAG64
+#define FS1_K3W_FLAG64 1
+#endif
+// FS1_K3W_NOTF >= 1: no fence.proxy.async / __threadfence before the arrival (the pass's
+// writes are generic-proxy stores, ordered by the block barrier and the red's own release,
+// which is cumulative over the CTA).  2: no fence.proxy.async after the spin either: the only
+// async-proxy (TMA) reads of the loop fetch the mantissa lines AM / BM, written once before
+// the fully fenced stm::grid_barrier that precedes the loop; everything a pass produces is
+// read back by generic ld.global.cg.
+#ifndef FS1_K3W_NOTF
+#define FS1_K3W_NOTF 2
+#endif
 __device__ __forceinline__ int grid_flag(sep::Ctx& c, const Sep2dParams& P, int myflag) {
+#if FS1_K3W_FLAG64
+  if (c.tid == 0) {
+    if (myflag) atomicOr(&P.bar[1], 1u);
+#if !FS1_K3W_NOTF
+    stm::fence_async();
+    __threadfence();
+#endif
+    const unsigned target = (c.gen + 1) * (unsigned)P.G;
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(P.bar) : "memory");
+    unsigned long long v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(P.bar) : "memory");
+    } while ((unsigned)v < target);
+#if FS1_K3W_NOTF < 2
+    stm::fence_async();
+#endif
+    c.s.ired[33] = (int)(v >> 32);
+  }
+  ++c.gen;
+  __syncthreads();
+  // the next write of ired[33] follows the next pass's block barriers: no trailing barrier
+  return c.s.ired[33];
+#else
   if (c.tid == 0 && myflag) atomicOr(&P.bar[1], 1u);
   stm::grid_barrier(P.bar, P.G, c.gen);
   if (c.tid == 0) c.s.ired[33] = (int)stm::ld_acquire(&P.bar[1]);
@@ -501,6 +541,7 @@ __device__ __forceinline__ int grid_flag(sep::Ctx& c, const Sep2dParams& P, int 
   const int f = c.s.ired[33];
   __syncthreads();
   return f;
+#endif
 }
 
 // ------------------------------------------------------------ the kernel (solve only)

@@ -164,6 +164,9 @@ __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+#ifndef FS1_GB_NOTF
+#define FS1_GB_NOTF 0
+#endif
 // Grid-wide barrier of the co-resident CTAs (the cooperative launch guarantees
 // residency): one release-add per CTA on a monotonic counter, then an acquire
 // spin until it reaches G x (barriers so far).  bar[0] must be 0 at launch.
@@ -171,7 +174,9 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned G, unsigned
   __syncthreads();
   if (threadIdx.x == 0) {
     fence_async();
+#if !FS1_GB_NOTF
     __threadfence();
+#endif
     const unsigned target = (gen + 1) * G;
     asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
     while (ld_acquire(bar) < target) {
